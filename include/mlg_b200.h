@@ -1,0 +1,185 @@
+/*
+ * mlg_b200.h -- C ABI of the B200 correction-step library (libmlg_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference (arXiv 1401.4969,
+ * /root/reference/proj): one multilevel correction step -- subdomain residual
+ * solves, strip solve, coarse-space-augmented eigensolve -- plus the level
+ * build it triggers.  The reference has no FFI of its own; its boundary is the
+ * C++ API of include/mleig/corrector.hpp, and every entry point below names
+ * the reference function it replaces (file:line under /root/reference/proj).
+ *
+ * Conventions (mirroring the reference's data layout):
+ *   - all arrays are host memory, caller-allocated, 0-based, int32 indices,
+ *     float64 values (except the *_device entry points);
+ *   - "full" vectors have one entry per dof of the level (boundary included,
+ *     dof = iy*(nx+1)+ix, fespace.cpp:230-290); "interior" vectors follow
+ *     FeSpace::interior_dofs order (ascending dof id); several vectors are
+ *     stored one after another (vector-major);
+ *   - a context owns all device state (mesh hierarchy, operators, workspaces)
+ *     like Hierarchy owns its LevelSystems (corrector.hpp:63-95); one context
+ *     per host thread, calls are synchronous;
+ *   - return value 0 on success, otherwise the reference's exception class as
+ *     its CLI exit code (tools/mleig_main.cpp:57-66) -- 2 ConfigError,
+ *     3 SolverError, 4 IoError, 1 other -- or 5 for a CUDA error; the message
+ *     (same text as the reference's exception where one exists) is returned
+ *     by mlg_last_error() on the calling thread.
+ */
+#ifndef MLG_B200_H
+#define MLG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLG_OK 0
+#define MLG_ERR_OTHER 1
+#define MLG_ERR_CONFIG 2 /* mleig::ConfigError, errors.hpp:10-12 */
+#define MLG_ERR_SOLVER 3 /* mleig::SolverError, errors.hpp:15-17 */
+#define MLG_ERR_IO 4     /* mleig::IoError,     errors.hpp:20-22 */
+#define MLG_ERR_CUDA 5
+
+/* RunConfig (corrector.hpp:21-33). example: 0 = "laplace", 1 = "variable". */
+typedef struct mlg_config {
+  double x_min, x_max, y_min, y_max; /* DomainRect (mesh.hpp:22-27) */
+  double H;                          /* coarse mesh size */
+  double delta;                      /* requested overlap (rounded up to the lattice) */
+  int m;                             /* subdomain count (perfect square) */
+  int n_levels;
+  int degree; /* 1 (P2 is not on the B200 path: ConfigError) */
+  int nev;
+  int example;
+  int workers; /* accepted for parity; the GPU path has no worker threads */
+  double cg_tol;
+  int deterministic;
+} mlg_config;
+
+typedef struct mlg_ctx mlg_ctx;
+
+typedef struct mlg_level_info {
+  int64_t num_vertices, num_triangles, num_boundary_edges;
+  int64_t ndofs, n_interior, nnz; /* nnz of A (== nnz of M) */
+  int nx, ny, level;
+  double h_max;
+} mlg_level_info;
+
+/* SolveReport (sparse.hpp:103-107) */
+typedef struct mlg_solve_report {
+  int iterations;
+  double final_residual;
+  int converged;
+} mlg_solve_report;
+
+/* StepTimings (corrector.hpp:97-101) plus device-side evidence. */
+typedef struct mlg_step_timings {
+  double local_seconds, iface_seconds, aug_seconds; /* CUDA events, as StepTimings */
+  double build_seconds;                             /* extend_to + region data of the step */
+  int local_iterations_max, strip_iterations_max;
+  double spmv_kernel_ms;   /* summed device time of the local-solve SpMV kernel (profiling on) */
+  int64_t spmv_launches;   /* number of such launches */
+  double spmv_rows;        /* summed active rows over those launches */
+  int64_t kernel_launches; /* CG kernel launches of the step */
+} mlg_step_timings;
+
+const char* mlg_last_error(void);
+
+/* Hierarchy::Hierarchy (corrector.cpp:111-129): validate_config, coarse mesh,
+ * partition (decomp.cpp:24-86, delta rounded up corrector.cpp:117-121), level-0
+ * space and operators. */
+int mlg_create(const mlg_config* cfg, mlg_ctx** out);
+void mlg_destroy(mlg_ctx* ctx);
+
+/* Hierarchy::extend_to (corrector.cpp:131-146): refine_regular, register_level,
+ * build_space, assemble_form x2, prolongation_matrix -- on device. */
+int mlg_extend_to(mlg_ctx* ctx, int level);
+int mlg_max_level(mlg_ctx* ctx, int* level);
+int mlg_get_level_info(mlg_ctx* ctx, int level, mlg_level_info* out);
+
+/* Mesh arrays (mesh.hpp:32-50): vertices[nv][2], vertex_lattice[nv][2],
+ * triangles[nt][3], parent[nt] (level >= 1), boundary_edges[nb][2].  Any
+ * pointer may be NULL. */
+int mlg_export_mesh(mlg_ctx* ctx, int level, double* vertices, int* vertex_lattice,
+                    int* triangles, int* parent, int* boundary_edges);
+
+/* FeSpace (fespace.hpp:52-65): dof_lattice[ndofs][2] (half units),
+ * interior_dofs[n_interior], interior_index[ndofs], connectivity[nt][3]. */
+int mlg_export_space(mlg_ctx* ctx, int level, int* dof_lattice, int* interior_dofs,
+                     int* interior_index, int* connectivity3);
+
+/* SparseSymMatrix CSR of the full-space form (sparse.hpp:30-55); form 0 =
+ * stiffness (assemble_stiffness), 1 = mass (assemble_mass). */
+int mlg_export_csr(mlg_ctx* ctx, int level, int form, int* row_ptr, int* cols, double* values);
+
+/* Partition (decomp.hpp:59-93): rects[m][3][4] = block, overlap, inner as
+ * x0,y0,x1,y1 in coarse cells; info[5] = m, side, delta_cells, nx0, ny0. */
+int mlg_partition(mlg_ctx* ctx, int* rects, int* info);
+
+/* restrict_space (decomp.cpp:167-217); kind 0 domain, 1 block, 2 overlap,
+ * 3 inner, 4 strip.  out may be NULL to query the count. */
+int mlg_region_dofs(mlg_ctx* ctx, int level, int kind, int j, int zero_trace, int* out,
+                    int64_t* count);
+/* Partition::region_elements (decomp.cpp:148-165). */
+int mlg_region_elements(mlg_ctx* ctx, int level, int kind, int j, int* out, int64_t* count);
+
+/* SparseSymMatrix::multiply (sparse.cpp:69-76) on full vectors. */
+int mlg_spmv(mlg_ctx* ctx, int level, int form, const double* x_full, double* y_full);
+/* Hierarchy::prolong / restrict_transpose (corrector.cpp:158-170), full vectors. */
+int mlg_prolong(mlg_ctx* ctx, int from_level, int to_level, const double* x, double* y);
+int mlg_restrict_transpose(mlg_ctx* ctx, int from_level, int to_level, const double* x,
+                           double* y);
+
+/* coarse_eigensolve / solve_interior_eigenproblem (fespace.hpp:128-132,
+ * sparse.cpp:326-355): lambdas[nev], coeffs[nev][n_interior]. */
+int mlg_coarse_eigensolve(mlg_ctx* ctx, int level, int nev, double* lambdas, double* coeffs);
+
+/* local_bvp_solve (corrector.hpp:112-113, corrector.cpp:198-214). */
+int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const double* u_full,
+                        double cg_tol, double* e_full, mlg_solve_report* report);
+
+/* interface_solve (corrector.hpp:118-120, corrector.cpp:216-254);
+ * corrections[m][ndofs]. */
+int mlg_interface_solve(mlg_ctx* ctx, int level, double lambda, const double* u_full,
+                        const double* corrections, double cg_tol, double* glued_full,
+                        mlg_solve_report* report);
+
+/* augmented_eigensolve (corrector.hpp:127-128, corrector.cpp:256-334);
+ * glued[k_in][ndofs] (k_in <= 8); lambdas[nev], coeffs[nev][n_interior]. */
+int mlg_augmented_eigensolve(mlg_ctx* ctx, int level, int k_in, const double* glued_full,
+                             int nev, double* lambdas, double* coeffs);
+
+/* one_correction_step (corrector.hpp:135-136, corrector.cpp:336-412).
+ * coeffs_in[nev][n_interior(from)], coeffs_out[nev][n_interior(to)];
+ * matched = CorrectionState::matched_previous.  nev <= 8. */
+int mlg_correction_step(mlg_ctx* ctx, int from_level, int to_level, int nev,
+                        const double* lambdas_in, const double* coeffs_in, double* lambdas_out,
+                        double* coeffs_out, int* matched, mlg_step_timings* timings);
+
+/* Same, with coefficient arrays resident in device memory (same layout). */
+int mlg_correction_step_device(mlg_ctx* ctx, int from_level, int to_level, int nev,
+                               const double* lambdas_in, const double* d_coeffs_in,
+                               double* lambdas_out, double* d_coeffs_out, int* matched,
+                               mlg_step_timings* timings);
+
+/* multilevel_correction (corrector.cpp:414-462) up to last_level (<= 0: the
+ * config's n_levels): lambdas[last_level][nev] (row k-1 = level k), matched
+ * and timings per level (may be NULL); final coefficients to host and/or
+ * device arrays [nev][n_interior(last)] (either may be NULL). */
+int mlg_multilevel_correction(mlg_ctx* ctx, int last_level, double* lambdas,
+                              double* final_coeffs, double* d_final_coeffs, int* matched,
+                              mlg_step_timings* timings);
+
+/* Record CUDA events around every local-solve SpMV launch (roofline evidence). */
+int mlg_set_profiling(mlg_ctx* ctx, int on);
+
+/* Interior-stiffness SpMV microbenchmark (extract_submatrix(A, interior) x):
+ * average device ms per launch over `reps` launches, and its algorithmic bytes. */
+int mlg_bench_spmv(mlg_ctx* ctx, int level, int reps, double* ms_per_launch,
+                   double* bytes_per_launch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MLG_B200_H */

@@ -426,6 +426,16 @@ int ref_cg_solve_csr(int n, const int* row_ptr, const int* cols, const double* v
   });
 }
 
+// FNV-1a-64 over raw bytes, chained from h (SURVEY.md Appendix B digests).
+unsigned long long ref_fnv1a64(const unsigned char* p, unsigned long long n,
+                               unsigned long long h) {
+  for (unsigned long long i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
 // a, b column-major n x n; vecs n x nev column-major.
 int ref_dense_gen_eigensolve(int n, const double* a, const double* b, int nev, double* lambdas,
                              double* vecs) {

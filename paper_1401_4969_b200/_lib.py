@@ -1,0 +1,139 @@
+"""ctypes binding of libmlg_b200.so (the C ABI in include/mlg_b200.h).
+
+There is no fallback: if the shared library is missing or cannot be loaded the
+import-time call `lib()` raises, and every API entry point fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libmlg_b200.so"
+
+c_int_p = C.POINTER(C.c_int)
+c_double_p = C.POINTER(C.c_double)
+c_int64_p = C.POINTER(C.c_int64)
+
+
+class MlgError(RuntimeError):
+    code = 1
+
+
+class ConfigError(MlgError):  # mleig::ConfigError (errors.hpp:10-12), exit code 2
+    code = 2
+
+
+class SolverError(MlgError):  # mleig::SolverError (errors.hpp:15-17), exit code 3
+    code = 3
+
+
+class IoError(MlgError):  # mleig::IoError (errors.hpp:20-22), exit code 4
+    code = 4
+
+
+class CudaError(MlgError):
+    code = 5
+
+
+_ERRORS = {1: MlgError, 2: ConfigError, 3: SolverError, 4: IoError, 5: CudaError}
+
+
+class MlgConfig(C.Structure):
+    _fields_ = [
+        ("x_min", C.c_double), ("x_max", C.c_double),
+        ("y_min", C.c_double), ("y_max", C.c_double),
+        ("H", C.c_double), ("delta", C.c_double),
+        ("m", C.c_int), ("n_levels", C.c_int), ("degree", C.c_int),
+        ("nev", C.c_int), ("example", C.c_int), ("workers", C.c_int),
+        ("cg_tol", C.c_double), ("deterministic", C.c_int),
+    ]
+
+
+class MlgLevelInfo(C.Structure):
+    _fields_ = [
+        ("num_vertices", C.c_int64), ("num_triangles", C.c_int64),
+        ("num_boundary_edges", C.c_int64), ("ndofs", C.c_int64),
+        ("n_interior", C.c_int64), ("nnz", C.c_int64),
+        ("nx", C.c_int), ("ny", C.c_int), ("level", C.c_int), ("h_max", C.c_double),
+    ]
+
+
+class MlgSolveReport(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("final_residual", C.c_double),
+                ("converged", C.c_int)]
+
+
+class MlgStepTimings(C.Structure):
+    _fields_ = [
+        ("local_seconds", C.c_double), ("iface_seconds", C.c_double),
+        ("aug_seconds", C.c_double), ("build_seconds", C.c_double),
+        ("local_iterations_max", C.c_int), ("strip_iterations_max", C.c_int),
+        ("spmv_kernel_ms", C.c_double), ("spmv_launches", C.c_int64),
+        ("spmv_rows", C.c_double), ("kernel_launches", C.c_int64),
+    ]
+
+
+# name -> argtypes (every symbol declared in include/mlg_b200.h)
+SIGNATURES = {
+    "mlg_last_error": [],
+    "mlg_create": [C.POINTER(MlgConfig), C.POINTER(C.c_void_p)],
+    "mlg_destroy": [C.c_void_p],
+    "mlg_extend_to": [C.c_void_p, C.c_int],
+    "mlg_max_level": [C.c_void_p, c_int_p],
+    "mlg_get_level_info": [C.c_void_p, C.c_int, C.POINTER(MlgLevelInfo)],
+    "mlg_export_mesh": [C.c_void_p, C.c_int, c_double_p, c_int_p, c_int_p, c_int_p, c_int_p],
+    "mlg_export_space": [C.c_void_p, C.c_int, c_int_p, c_int_p, c_int_p, c_int_p],
+    "mlg_export_csr": [C.c_void_p, C.c_int, C.c_int, c_int_p, c_int_p, c_double_p],
+    "mlg_partition": [C.c_void_p, c_int_p, c_int_p],
+    "mlg_region_dofs": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, c_int_p, c_int64_p],
+    "mlg_region_elements": [C.c_void_p, C.c_int, C.c_int, C.c_int, c_int_p, c_int64_p],
+    "mlg_spmv": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
+    "mlg_prolong": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
+    "mlg_restrict_transpose": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
+    "mlg_coarse_eigensolve": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
+    "mlg_local_bvp_solve": [C.c_void_p, C.c_int, C.c_int, C.c_double, c_double_p, C.c_double,
+                            c_double_p, C.POINTER(MlgSolveReport)],
+    "mlg_interface_solve": [C.c_void_p, C.c_int, C.c_double, c_double_p, c_double_p,
+                            C.c_double, c_double_p, C.POINTER(MlgSolveReport)],
+    "mlg_augmented_eigensolve": [C.c_void_p, C.c_int, C.c_int, c_double_p, C.c_int,
+                                 c_double_p, c_double_p],
+    "mlg_correction_step": [C.c_void_p, C.c_int, C.c_int, C.c_int, c_double_p, c_double_p,
+                            c_double_p, c_double_p, c_int_p, C.POINTER(MlgStepTimings)],
+    "mlg_correction_step_device": [C.c_void_p, C.c_int, C.c_int, C.c_int, c_double_p,
+                                   C.c_void_p, c_double_p, C.c_void_p, c_int_p,
+                                   C.POINTER(MlgStepTimings)],
+    "mlg_multilevel_correction": [C.c_void_p, C.c_int, c_double_p, c_double_p, C.c_void_p,
+                                  c_int_p, C.POINTER(MlgStepTimings)],
+    "mlg_set_profiling": [C.c_void_p, C.c_int],
+    "mlg_bench_spmv": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
+}
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    """Load the CUDA library; raise if it is absent (no CPU fallback exists)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                    "(the B200 path has no CPU fallback)")
+            h = C.CDLL(str(LIB_PATH))
+            for name, args in SIGNATURES.items():
+                fn = getattr(h, name)
+                fn.argtypes = args
+                fn.restype = C.c_int
+            h.mlg_last_error.restype = C.c_char_p
+            h.mlg_destroy.restype = None
+            _lib = h
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().mlg_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, MlgError)(msg)

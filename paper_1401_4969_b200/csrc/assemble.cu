@@ -1,0 +1,269 @@
+// Level build, floating-point part: P1 stiffness and mass assembly, bit-exact
+// with the reference's element-order triplet accumulation.
+//
+//   local_matrix / element_geometry  fespace.cpp:169-217 (3-point edge-midpoint
+//                                    rule, quad_degree2 fespace.cpp:41-47)
+//   assemble_form                    fespace.cpp:314-341
+//   SparseSymMatrix::from_upper_triplets  sparse.cpp:24-61 (stable (row,col)
+//                                    sort => duplicates summed from 0.0 in
+//                                    ascending element id; mirrored bitwise)
+//
+// B200 design (row gather, no sort): entry (r,c) of the global matrix is the
+// sum, over the <=6 triangles that contain both dofs, of local[i][j] in
+// ascending element id.  Every triangle of the structured lattice is found
+// through the per-level slot table `geo` (cell, L/U) -> (elem<<2 | rotation)
+// that refinement writes, so one thread per dof gathers its <=6 triangles,
+// recomputes their element matrices with the reference's exact operation
+// sequence (unfused __d*_rn), sorts the contributions by element id and sums
+// them.  Output is the 4-entry upper stencil {C,E,N,NE} of A and M per dof
+// (64 B/dof written, coalesced); CSR export is a second closed-form pass.
+#include <algorithm>
+
+#include "ctx.cuh"
+
+namespace mlg {
+namespace {
+
+constexpr int kBlock = 256;
+
+struct Contrib {
+  unsigned e;
+  double a, m;
+};
+
+// Element-local entries (i<=j) of the P1 Laplace stiffness and unit mass for
+// a triangle with vertices v0,v1,v2 in element order (fespace.cpp:169-217).
+__device__ __forceinline__ void local_entry(double v0x, double v0y, double v1x, double v1y,
+                                            double v2x, double v2y, int i, int j, double* a_out,
+                                            double* m_out) {
+  const double area2 = xsub(xmul(xsub(v1x, v0x), xsub(v2y, v0y)),
+                            xmul(xsub(v2x, v0x), xsub(v1y, v0y)));
+  const double area = xmul(0.5, area2);
+  double g[3][2];
+  g[0][0] = xdiv(xsub(v1y, v2y), area2);
+  g[0][1] = xdiv(xsub(v2x, v1x), area2);
+  g[1][0] = xdiv(xsub(v2y, v0y), area2);
+  g[1][1] = xdiv(xsub(v0x, v2x), area2);
+  g[2][0] = xdiv(xsub(v0y, v1y), area2);
+  g[2][1] = xdiv(xsub(v1x, v0x), area2);
+  const double w = xmul(1.0 / 3.0, area);  // rule.weights[q] * g.area, same for all q
+  // stiffness with A = I (CoefficientField::laplace, fespace.cpp:105-112)
+  const double agx = xadd(xmul(1.0, g[i][0]), xmul(0.0, g[i][1]));
+  const double agy = xadd(xmul(0.0, g[i][0]), xmul(1.0, g[i][1]));
+  const double s = xmul(w, xadd(xmul(agx, g[j][0]), xmul(agy, g[j][1])));
+  double a = 0.0;
+  a = xadd(a, s);
+  a = xadd(a, s);
+  a = xadd(a, s);
+  // mass with phi = 1: points {.5,.5,0},{0,.5,.5},{.5,0,.5}
+  const double P[3][3] = {{0.5, 0.5, 0.0}, {0.0, 0.5, 0.5}, {0.5, 0.0, 0.5}};
+  double m = 0.0;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) m = xadd(m, xmul(xmul(xmul(w, 1.0), P[q][i]), P[q][j]));
+  *a_out = a;
+  *m_out = m;
+}
+
+struct LevelGeom {
+  int nx, ny;
+  double x0, y0, dx, dy;
+  const unsigned* geo;
+};
+
+// Canonical vertex k of the L/U triangle of cell (cx,cy):
+//   L: (cx,cy), (cx+1,cy), (cx+1,cy+1)     U: (cx,cy), (cx+1,cy+1), (cx,cy+1)
+__device__ __forceinline__ void canon_vertex(int cx, int cy, int upper, int k, int* x, int* y) {
+  if (k == 0) {
+    *x = cx;
+    *y = cy;
+  } else if (k == 1) {
+    *x = cx + 1;
+    *y = cy + (upper ? 1 : 0);
+  } else {
+    *x = cx + (upper ? 0 : 1);
+    *y = cy + 1;
+  }
+}
+
+// Contribution of triangle (cell, upper) to the pair of canonical vertices
+// (kd, kn) (kd == kn for a diagonal entry).
+__device__ __forceinline__ bool contribution(const LevelGeom& G, int cx, int cy, int upper,
+                                             int kd, int kn, Contrib* out) {
+  if (cx < 0 || cy < 0 || cx >= G.nx || cy >= G.ny) return false;
+  const unsigned code = G.geo[2 * (static_cast<std::int64_t>(cy) * G.nx + cx) + upper];
+  const int rot = static_cast<int>(code & 3u);
+  double vx[3], vy[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    int lx, ly;
+    canon_vertex(cx, cy, upper, (rot + j) % 3, &lx, &ly);
+    vx[j] = lattice_coord(G.x0, lx, G.dx);
+    vy[j] = lattice_coord(G.y0, ly, G.dy);
+  }
+  const int ld = (kd - rot + 3) % 3, ln = (kn - rot + 3) % 3;
+  local_entry(vx[0], vy[0], vx[1], vy[1], vx[2], vy[2], min(ld, ln), max(ld, ln), &out->a,
+              &out->m);
+  out->e = code >> 2;
+  return true;
+}
+
+// Sum in ascending element id, from 0.0 (sparse.cpp:36-46).
+template <int N>
+__device__ __forceinline__ void ordered_sum(Contrib* c, int n, double* a, double* m) {
+  for (int i = 1; i < n; ++i) {  // insertion sort, n <= 6
+    Contrib t = c[i];
+    int k = i;
+    while (k > 0 && c[k - 1].e > t.e) {
+      c[k] = c[k - 1];
+      --k;
+    }
+    c[k] = t;
+  }
+  double sa = 0.0, sm = 0.0;
+  for (int i = 0; i < n; ++i) {
+    sa = xadd(sa, c[i].a);
+    sm = xadd(sm, c[i].m);
+  }
+  *a = sa;
+  *m = sm;
+}
+
+__global__ void __launch_bounds__(kBlock) k_assemble(LevelGeom G, Stencil* stA, Stencil* stM,
+                                                     double* dinv) {
+  const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t nd = static_cast<std::int64_t>(G.nx + 1) * (G.ny + 1);
+  if (d >= nd) return;
+  const int ix = static_cast<int>(d % (G.nx + 1)), iy = static_cast<int>(d / (G.nx + 1));
+  Contrib c[6];
+  int n;
+  Stencil A{0.0, 0.0, 0.0, 0.0}, M{0.0, 0.0, 0.0, 0.0};
+  // diagonal: the six triangles around (ix,iy) with the dof's canonical index
+  n = 0;
+  n += contribution(G, ix, iy, 0, 0, 0, c + n);
+  n += contribution(G, ix, iy, 1, 0, 0, c + n);
+  n += contribution(G, ix - 1, iy, 0, 1, 1, c + n);
+  n += contribution(G, ix, iy - 1, 1, 2, 2, c + n);
+  n += contribution(G, ix - 1, iy - 1, 0, 2, 2, c + n);
+  n += contribution(G, ix - 1, iy - 1, 1, 1, 1, c + n);
+  ordered_sum<6>(c, n, &A.c, &M.c);
+  if (ix < G.nx) {  // E: L(ix,iy) (0,1), U(ix,iy-1) (2,1)
+    n = 0;
+    n += contribution(G, ix, iy, 0, 0, 1, c + n);
+    n += contribution(G, ix, iy - 1, 1, 2, 1, c + n);
+    ordered_sum<2>(c, n, &A.e, &M.e);
+  }
+  if (iy < G.ny) {  // N: U(ix,iy) (0,2), L(ix-1,iy) (1,2)
+    n = 0;
+    n += contribution(G, ix, iy, 1, 0, 2, c + n);
+    n += contribution(G, ix - 1, iy, 0, 1, 2, c + n);
+    ordered_sum<2>(c, n, &A.n, &M.n);
+  }
+  if (ix < G.nx && iy < G.ny) {  // NE: L(ix,iy) (0,2), U(ix,iy) (0,1)
+    n = 0;
+    n += contribution(G, ix, iy, 0, 0, 2, c + n);
+    n += contribution(G, ix, iy, 1, 0, 1, c + n);
+    ordered_sum<2>(c, n, &A.ne, &M.ne);
+  }
+  stA[d] = A;
+  stM[d] = M;
+  dinv[d] = 1.0 / A.c;  // JacobiPreconditioner: inv_diag = 1.0 / coeff(r,r)
+}
+
+// row_ptr of the full 7-point pattern in closed form.
+__device__ __forceinline__ long long row_start(int ix, int iy, int nx, int ny) {
+  const long long r = static_cast<long long>(iy) * (3LL * nx + 1) +
+                      (2LL * nx + 1) * (max(iy - 1, 0) + min(iy, ny));
+  const long long w = ix + max(ix - 1, 0) + ix + (iy > 0 ? ix + max(ix - 1, 0) : 0) +
+                      (iy < ny ? 2LL * ix : 0);
+  return r + w;
+}
+
+__global__ void k_export_csr(int nx, int ny, long long nnz, const Stencil* st, int* row_ptr,
+                             int* cols, double* vals) {
+  const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t nd = static_cast<std::int64_t>(nx + 1) * (ny + 1);
+  if (d > nd) return;
+  if (d == nd) {
+    if (row_ptr) row_ptr[nd] = static_cast<int>(nnz);
+    return;
+  }
+  const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
+  long long k = row_start(ix, iy, nx, ny);
+  if (row_ptr) row_ptr[d] = static_cast<int>(k);
+  const std::int64_t s = nx + 1;
+  auto put = [&](std::int64_t col, double v) {
+    if (cols) cols[k] = static_cast<int>(col);
+    if (vals) vals[k] = v;
+    ++k;
+  };
+  if (iy > 0 && ix > 0) put(d - s - 1, st[d - s - 1].ne);
+  if (iy > 0) put(d - s, st[d - s].n);
+  if (ix > 0) put(d - 1, st[d - 1].e);
+  put(d, st[d].c);
+  if (ix < nx) put(d + 1, st[d].e);
+  if (iy < ny) put(d + s, st[d].n);
+  if (iy < ny && ix < nx) put(d + s + 1, st[d].ne);
+}
+
+// to_dense(extract_submatrix(a, interior_dofs)) (sparse.cpp:156-184),
+// column-major n x n with n = (nx-1)(ny-1); entries mirror bitwise.
+__global__ void k_interior_dense(int nx, int ny, const Stencil* st, double* dense) {
+  const std::int64_t k = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const int w = nx - 1, h = ny - 1;
+  const std::int64_t n = static_cast<std::int64_t>(w) * h;
+  if (k >= n) return;
+  const int i = static_cast<int>(k % w), j = static_cast<int>(k / w);
+  const std::int64_t d = static_cast<std::int64_t>(j + 1) * (nx + 1) + (i + 1);
+  const std::int64_t s = nx + 1;
+  auto put = [&](std::int64_t col_k, double v) { dense[col_k * n + k] = v; };
+  if (j > 0 && i > 0) put(k - w - 1, st[d - s - 1].ne);
+  if (j > 0) put(k - w, st[d - s].n);
+  if (i > 0) put(k - 1, st[d - 1].e);
+  put(k, st[d].c);
+  if (i < w - 1) put(k + 1, st[d].e);
+  if (j < h - 1) put(k + w, st[d].n);
+  if (j < h - 1 && i < w - 1) put(k + w + 1, st[d].ne);
+}
+
+}  // namespace
+
+std::int64_t csr_nnz(const Level& L) {
+  const std::int64_t n = L.nx, m = L.ny;
+  // sum over rows: (3nx+1)(ny+1) + (2nx+1)*2ny
+  return (3 * n + 1) * (m + 1) + (2 * n + 1) * 2 * m;
+}
+
+void assemble_level(Ctx& c, Level& L) {
+  const std::int64_t nd = L.ndofs();
+  L.stA.alloc(nd);
+  L.stM.alloc(nd);
+  L.dinv.alloc(nd);
+  LevelGeom G{L.nx, L.ny, c.cfg.x_min, c.cfg.y_min, L.dx, L.dy, L.geo.get()};
+  k_assemble<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
+                                                            L.dinv.get());
+  MLG_LAUNCH_CHECK();
+}
+
+void export_csr(Ctx& c, const Level& L, int form, int* row_ptr, int* cols, double* vals) {
+  const std::int64_t nd = L.ndofs(), nnz = csr_nnz(L);
+  DevBuf<int> rp(row_ptr ? nd + 1 : 0), cl(cols ? nnz : 0);
+  DevBuf<double> vl(vals ? nnz : 0);
+  k_export_csr<<<grid_for(nd + 1, kBlock), kBlock, 0, c.stream>>>(
+      L.nx, L.ny, nnz, form == 0 ? L.stA.get() : L.stM.get(), row_ptr ? rp.get() : nullptr,
+      cols ? cl.get() : nullptr, vals ? vl.get() : nullptr);
+  MLG_LAUNCH_CHECK();
+  if (row_ptr) rp.download(row_ptr, nd + 1, c.stream);
+  if (cols) cl.download(cols, nnz, c.stream);
+  if (vals) vl.download(vals, nnz, c.stream);
+  c.sync();
+}
+
+void interior_dense(Ctx& c, const Level& L, int form, double* d_dense) {
+  const std::int64_t n = L.nint();
+  MLG_CUDA(cudaMemsetAsync(d_dense, 0, sizeof(double) * n * n, c.stream));
+  k_interior_dense<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(
+      L.nx, L.ny, form == 0 ? L.stA.get() : L.stM.get(), d_dense);
+  MLG_LAUNCH_CHECK();
+}
+
+}  // namespace mlg

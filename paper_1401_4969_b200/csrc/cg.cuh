@@ -1,0 +1,79 @@
+// Batched Jacobi-PCG over many lattice-window systems at once (the local
+// Dirichlet solves of all subdomains x eigenvectors, or the strip solve).
+// Semantics are the reference's cg_solve (sparse.cpp:199-258), per system and
+// per right-hand side: x0 = 0; zero rhs returns after 0 iterations; stop when
+// ||r|| <= tol ||b|| *confirmed by the true residual* (else restart from it);
+// maxit = 10 n; p'Ap <= 0 is an error; non-convergence is reported.
+#pragma once
+
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace mlg {
+
+// A system is a rectangular window [x0, x0+w) x [y0, y0+h) of the fine
+// full lattice (interior dofs only) optionally restricted by a byte mask; its
+// matrix is the window (mask) restriction of the level's stiffness, exactly
+// extract_submatrix (sparse.cpp:156-174).  Vectors are window-compact,
+// row-major, NR right-hand sides interleaved.
+struct CgSys {
+  int x0, y0, w, h;
+  long long voff;  // first row in the pooled vectors
+  int toff;        // first tile id (partials index)
+  int ntiles;
+  int nrows;
+  int maxit;
+};
+
+struct CgTile {
+  int sys;
+  int t;
+};
+
+struct CgCtl {
+  double alpha, beta, rho, bnorm, final_res;
+  int mode_a, mode_b, iters, status, restart, pad;
+};
+
+enum : int { kModeSkip = 0, kModeNormal = 1, kModeCheck = 2 };
+enum : int { kRunning = 0, kConverged = 1, kNotConverged = 2, kIndefinite = 3 };
+
+struct CgResult {
+  std::vector<SolveReport> reports;  // [sys * nr + rhs]
+  int iters_max = 0;
+};
+
+class CgBatch {
+ public:
+  // rows per tile = kCgBlock * kCgRowsPerThread
+  static constexpr int kBlock = 256;
+  static constexpr int kRowsPerThread = 8;
+  static constexpr int kTile = kBlock * kRowsPerThread;
+
+  // Lays out systems (computing voff/toff/ntiles) and sizes the pools.
+  void setup(Ctx& c, const Level& L, std::vector<CgSys> systems, int nr,
+             const unsigned char* mask, const double* bsrc);
+  // Runs to completion; throws SolverError for p'Ap <= 0.
+  CgResult solve(Ctx& c, double tol, int maxit_override = 0);
+
+  const double* x() const { return X.get(); }
+  double* x_mut() { return X.get(); }
+  const std::vector<CgSys>& systems() const { return sys_h; }
+  const CgSys* sys_dev() const { return sys_d.get(); }
+  int nr = 1;
+
+ private:
+  const Level* L = nullptr;
+  const unsigned char* mask = nullptr;
+  const double* bsrc = nullptr;
+  std::vector<CgSys> sys_h;
+  long long total_rows = 0;
+  int total_tiles = 0;
+  DevBuf<CgSys> sys_d;
+  DevBuf<CgTile> tiles_d;
+  DevBuf<CgCtl> ctl_d;
+  DevBuf<double> X, R, P0, P1, Q, partA, partB;
+};
+
+}  // namespace mlg

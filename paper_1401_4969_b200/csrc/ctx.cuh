@@ -1,0 +1,145 @@
+// Host-side data model of the B200 path.  Mirrors the reference's ownership
+// (corrector.hpp:47-95): a Hierarchy owns the coarse level, the partition and
+// every refinement built so far; each level owns its mesh, space and operators.
+// Here all per-level arrays live in HBM and the host keeps only sizes and the
+// (tiny) partition rectangles.
+//
+// HBM layout (full lattice = the reference's DOF numbering, fespace.cpp:230-290:
+// dof = iy*(nx+1)+ix on the P1 lattice of a rectangle):
+//   tri[nt][3] int32, lat[nv][2] int32, xy[nv][2] f64, parent[nt] int32,
+//   bedges[nb][2] int32                         -- Mesh (mesh.hpp:32-50), bit-exact
+//   vid[(nx+1)(ny+1)] int32   lattice point -> vertex id (history dependent)
+//   geo[2*nx*ny] uint32       geometric triangle (cell, lower/upper) -> (elem<<2)|rot
+//   stA[ndofs], stM[ndofs]    Stencil{c,e,n,ne}: the upper half of the symmetric
+//                             7-point rows of A and M (W/S/SW are the mirrored
+//                             E/N/NE of the neighbour rows, sparse.cpp:36-46)
+//   dinv[ndofs] f64           1/A_ii (JacobiPreconditioner, sparse.cpp:186-193)
+// Vectors are full-lattice, rhs-interleaved: v[dof*NR + r], boundary rows 0.
+#pragma once
+
+#include <cusolverDn.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mlg {
+
+struct alignas(32) Stencil {
+  double c, e, n, ne;
+};
+
+struct Config {
+  double x_min = -1.0, x_max = 1.0, y_min = -1.0, y_max = 1.0;
+  double H = 0.25;
+  double delta = 0.1;
+  int m = 4;
+  int n_levels = 5;
+  int degree = 1;
+  int nev = 5;
+  int example = 0;  // 0 laplace (1 variable: not on this path)
+  int workers = 1;
+  double cg_tol = 1e-10;
+  int deterministic = 1;
+};
+
+struct IRect {
+  int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+};
+
+// decomp.hpp:59-93 / decomp.cpp:24-86.
+struct Partition {
+  int m = 0, side = 0, delta_cells = 0, nx0 = 0, ny0 = 0;
+  double cell_h = 0.0;
+  std::vector<IRect> blocks, overlaps, inners;
+  // Level-0 element sets (decomp.cpp:101-121); finer levels are the
+  // contiguous descendant ranges [t*4^L, (t+1)*4^L) (children are 4t+c).
+  std::vector<std::vector<int>> block_elems, overlap_elems, inner_elems;
+  std::vector<int> strip_elems;
+};
+
+struct Level {
+  int level = 0, nx = 0, ny = 0;
+  double dx = 0.0, dy = 0.0;
+  std::int64_t nv = 0, nt = 0, nb = 0;
+  double h_max = 0.0;
+  DevBuf<int> tri, lat, parent, bedges, vid;
+  DevBuf<double> xy;
+  DevBuf<unsigned> geo;
+  DevBuf<Stencil> stA, stM;
+  DevBuf<double> dinv;
+  DevBuf<unsigned char> strip_mask;  // built lazily (1 = interior dof of the strip)
+
+  std::int64_t ndofs() const { return static_cast<std::int64_t>(nx + 1) * (ny + 1); }
+  std::int64_t nint() const { return static_cast<std::int64_t>(nx - 1) * (ny - 1); }
+};
+
+struct StepTimes {
+  double local_s = 0, iface_s = 0, aug_s = 0, build_s = 0;
+  int local_iters_max = 0, strip_iters_max = 0;
+  double ka_ms_sum = 0;  // summed device time of the local-solve SpMV kernel
+  int ka_launches = 0;
+  double ka_rows = 0;    // summed active rows over those launches
+  int kernel_launches = 0;
+};
+
+struct SolveReport {
+  int iterations = 0;
+  double final_residual = 0.0;
+  int converged = 0;
+};
+
+class Ctx;
+
+// ---- mesh.cu -------------------------------------------------------------
+void build_level0(Ctx& c);
+void refine_level(Ctx& c, const Level& coarse, Level& fine);
+void export_mesh(Ctx& c, const Level& L, double* xy, int* lat, int* tri, int* parent,
+                 int* bedges);
+void export_space(Ctx& c, const Level& L, int* dof_lattice, int* interior_dofs,
+                  int* interior_index, int* conn3);
+
+// ---- assemble.cu ---------------------------------------------------------
+void assemble_level(Ctx& c, Level& L);
+void export_csr(Ctx& c, const Level& L, int form, int* row_ptr, int* cols, double* vals);
+std::int64_t csr_nnz(const Level& L);
+void interior_dense(Ctx& c, const Level& L, int form, double* d_dense);
+
+class Ctx {
+ public:
+  explicit Ctx(const Config& cfg);
+  ~Ctx();
+  Config cfg;
+  Partition part;
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  std::vector<std::unique_ptr<Level>> levels;
+  int max_level() const { return static_cast<int>(levels.size()) - 1; }
+  Level& level(int k) {
+    if (k < 0 || k > max_level())
+      throw ConfigError("level " + std::to_string(k) + " not built");
+    return *levels[k];
+  }
+  void extend_to(int level);
+  void sync() { MLG_CUDA(cudaStreamSynchronize(stream)); }
+
+  // Coarse dense interior blocks (corrector.cpp:172-181), cached.
+  DevBuf<double> coarse_a, coarse_b, coarse_bchol;
+  int mc = 0;
+  bool coarse_ready = false;
+  void ensure_coarse_dense();
+
+  // Scratch (grow-only) owned by the context.
+  DevBuf<unsigned char> scratch;
+  void* scratch_bytes(std::size_t n) {
+    scratch.ensure(n);
+    return scratch.get();
+  }
+  std::shared_ptr<void> ws;  // corrector.cu Workspace (CG pools, step vectors)
+  bool profile = false;  // record CUDA events around the local-solve SpMV kernel
+  StepTimes times;
+};
+
+}  // namespace mlg
