@@ -54,6 +54,7 @@ typedef struct mlg_config {
   int workers; /* accepted for parity; the GPU path has no worker threads */
   double cg_tol;
   int deterministic;
+  int device; /* CUDA device ordinal of the context (B200-specific) */
 } mlg_config;
 
 typedef struct mlg_ctx mlg_ctx;
@@ -81,6 +82,8 @@ typedef struct mlg_step_timings {
   int64_t spmv_launches;   /* number of such launches */
   double spmv_rows;        /* summed active rows over those launches */
   int64_t kernel_launches; /* CG kernel launches of the step */
+  double step_seconds;     /* CUDA events on the context stream around the whole call,
+                              host<->device copies included for the host-array variant */
 } mlg_step_timings;
 
 const char* mlg_last_error(void);

@@ -46,7 +46,7 @@ class MlgConfig(C.Structure):
         ("H", C.c_double), ("delta", C.c_double),
         ("m", C.c_int), ("n_levels", C.c_int), ("degree", C.c_int),
         ("nev", C.c_int), ("example", C.c_int), ("workers", C.c_int),
-        ("cg_tol", C.c_double), ("deterministic", C.c_int),
+        ("cg_tol", C.c_double), ("deterministic", C.c_int), ("device", C.c_int),
     ]
 
 
@@ -71,6 +71,7 @@ class MlgStepTimings(C.Structure):
         ("local_iterations_max", C.c_int), ("strip_iterations_max", C.c_int),
         ("spmv_kernel_ms", C.c_double), ("spmv_launches", C.c_int64),
         ("spmv_rows", C.c_double), ("kernel_launches", C.c_int64),
+        ("step_seconds", C.c_double),
     ]
 
 

@@ -52,13 +52,14 @@ class RunConfig:  # corrector.hpp:21-33
     cg_tol: float = 1e-10
     workers: int = 1
     deterministic: bool = True
+    device: int = 0  # CUDA device of the context (B200-specific)
 
     def to_c(self) -> MlgConfig:
         ex = {"laplace": 0, "variable": 1}.get(self.example, -1)
         return MlgConfig(self.domain.x_min, self.domain.x_max, self.domain.y_min,
                          self.domain.y_max, self.H, self.delta, self.m, self.n_levels,
                          self.degree, self.nev, ex, self.workers, self.cg_tol,
-                         int(self.deterministic))
+                         int(self.deterministic), self.device)
 
 
 @dataclass
@@ -80,12 +81,13 @@ class StepTimings:  # corrector.hpp:97-101 (+ device evidence)
     spmv_launches: int = 0
     spmv_rows: float = 0.0
     kernel_launches: int = 0
+    step_seconds: float = 0.0
 
     @classmethod
     def from_c(cls, t: MlgStepTimings) -> "StepTimings":
         return cls(t.local_seconds, t.iface_seconds, t.aug_seconds, t.build_seconds,
                    t.local_iterations_max, t.strip_iterations_max, t.spmv_kernel_ms,
-                   t.spmv_launches, t.spmv_rows, t.kernel_launches)
+                   t.spmv_launches, t.spmv_rows, t.kernel_launches, t.step_seconds)
 
 
 @dataclass
@@ -340,6 +342,47 @@ def one_correction_step(hy: Hierarchy, state: CorrectionState, to_level: int):
                                     C.byref(t)))
     pairs = [EigenPair(float(lam_out[i]), cout[i].copy(), to_level) for i in range(nev)]
     return CorrectionState(to_level, pairs, bool(matched.value)), StepTimings.from_c(t)
+
+
+def one_correction_step_raw(hy: Hierarchy, from_level: int, to_level: int, lambdas_in,
+                            coeffs_in: np.ndarray, coeffs_out: np.ndarray):
+    """one_correction_step on caller-owned (e.g. pinned) host arrays, no copies on
+    the Python side: coeffs_in (nev, n_int(from)), coeffs_out (nev, n_int(to))."""
+    lam_in = _f64(lambdas_in)
+    nev = len(lam_in)
+    lam_out = np.empty(nev, np.float64)
+    matched = C.c_int()
+    t = MlgStepTimings()
+    check(lib().mlg_correction_step(hy.handle, from_level, to_level, nev, _dp(lam_in),
+                                    _dp(coeffs_in), _dp(lam_out), _dp(coeffs_out),
+                                    C.byref(matched), C.byref(t)))
+    return lam_out, bool(matched.value), StepTimings.from_c(t)
+
+
+def one_correction_step_device(hy: Hierarchy, from_level: int, to_level: int, lambdas_in,
+                               d_coeffs_in: int, d_coeffs_out: int):
+    """Same on device-resident coefficient arrays (raw CUDA pointers)."""
+    lam_in = _f64(lambdas_in)
+    nev = len(lam_in)
+    lam_out = np.empty(nev, np.float64)
+    matched = C.c_int()
+    t = MlgStepTimings()
+    check(lib().mlg_correction_step_device(hy.handle, from_level, to_level, nev, _dp(lam_in),
+                                           C.c_void_p(d_coeffs_in), _dp(lam_out),
+                                           C.c_void_p(d_coeffs_out), C.byref(matched),
+                                           C.byref(t)))
+    return lam_out, bool(matched.value), StepTimings.from_c(t)
+
+
+def multilevel_correction_device(hy: Hierarchy, last_level: int, d_final_coeffs: int):
+    """multilevel_correction up to last_level leaving the final coefficients in
+    device memory (raw pointer, (nev, n_int(last))); returns lambdas per level."""
+    nev = hy.config.nev
+    lam = np.empty((last_level, nev), np.float64)
+    hy.extend_to(last_level)
+    check(lib().mlg_multilevel_correction(hy.handle, last_level, _dp(lam), None,
+                                          C.c_void_p(d_final_coeffs), None, None))
+    return lam
 
 
 def multilevel_correction(hy: Hierarchy, last_level: int = 0):

@@ -45,6 +45,7 @@ int guarded(F&& f) {
 
 mlg::Ctx& C(mlg_ctx* x) {
   if (!x || !x->c) throw mlg::ConfigError("null context");
+  MLG_CUDA(cudaSetDevice(x->c->cfg.device));  // one context per device, any host thread
   return *x->c;
 }
 
@@ -59,7 +60,7 @@ void fill_timings(mlg_step_timings* t, const mlg::StepTimes& s, const mlg::Ctx& 
   t->spmv_kernel_ms = c.times.ka_ms_sum;
   t->spmv_launches = c.times.ka_launches;
   t->spmv_rows = c.times.ka_rows;
-  t->kernel_launches = c.times.kernel_launches;
+  t->kernel_launches = mlg::launch_counter().load() - c.times.launch_base;
 }
 
 void reset_kernel_stats(mlg::Ctx& c) {
@@ -67,6 +68,7 @@ void reset_kernel_stats(mlg::Ctx& c) {
   c.times.ka_launches = 0;
   c.times.ka_rows = 0;
   c.times.kernel_launches = 0;
+  c.times.launch_base = mlg::launch_counter().load();
 }
 
 struct Region {
@@ -116,6 +118,7 @@ int mlg_create(const mlg_config* cfg, mlg_ctx** out) {
     c.workers = cfg->workers;
     c.cg_tol = cfg->cg_tol;
     c.deterministic = cfg->deterministic;
+    c.device = cfg->device;
     auto h = std::make_unique<mlg_ctx>();
     h->c = std::make_unique<mlg::Ctx>(c);
     *out = h.release();
@@ -407,6 +410,10 @@ static int step_impl(mlg_ctx* ctx, int from_level, int to_level, int nev,
     const int nr = mlg::nr_for(nev);
     const mlg::Level& A = c.level(from_level);
     reset_kernel_stats(c);
+    cudaEvent_t ev0, ev1;
+    MLG_CUDA(cudaEventCreate(&ev0));
+    MLG_CUDA(cudaEventCreate(&ev1));
+    MLG_CUDA(cudaEventRecord(ev0, c.stream));
     mlg::DevBuf<double> in_ri, u_in(A.ndofs() * nr), u_out;
     const double* src = coeffs_in;
     if (!device_in) {
@@ -428,9 +435,15 @@ static int step_impl(mlg_ctx* ctx, int from_level, int to_level, int nev,
         out.download(coeffs_out, B.nint() * nev, c.stream);
       }
     }
+    MLG_CUDA(cudaEventRecord(ev1, c.stream));
     c.sync();
+    float ms = 0.f;
+    MLG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     if (matched) *matched = r.matched ? 1 : 0;
     fill_timings(timings, r.times, c);
+    if (timings) timings->step_seconds = ms * 1e-3;
   });
 }
 

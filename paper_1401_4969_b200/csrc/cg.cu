@@ -1,17 +1,23 @@
 // Batched Jacobi-PCG (sparse.cpp:199-258) for lattice-window systems.
 //
 // One CG iteration = 4 launches on the context stream:
-//   k_cg_a   (streaming)  p = z + beta p  (z = D^-1 r, recomputed for the 6
-//                         neighbours from r and p_old, so p is never re-read
-//                         after its update), q = A p with the window-masked
-//                         7-point stencil in the reference's column order,
-//                         partial p.q per tile;  or, for a right-hand side
-//                         whose recurrence residual met the tolerance, the
-//                         true residual b - A x (the reference's
-//                         confirmation step, sparse.cpp:232-246).
+//   k_cg_a   (streaming)  p = z + beta p  (z = D^-1 r), q = A p with the
+//                         window/mask-restricted 7-point stencil in the
+//                         reference's column order, partial p.q per tile;  or,
+//                         for a right-hand side whose recurrence residual met
+//                         the tolerance, the true residual b - A x (the
+//                         reference's confirmation step, sparse.cpp:232-246).
 //   k_cg_reduce<A>        one warp per (system, rhs): alpha = rho / p.q
 //   k_cg_b   (streaming)  x += alpha p, r -= alpha q, partial r.r and r.z
 //   k_cg_reduce<B>        beta, convergence test, mode of the next k_cg_a
+//
+// Memory pattern (B200): each warp sweeps a 32-column strip of its window
+// upwards with a 3-row register window (S, C, N).  Every r, p, D^-1 and
+// stencil value is loaded from HBM once per iteration (coalesced 32 x NR x 8 B
+// per row segment); the E/W/NE/SW neighbours come from warp shuffles, so the
+// L1 carries ~1x the DRAM traffic instead of 7x.  Lanes 1..30 produce output,
+// lanes 0 and 31 are the strip's halo columns.
+//
 // Partial sums are reduced in a fixed tree (no floating-point atomics), so the
 // result is run-to-run bitwise deterministic (SURVEY finding 10).  Every
 // (system, rhs) keeps its own scalars and stops independently; tiles of
@@ -27,8 +33,116 @@ namespace mlg {
 namespace {
 
 constexpr int kBlock = CgBatch::kBlock;
-constexpr int kRPT = CgBatch::kRowsPerThread;
-constexpr int kTile = CgBatch::kTile;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int NR>
+struct RowV {
+  double v[NR];
+  Stencil st;
+  int in;
+};
+
+struct Task {
+  bool valid;
+  int col, ly0, ly1;
+};
+
+__device__ __forceinline__ Task task_of(const CgSys& S, int t) {
+  Task k;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = t * kCgWarps + warp;
+  k.valid = task < S.ntasks;
+  const int rb = k.valid ? task / S.nstrips : 0;
+  const int strip = k.valid ? task % S.nstrips : 0;
+  k.col = strip * kCgCols - 1 + lane;
+  k.ly0 = rb * S.krows;
+  k.ly1 = min(k.ly0 + S.krows, S.h);
+  return k;
+}
+
+__device__ __forceinline__ bool out_lane(const CgSys& S, const Task& k) {
+  const int lane = threadIdx.x & 31;
+  return k.valid && lane >= 1 && lane <= kCgCols && k.col < S.w;
+}
+
+template <int NR>
+__device__ __forceinline__ void zero_row(RowV<NR>& o) {
+#pragma unroll
+  for (int r = 0; r < NR; ++r) o.v[r] = 0.0;
+  o.st = Stencil{0.0, 0.0, 0.0, 0.0};
+  o.in = 0;
+}
+
+// Row product of the window-restricted matrix at the C row of the register
+// window, terms in CSR column order SW,S,W,C,E,N,NE (sparse.cpp:69-76).
+template <int NR>
+__device__ __forceinline__ void window_row_product(const RowV<NR>& S_, const RowV<NR>& C_,
+                                                   const RowV<NR>& N_, double (&q)[NR]) {
+  const double wa = __shfl_up_sync(kFull, C_.st.e, 1);
+  const double swa = __shfl_up_sync(kFull, S_.st.ne, 1);
+  const int win = __shfl_up_sync(kFull, C_.in, 1);
+  const int ein = __shfl_down_sync(kFull, C_.in, 1);
+  const int swin = __shfl_up_sync(kFull, S_.in, 1);
+  const int nein = __shfl_down_sync(kFull, N_.in, 1);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const double wv = __shfl_up_sync(kFull, C_.v[r], 1);
+    const double ev = __shfl_down_sync(kFull, C_.v[r], 1);
+    const double swv = __shfl_up_sync(kFull, S_.v[r], 1);
+    const double nev = __shfl_down_sync(kFull, N_.v[r], 1);
+    double a = 0.0;
+    if (swin) a = xadd(a, xmul(swa, swv));
+    if (S_.in) a = xadd(a, xmul(S_.st.n, S_.v[r]));
+    if (win) a = xadd(a, xmul(wa, wv));
+    a = xadd(a, xmul(C_.st.c, C_.v[r]));
+    if (ein) a = xadd(a, xmul(C_.st.e, ev));
+    if (N_.in) a = xadd(a, xmul(C_.st.n, N_.v[r]));
+    if (nein) a = xadd(a, xmul(C_.st.ne, nev));
+    q[r] = a;
+  }
+}
+
+struct SweepArgs {
+  const Stencil* st;
+  const double* dinv;
+  int nxp1;
+  const unsigned char* mask;
+};
+
+// Loads row ly of this lane's column: in-system flag, stencil and the source
+// value (p_new = z + beta p for kModeNormal, x for kModeCheck).
+template <int NR, int MODE>
+__device__ __forceinline__ void load_row(const CgSys& S, const SweepArgs& A, int col, int ly,
+                                         const double* R, const double* P, const double* X,
+                                         const double (&beta)[NR], const bool (&rst)[NR],
+                                         RowV<NR>& o) {
+  const bool inside = col >= 0 && col < S.w && ly >= 0 && ly < S.h;
+  if (!inside) {
+    zero_row<NR>(o);
+    return;
+  }
+  const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + col);
+  if (A.mask && !A.mask[g]) {
+    zero_row<NR>(o);
+    return;
+  }
+  o.in = 1;
+  o.st = A.st[g];
+  const long long v = (S.voff + static_cast<long long>(ly) * S.w + col) * NR;
+  if (MODE == kModeNormal) {
+    double rv[NR], pv[NR];
+    ldv<NR>(R + v, rv);
+    ldv<NR>(P + v, pv);
+    const double dv = A.dinv[g];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const double z = xmul(dv, rv[r]);
+      o.v[r] = rst[r] ? z : xadd(z, xmul(beta[r], pv[r]));
+    }
+  } else {
+    ldv<NR>(X + v, o.v);
+  }
+}
 
 template <int NR>
 __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTile* tiles,
@@ -38,42 +152,41 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
                                                     double* part) {
   const CgTile tl = tiles[blockIdx.x];
   const CgSys S = sys[tl.sys];
+  const Task k = task_of(S, tl.t);
   double acc[2 * NR];
 #pragma unroll
-  for (int k = 0; k < 2 * NR; ++k) acc[k] = 0.0;
-  const int row0 = tl.t * kTile;
-  for (int k = 0; k < kRPT; ++k) {
-    const int i = row0 + k * kBlock + threadIdx.x;
-    if (i >= S.nrows) break;
-    const long long v = (S.voff + i) * NR;
-    double b[NR], z0[NR];
+  for (int q = 0; q < 2 * NR; ++q) acc[q] = 0.0;
+  if (out_lane(S, k)) {
+    for (int ly = k.ly0; ly < k.ly1; ++ly) {
+      const long long g = static_cast<long long>(S.y0 + ly) * nxp1 + (S.x0 + k.col);
+      const long long v = (S.voff + static_cast<long long>(ly) * S.w + k.col) * NR;
+      double b[NR], z0[NR];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) z0[r] = 0.0;
-    Nbhd h;
-    if (!decode(S, i, nxp1, mask, &h)) {
+      for (int r = 0; r < NR; ++r) z0[r] = 0.0;
       stv<NR>(X + v, z0);
-      stv<NR>(R + v, z0);
-      continue;
-    }
-    ldv<NR>(bsrc + h.g * NR, b);
-    const double dv = dinv[h.g];
-    stv<NR>(X + v, z0);
-    stv<NR>(R + v, b);
+      if (mask && !mask[g]) {
+        stv<NR>(R + v, z0);
+        continue;
+      }
+      ldv<NR>(bsrc + g * NR, b);
+      const double dv = dinv[g];
+      stv<NR>(R + v, b);
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      acc[2 * r] += b[r] * b[r];
-      acc[2 * r + 1] += b[r] * xmul(dv, b[r]);
+      for (int r = 0; r < NR; ++r) {
+        acc[2 * r] += b[r] * b[r];
+        acc[2 * r + 1] += b[r] * xmul(dv, b[r]);
+      }
     }
   }
-  block_reduce_store<2 * NR>(acc, part + static_cast<long long>(S.toff + tl.t) * 2 * NR);
+  block_reduce_store<2 * NR, kBlock>(acc,
+                                     part + static_cast<long long>(S.toff + tl.t) * 2 * NR);
 }
 
 template <int NR>
-__global__ void __launch_bounds__(kBlock)
-    k_cg_a(const CgSys* sys, const CgTile* tiles, const CgCtl* ctl, const Stencil* st,
-           const double* dinv, int nxp1, const unsigned char* mask, const double* bsrc,
-           const double* X, double* R, const double* Pin, double* Pout, double* Q,
-           double* part) {
+__global__ void __launch_bounds__(kBlock, 4)
+    k_cg_a(const CgSys* sys, const CgTile* tiles, const CgCtl* ctl, SweepArgs A,
+           const double* bsrc, const double* X, double* R, const double* Pin, double* Pout,
+           double* Q, double* part) {
   const CgTile tl = tiles[blockIdx.x];
   const CgSys S = sys[tl.sys];
   __shared__ double s_beta[NR];
@@ -96,70 +209,65 @@ __global__ void __launch_bounds__(kBlock)
     rst[r] = s_restart[r] != 0;
   }
   if (!any_normal && !any_check) return;
+  const Task k = task_of(S, tl.t);
+  const bool out = out_lane(S, k);
   double acc[2 * NR];
 #pragma unroll
-  for (int k = 0; k < 2 * NR; ++k) acc[k] = 0.0;
-  const int row0 = tl.t * kTile;
-  const double* Rb = R + S.voff * NR;
-  const double* Pb = Pin + S.voff * NR;
-  if (any_normal) {
-    auto pnew = [&](int j, long long gj, double (&o)[NR]) {
-      double rv[NR], pv[NR];
-      ldv<NR>(Rb + static_cast<long long>(j) * NR, rv);
-      ldv<NR>(Pb + static_cast<long long>(j) * NR, pv);
-      const double dv = dinv[gj];
+  for (int q = 0; q < 2 * NR; ++q) acc[q] = 0.0;
+  if (any_normal && k.valid) {
+    RowV<NR> S_, C_, N_;
+    load_row<NR, kModeNormal>(S, A, k.col, k.ly0 - 1, R, Pin, X, beta, rst, S_);
+    load_row<NR, kModeNormal>(S, A, k.col, k.ly0, R, Pin, X, beta, rst, C_);
+    for (int ly = k.ly0; ly < k.ly1; ++ly) {
+      load_row<NR, kModeNormal>(S, A, k.col, ly + 1, R, Pin, X, beta, rst, N_);
+      double q[NR];
+      window_row_product<NR>(S_, C_, N_, q);
+      if (out && C_.in) {
+        const long long v = (S.voff + static_cast<long long>(ly) * S.w + k.col) * NR;
+        stv<NR>(Pout + v, C_.v);
+        stv<NR>(Q + v, q);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const double z = xmul(dv, rv[r]);
-        o[r] = rst[r] ? z : xadd(z, xmul(beta[r], pv[r]));
+        for (int r = 0; r < NR; ++r) acc[2 * r] += C_.v[r] * q[r];
       }
-    };
-    for (int k = 0; k < kRPT; ++k) {
-      const int i = row0 + k * kBlock + threadIdx.x;
-      if (i >= S.nrows) break;
-      Nbhd h;
-      if (!decode(S, i, nxp1, mask, &h)) continue;
-      double pc[NR], q[NR];
-      stencil_apply<NR>(h, i, S.w, nxp1, st, pnew, pc, q);
-      const long long v = (S.voff + i) * NR;
-      stv<NR>(Pout + v, pc);
-      stv<NR>(Q + v, q);
-#pragma unroll
-      for (int r = 0; r < NR; ++r) acc[2 * r] += pc[r] * q[r];
+      S_ = C_;
+      C_ = N_;
     }
   }
-  if (any_check) {
+  if (any_check && k.valid) {
     // True residual r = b - A x for the right-hand sides under confirmation.
 #pragma unroll
     for (int r = 0; r < NR; ++r)
       if (s_mode[r] == kModeCheck) acc[2 * r] = acc[2 * r + 1] = 0.0;
-    const double* Xb = X + S.voff * NR;
-    auto xval = [&](int j, long long, double (&o)[NR]) {
-      ldv<NR>(Xb + static_cast<long long>(j) * NR, o);
-    };
-    for (int k = 0; k < kRPT; ++k) {
-      const int i = row0 + k * kBlock + threadIdx.x;
-      if (i >= S.nrows) break;
-      Nbhd h;
-      if (!decode(S, i, nxp1, mask, &h)) continue;
-      double xs[NR], ax[NR], b[NR], rv[NR];
-      stencil_apply<NR>(h, i, S.w, nxp1, st, xval, xs, ax);
-      ldv<NR>(bsrc + h.g * NR, b);
-      const long long v = (S.voff + i) * NR;
-      ldv<NR>(R + v, rv);
-      const double dv = dinv[h.g];
+    RowV<NR> S_, C_, N_;
+    load_row<NR, kModeCheck>(S, A, k.col, k.ly0 - 1, R, Pin, X, beta, rst, S_);
+    load_row<NR, kModeCheck>(S, A, k.col, k.ly0, R, Pin, X, beta, rst, C_);
+    for (int ly = k.ly0; ly < k.ly1; ++ly) {
+      load_row<NR, kModeCheck>(S, A, k.col, ly + 1, R, Pin, X, beta, rst, N_);
+      double ax[NR];
+      window_row_product<NR>(S_, C_, N_, ax);
+      if (out && C_.in) {
+        const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
+        const long long v = (S.voff + static_cast<long long>(ly) * S.w + k.col) * NR;
+        double b[NR], rv[NR];
+        ldv<NR>(bsrc + g * NR, b);
+        ldv<NR>(R + v, rv);
+        const double dv = A.dinv[g];
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        if (s_mode[r] != kModeCheck) continue;
-        const double rt = xsub(b[r], ax[r]);
-        rv[r] = rt;
-        acc[2 * r] += rt * rt;
-        acc[2 * r + 1] += rt * xmul(dv, rt);
+        for (int r = 0; r < NR; ++r) {
+          if (s_mode[r] != kModeCheck) continue;
+          const double rt = xsub(b[r], ax[r]);
+          rv[r] = rt;
+          acc[2 * r] += rt * rt;
+          acc[2 * r + 1] += rt * xmul(dv, rt);
+        }
+        stv<NR>(R + v, rv);
       }
-      stv<NR>(R + v, rv);
+      S_ = C_;
+      C_ = N_;
     }
   }
-  block_reduce_store<2 * NR>(acc, part + static_cast<long long>(S.toff + tl.t) * 2 * NR);
+  block_reduce_store<2 * NR, kBlock>(acc,
+                                     part + static_cast<long long>(S.toff + tl.t) * 2 * NR);
 }
 
 template <int NR>
@@ -186,40 +294,35 @@ __global__ void __launch_bounds__(kBlock)
     alpha[r] = s_alpha[r];
   }
   if (!any) return;
+  const Task k = task_of(S, tl.t);
   double acc[2 * NR];
 #pragma unroll
-  for (int k = 0; k < 2 * NR; ++k) acc[k] = 0.0;
-  const int row0 = tl.t * kTile;
-  for (int k = 0; k < kRPT; ++k) {
-    const int i = row0 + k * kBlock + threadIdx.x;
-    if (i >= S.nrows) break;
-    long long g = 0;
-    if (mask) {
-      const int lx = i % S.w, ly = i / S.w;
-      g = static_cast<long long>(S.y0 + ly) * nxp1 + (S.x0 + lx);
-      if (!mask[g]) continue;
-    } else {
-      g = static_cast<long long>(S.y0 + i / S.w) * nxp1 + (S.x0 + i % S.w);
-    }
-    const long long v = (S.voff + i) * NR;
-    double x[NR], r[NR], p[NR], q[NR];
-    ldv<NR>(X + v, x);
-    ldv<NR>(R + v, r);
-    ldv<NR>(P + v, p);
-    ldv<NR>(Q + v, q);
-    const double dv = dinv[g];
+  for (int q = 0; q < 2 * NR; ++q) acc[q] = 0.0;
+  if (out_lane(S, k)) {
+    for (int ly = k.ly0; ly < k.ly1; ++ly) {
+      const long long g = static_cast<long long>(S.y0 + ly) * nxp1 + (S.x0 + k.col);
+      if (mask && !mask[g]) continue;
+      const long long v = (S.voff + static_cast<long long>(ly) * S.w + k.col) * NR;
+      double x[NR], r[NR], p[NR], q[NR];
+      ldv<NR>(X + v, x);
+      ldv<NR>(R + v, r);
+      ldv<NR>(P + v, p);
+      ldv<NR>(Q + v, q);
+      const double dv = dinv[g];
 #pragma unroll
-    for (int k2 = 0; k2 < NR; ++k2) {
-      if (!upd[k2]) continue;
-      x[k2] = xadd(x[k2], xmul(alpha[k2], p[k2]));
-      r[k2] = xsub(r[k2], xmul(alpha[k2], q[k2]));
-      acc[2 * k2] += r[k2] * r[k2];
-      acc[2 * k2 + 1] += r[k2] * xmul(dv, r[k2]);
+      for (int j = 0; j < NR; ++j) {
+        if (!upd[j]) continue;
+        x[j] = xadd(x[j], xmul(alpha[j], p[j]));
+        r[j] = xsub(r[j], xmul(alpha[j], q[j]));
+        acc[2 * j] += r[j] * r[j];
+        acc[2 * j + 1] += r[j] * xmul(dv, r[j]);
+      }
+      stv<NR>(X + v, x);
+      stv<NR>(R + v, r);
     }
-    stv<NR>(X + v, x);
-    stv<NR>(R + v, r);
   }
-  block_reduce_store<2 * NR>(acc, part + static_cast<long long>(S.toff + tl.t) * 2 * NR);
+  block_reduce_store<2 * NR, kBlock>(acc,
+                                     part + static_cast<long long>(S.toff + tl.t) * 2 * NR);
 }
 
 enum Phase { kPhaseInit = 0, kPhaseA = 1, kPhaseB = 2 };
@@ -243,8 +346,8 @@ __global__ void k_cg_reduce(const CgSys* sys, int nsys, int nr, CgCtl* ctl, cons
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a0 += __shfl_xor_sync(kFull, a0, o);
+    a1 += __shfl_xor_sync(kFull, a1, o);
   }
   if (lane != 0) return;
   if (PH == kPhaseInit) {
@@ -317,8 +420,8 @@ void launch_a(unsigned ntiles, cudaStream_t st, const CgSys* sys, const CgTile* 
               const CgCtl* ctl, const Level& L, const unsigned char* mask, const double* bsrc,
               const double* X, double* R, const double* Pin, double* Pout, double* Q,
               double* part) {
-  k_cg_a<NR><<<ntiles, kBlock, 0, st>>>(sys, tiles, ctl, L.stA.get(), L.dinv.get(), L.nx + 1,
-                                        mask, bsrc, X, R, Pin, Pout, Q, part);
+  SweepArgs A{L.stA.get(), L.dinv.get(), L.nx + 1, mask};
+  k_cg_a<NR><<<ntiles, kBlock, 0, st>>>(sys, tiles, ctl, A, bsrc, X, R, Pin, Pout, Q, part);
 }
 template <int NR>
 void launch_b(unsigned ntiles, cudaStream_t st, const CgSys* sys, const CgTile* tiles,
@@ -349,10 +452,20 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems, int nr
   bsrc = bsrc_;
   total_rows = 0;
   total_tiles = 0;
+  long long all_rows = 0;
+  for (const CgSys& s : systems) all_rows += static_cast<long long>(s.w) * s.h;
+  // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
+  // must still offer >= ~4k warps (148 SMs x ~28 resident) to hide latency.
+  const int krows = static_cast<int>(
+      std::min<long long>(kCgRows, std::max<long long>(16, all_rows / (kCgCols * 4096LL))));
   for (CgSys& s : systems) {
     s.nrows = s.w * s.h;
     s.voff = total_rows;
-    s.ntiles = std::max(1, (s.nrows + kTile - 1) / kTile);
+    s.krows = krows;
+    s.nstrips = std::max(1, (s.w + kCgCols - 1) / kCgCols);
+    s.nrb = std::max(1, (s.h + krows - 1) / krows);
+    s.ntasks = s.nstrips * s.nrb;
+    s.ntiles = (s.ntasks + kCgWarps - 1) / kCgWarps;
     s.toff = total_tiles;
     s.maxit = 10 * std::max(s.nrows, 1);
     total_rows += s.nrows;
@@ -409,7 +522,6 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
   int chunk = 16;
-  int iters_done = 0;
   while (true) {
     for (int it = 0; it < chunk && !tiles.empty(); ++it) {
       const unsigned nt = static_cast<unsigned>(tiles.size());
@@ -437,9 +549,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
                                                        partB.get(), tol);
       MLG_LAUNCH_CHECK();
       std::swap(pin, pout);
-      c.times.kernel_launches += 4;
     }
-    iters_done += chunk;
     ctl_d.download(ctl.data(), ctl.size(), st);
     c.sync();
     bool running = false;

@@ -17,6 +17,11 @@ namespace mlg {
 // matrix is the window (mask) restriction of the level's stiffness, exactly
 // extract_submatrix (sparse.cpp:156-174).  Vectors are window-compact,
 // row-major, NR right-hand sides interleaved.
+//
+// Work decomposition: a warp task is one column strip (32 lanes covering 30
+// output columns plus one halo column each side) of kCgRows window rows,
+// swept bottom to top with a 3-row register window; a CTA ("tile") runs
+// kCgWarps consecutive tasks of one system and owns one partial-sum slot.
 struct CgSys {
   int x0, y0, w, h;
   long long voff;  // first row in the pooled vectors
@@ -24,6 +29,7 @@ struct CgSys {
   int ntiles;
   int nrows;
   int maxit;
+  int nstrips, nrb, ntasks, krows;
 };
 
 struct CgTile {
@@ -39,6 +45,10 @@ struct CgCtl {
 enum : int { kModeSkip = 0, kModeNormal = 1, kModeCheck = 2 };
 enum : int { kRunning = 0, kConverged = 1, kNotConverged = 2, kIndefinite = 3 };
 
+constexpr int kCgWarps = 4;     // warps (tasks) per CTA
+constexpr int kCgCols = 30;     // output columns per warp task
+constexpr int kCgRows = 64;     // max window rows per warp task
+
 struct CgResult {
   std::vector<SolveReport> reports;  // [sys * nr + rhs]
   int iters_max = 0;
@@ -46,10 +56,7 @@ struct CgResult {
 
 class CgBatch {
  public:
-  // rows per tile = kCgBlock * kCgRowsPerThread
-  static constexpr int kBlock = 256;
-  static constexpr int kRowsPerThread = 8;
-  static constexpr int kTile = kBlock * kRowsPerThread;
+  static constexpr int kBlock = 32 * kCgWarps;
 
   // Lays out systems (computing voff/toff/ntiles) and sizes the pools.
   void setup(Ctx& c, const Level& L, std::vector<CgSys> systems, int nr,

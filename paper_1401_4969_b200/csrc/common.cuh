@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -33,8 +34,18 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     throw CudaError(std::string("CUDA error in ") + what + " (" + file + ":" +
                     std::to_string(line) + "): " + cudaGetErrorString(e));
 }
+// Process-wide count of this library's kernel launches (bench evidence).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> n{0};
+  return n;
+}
+
 #define MLG_CUDA(call) ::mlg::cuda_check((call), #call, __FILE__, __LINE__)
-#define MLG_LAUNCH_CHECK() ::mlg::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+#define MLG_LAUNCH_CHECK()                                                           \
+  do {                                                                               \
+    ::mlg::launch_counter().fetch_add(1, std::memory_order_relaxed);                 \
+    ::mlg::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);      \
+  } while (0)
 
 template <class T>
 class DevBuf {

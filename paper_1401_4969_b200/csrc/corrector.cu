@@ -614,6 +614,7 @@ struct Workspace {
 
 Ctx::Ctx(const Config& config) : cfg(config) {
   validate_config(cfg);
+  MLG_CUDA(cudaSetDevice(cfg.device));
   MLG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   if (cusolverDnCreate(&solver) != CUSOLVER_STATUS_SUCCESS)
     throw CudaError("cusolverDnCreate failed");

@@ -43,6 +43,7 @@ struct Config {
   int workers = 1;
   double cg_tol = 1e-10;
   int deterministic = 1;
+  int device = 0;
 };
 
 struct IRect {
@@ -82,7 +83,8 @@ struct StepTimes {
   double ka_ms_sum = 0;  // summed device time of the local-solve SpMV kernel
   int ka_launches = 0;
   double ka_rows = 0;    // summed active rows over those launches
-  int kernel_launches = 0;
+  long long kernel_launches = 0;
+  long long launch_base = 0;  // launch_counter() at the start of the step
 };
 
 struct SolveReport {

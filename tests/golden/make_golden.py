@@ -1,0 +1,149 @@
+"""Generate the golden fixtures in tests/golden/ from the compiled reference
+(oracle/_ref/libmleig_ref.so = /root/reference/proj/src built by oracle/Makefile).
+
+    python tests/golden/make_golden.py            # small + medium fixtures
+    python tests/golden/make_golden.py --big      # adds the 4096^2 mesh/CSR digests and
+                                                  # the 2048^2 nev=4 run (tens of minutes)
+
+Outputs: golden.json (digests, eigenvalues per level, CG iteration counts,
+seeded projections of final eigenvectors) and unit8_L4_u1.npy (one small
+eigenvector).  Digests are FNV-1a-64 over raw little-endian bytes
+(SURVEY.md Appendix B).
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+from oracle import ref  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+UNIT = (0.0, 1.0, 0.0, 1.0)
+SQUARE = (-1.0, 1.0, -1.0, 1.0)
+N_PROJ = 8
+
+
+def projections(vecs, seed=20261019):
+    """u . r_k for seeded uniform(-1,1) r_k (size-independent eigenvector pins)."""
+    vecs = np.atleast_2d(vecs)
+    rng = np.random.default_rng(seed)
+    R = rng.uniform(-1.0, 1.0, size=(N_PROJ, vecs.shape[1]))
+    return (vecs @ R.T).tolist()
+
+
+def digests(n0, levels, m, delta):
+    t = time.time()
+    h = ref.RefHierarchy(domain=UNIT, H=1.0 / n0, delta=delta, m=m, n_levels=levels, nev=1)
+    h.extend_to(levels)
+    L = levels
+    mesh = h.mesh(L)
+    s = h.sizes(L)
+    out = {
+        "counts": {k: s[k] for k in ("nv", "nt", "nb", "ndofs", "n_int", "nnz_a")},
+        "h_max": s["h_max"],
+        "mesh": ref.fnv1a64(mesh["triangles"], mesh["vertices"], mesh["parent"],
+                            mesh["boundary_edges"]),
+        "lattice": ref.fnv1a64(mesh["lattice"]),
+    }
+    del mesh
+    rp, cols, va = h.csr(L, "stiffness")
+    out.update(row_ptr=ref.fnv1a64(rp), cols=ref.fnv1a64(cols), values_A=ref.fnv1a64(va))
+    del rp, cols, va
+    _, _, vm = h.csr(L, "mass")
+    out["values_M"] = ref.fnv1a64(vm)
+    del vm
+    sp = h.space(L)
+    out["connectivity"] = ref.fnv1a64(sp["connectivity"])
+    out["interior_dofs"] = ref.fnv1a64(sp["interior_dofs"])
+    out["seconds"] = time.time() - t
+    h.close()
+    return out
+
+
+def multilevel(name, domain, H, delta, m, levels, nev, workers=8, save_vec=None):
+    t = time.time()
+    h = ref.RefHierarchy(domain=domain, H=H, delta=delta, m=m, n_levels=levels, nev=nev,
+                         workers=workers)
+    lam, co, matched, times = h.multilevel(levels, nev)
+    out = {
+        "config": dict(domain=domain, H=H, delta=delta, m=m, n_levels=levels, nev=nev),
+        "lambdas": lam.tolist(),
+        "matched": matched.tolist(),
+        "projections": projections(co),
+        "norm2": [float(v @ v) for v in co],
+        "seconds": time.time() - t,
+    }
+    if save_vec:
+        np.save(OUT / save_vec, co)
+    h.close()
+    print(name, out["lambdas"][-1], f"{out['seconds']:.1f}s", flush=True)
+    return out
+
+
+def cg_iterations():
+    """Iteration counts of the reference's local solves (test_corrector-style)."""
+    h = ref.RefHierarchy(domain=UNIT, H=1 / 8, delta=1 / 8, m=4, n_levels=4, nev=1)
+    lam, co = h.coarse_eigensolve(3, 1)
+    h.extend_to(4)
+    u = h.prolong(np.concatenate([[0.0]]) if False else _expand(h, 3, co[0]), 3, 4)
+    its = []
+    for j in range(4):
+        _, it, _ = h.local_bvp_solve(4, j, lam[0], u, 1e-10)
+        its.append(it)
+    return {"unit8_L3to4_local_iterations": its}
+
+
+def _expand(h, level, coeffs):
+    s = h.sizes(level)
+    full = np.zeros(s["ndofs"])
+    full.reshape(s["ny"] + 1, s["nx"] + 1)[1:-1, 1:-1] = coeffs.reshape(s["ny"] - 1, s["nx"] - 1)
+    return full
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true")
+    args = ap.parse_args()
+    if not ref.available():
+        ref.build()
+    path = OUT / "golden.json"
+    g = json.loads(path.read_text()) if path.exists() else {}
+    g.setdefault("digests", {})
+    g.setdefault("multilevel", {})
+    g["generator"] = "tests/golden/make_golden.py via oracle/_ref (reference sources + shims)"
+    for (n0, L, m, d) in [(8, 4, 4, 1 / 8), (16, 3, 16, 1 / 16), (16, 6, 16, 1 / 16),
+                          (16, 7, 16, 1 / 16)]:
+        key = f"{n0}_{L}"
+        if key not in g["digests"]:
+            g["digests"][key] = digests(n0, L, m, d)
+            print(key, g["digests"][key]["mesh"], flush=True)
+    runs = {
+        "small_L3_nev3": (SQUARE, 0.25, 0.25, 4, 3, 3, None),
+        "whole_L3_nev3": (SQUARE, 0.5, 0.5, 1, 3, 3, None),
+        "square_L4_nev5": (SQUARE, 0.25, 0.25, 4, 4, 5, None),
+        "unit8_L4_m4_nev1": (UNIT, 1 / 8, 1 / 8, 4, 4, 1, "unit8_L4_u1.npy"),
+        "unit16_L3_m16_nev1": (UNIT, 1 / 16, 1 / 16, 16, 3, 1, None),
+        "unit8_L3_m4_nev4": (UNIT, 1 / 8, 1 / 8, 4, 3, 4, None),
+        "c2sub_16_L6_m16_nev1": (UNIT, 1 / 16, 1 / 16, 16, 6, 1, None),
+        "c5shape_32_L5_m64_nev4": (UNIT, 1 / 32, 1 / 32, 64, 5, 4, None),
+    }
+    if args.big:
+        runs["c5shape_32_L6_m64_nev4"] = (UNIT, 1 / 32, 1 / 32, 64, 6, 4, None)
+    for name, (dom, H, d, m, L, nev, vec) in runs.items():
+        if name not in g["multilevel"]:
+            g["multilevel"][name] = multilevel(name, dom, H, d, m, L, nev, save_vec=vec)
+            path.write_text(json.dumps(g, indent=1))
+    if "cg" not in g:
+        g["cg"] = cg_iterations()
+    if args.big and "32_7" not in g["digests"]:
+        g["digests"]["32_7"] = digests(32, 7, 64, 1 / 32)
+    path.write_text(json.dumps(g, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,50 @@
+"""CPU checks of the drop-in boundary: the CUDA library loads (built for
+sm_100a) and exports every symbol include/mlg_b200.h declares; the ctypes
+mirror binds all of them.  No compute calls (no GPU here)."""
+import re
+import subprocess
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "mlg_b200.h"
+
+
+def declared_symbols():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(mlg_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for s in ("mlg_create", "mlg_correction_step", "mlg_local_bvp_solve",
+              "mlg_interface_solve", "mlg_augmented_eigensolve", "mlg_multilevel_correction",
+              "mlg_export_csr", "mlg_export_mesh"):
+        assert s in syms
+
+
+def test_library_loads_and_exports_all_symbols(mlg):
+    lib = mlg.lib()
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    out = subprocess.run(["nm", "-D", "--defined-only", str(mlg._lib.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (mlg_\w+)", out))
+    assert set(declared_symbols()) <= exported
+
+
+def test_ctypes_signatures_cover_header(mlg):
+    assert set(declared_symbols()) == set(mlg._lib.SIGNATURES)
+
+
+def test_library_is_sm100a():
+    so = ROOT / "paper_1401_4969_b200" / "libmlg_b200.so"
+    out = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_in_product():
+    """The product never imports the oracle."""
+    pkg = ROOT / "paper_1401_4969_b200"
+    for f in list(pkg.glob("*.py")) + list((pkg / "csrc").glob("*")):
+        assert "oracle" not in f.read_text().replace("oracle/_ref", ""), f
