@@ -84,6 +84,8 @@ typedef struct mlg_step_timings {
   int64_t kernel_launches; /* CG kernel launches of the step */
   double step_seconds;     /* CUDA events on the context stream around the whole call,
                               host<->device copies included for the host-array variant */
+  int spmv_uniform_stencil; /* 1: stencil/D^-1 taken from kernel parameters (bytes/row
+                               of the SpMV kernel = 32*NR instead of 40 + 32*NR) */
 } mlg_step_timings;
 
 const char* mlg_last_error(void);

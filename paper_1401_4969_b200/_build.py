@@ -72,7 +72,28 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_driver(verbose, force)
     return LIB
+
+
+DRIVER_SRC = PKG.parent / "tools" / "mlg_run.cpp"
+DRIVER = OBJ / "mlg_run"
+
+
+def build_driver(verbose: bool = False, force: bool = False) -> Path:
+    """C++ host driver over include/mleig_b200.hpp (the drop-in host API)."""
+    inc = PKG.parent / "include"
+    deps = [DRIVER_SRC, inc / "mleig_b200.hpp", inc / "mlg_b200.h", LIB]
+    if force or _stale(DRIVER, deps):
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-O2", "-std=c++17", f"-I{inc}", str(DRIVER_SRC), "-o", str(DRIVER),
+               f"-L{PKG}", "-l:libmlg_b200.so", f"-Wl,-rpath,{PKG}"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C++ driver build failed:\n{r.stdout}\n{r.stderr}")
+    return DRIVER
 
 
 if __name__ == "__main__":

@@ -82,12 +82,14 @@ class StepTimings:  # corrector.hpp:97-101 (+ device evidence)
     spmv_rows: float = 0.0
     kernel_launches: int = 0
     step_seconds: float = 0.0
+    spmv_uniform_stencil: bool = False
 
     @classmethod
     def from_c(cls, t: MlgStepTimings) -> "StepTimings":
         return cls(t.local_seconds, t.iface_seconds, t.aug_seconds, t.build_seconds,
                    t.local_iterations_max, t.strip_iterations_max, t.spmv_kernel_ms,
-                   t.spmv_launches, t.spmv_rows, t.kernel_launches, t.step_seconds)
+                   t.spmv_launches, t.spmv_rows, t.kernel_launches, t.step_seconds,
+                   bool(t.spmv_uniform_stencil))
 
 
 @dataclass

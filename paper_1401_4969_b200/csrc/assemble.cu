@@ -18,6 +18,7 @@
 // them.  Output is the 4-entry upper stencil {C,E,N,NE} of A and M per dof
 // (64 B/dof written, coalesced); CSR export is a second closed-form pass.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ctx.cuh"
 
@@ -225,6 +226,23 @@ __global__ void k_interior_dense(int nx, int ny, const Stencil* st, double* dens
   if (j < h - 1 && i < w - 1) put(k + w + 1, st[d].ne);
 }
 
+// Clears *flag if any interior row of st / dinv differs bitwise from row (1,1).
+__global__ void k_uniform_check(int nx, int ny, const Stencil* st, const double* dinv,
+                                int* flag) {
+  const std::int64_t k = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const int w = nx - 1;
+  if (k >= static_cast<std::int64_t>(w) * (ny - 1)) return;
+  const std::int64_t d = (k / w + 1) * (nx + 1) + (k % w + 1);
+  const std::int64_t d0 = (nx + 1) + 1;
+  const Stencil a = st[d], b = st[d0];
+  const bool same = __double_as_longlong(a.c) == __double_as_longlong(b.c) &&
+                    __double_as_longlong(a.e) == __double_as_longlong(b.e) &&
+                    __double_as_longlong(a.n) == __double_as_longlong(b.n) &&
+                    __double_as_longlong(a.ne) == __double_as_longlong(b.ne) &&
+                    __double_as_longlong(dinv[d]) == __double_as_longlong(dinv[d0]);
+  if (!same) atomicAnd(flag, 0);
+}
+
 }  // namespace
 
 std::int64_t csr_nnz(const Level& L) {
@@ -242,6 +260,27 @@ void assemble_level(Ctx& c, Level& L) {
   k_assemble<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
                                                             L.dinv.get());
   MLG_LAUNCH_CHECK();
+  // Constant-coefficient detection for the CG fast path (MLG_GENERAL_STENCIL=1
+  // forces the general per-row path, used by the tests to cover both).
+  L.uniform = 0;
+  const char* env = std::getenv("MLG_GENERAL_STENCIL");
+  if (L.nx >= 2 && L.ny >= 2 && !(env && env[0] == '1')) {
+    DevBuf<int> flag(1);
+    const int one = 1;
+    flag.upload(&one, 1, c.stream);
+    k_uniform_check<<<grid_for(L.nint(), kBlock), kBlock, 0, c.stream>>>(
+        L.nx, L.ny, L.stA.get(), L.dinv.get(), flag.get());
+    MLG_LAUNCH_CHECK();
+    int f = 0;
+    flag.download(&f, 1, c.stream);
+    const std::int64_t d0 = (L.nx + 1) + 1;
+    MLG_CUDA(cudaMemcpyAsync(&L.ust, L.stA.get() + d0, sizeof(Stencil), cudaMemcpyDeviceToHost,
+                             c.stream));
+    MLG_CUDA(cudaMemcpyAsync(&L.udinv, L.dinv.get() + d0, sizeof(double),
+                             cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    L.uniform = f;
+  }
 }
 
 void export_csr(Ctx& c, const Level& L, int form, int* row_ptr, int* cols, double* vals) {

@@ -61,6 +61,7 @@ void fill_timings(mlg_step_timings* t, const mlg::StepTimes& s, const mlg::Ctx& 
   t->spmv_launches = c.times.ka_launches;
   t->spmv_rows = c.times.ka_rows;
   t->kernel_launches = mlg::launch_counter().load() - c.times.launch_base;
+  t->spmv_uniform_stencil = c.times.ka_uniform;
 }
 
 void reset_kernel_stats(mlg::Ctx& c) {
@@ -414,10 +415,14 @@ static int step_impl(mlg_ctx* ctx, int from_level, int to_level, int nev,
     MLG_CUDA(cudaEventCreate(&ev0));
     MLG_CUDA(cudaEventCreate(&ev1));
     MLG_CUDA(cudaEventRecord(ev0, c.stream));
-    mlg::DevBuf<double> in_ri, u_in(A.ndofs() * nr), u_out;
+    // grow-only context buffers: no allocation inside a steady-state step
+    mlg::DevBuf<double>& in_ri = c.io_in;
+    mlg::DevBuf<double>& u_in = c.io_u_in;
+    mlg::DevBuf<double>& u_out = c.io_u_out;
+    u_in.ensure(A.ndofs() * nr);
     const double* src = coeffs_in;
     if (!device_in) {
-      in_ri.alloc(A.nint() * nev);
+      in_ri.ensure(A.nint() * nev);
       in_ri.upload(coeffs_in, A.nint() * nev, c.stream);
       src = in_ri.get();
     }
@@ -430,7 +435,8 @@ static int step_impl(mlg_ctx* ctx, int from_level, int to_level, int nev,
       if (device_out) {
         mlg::deinterleave(c, B, nr, nev, nullptr, u_out.get(), 1, coeffs_out);
       } else {
-        mlg::DevBuf<double> out(B.nint() * nev);
+        mlg::DevBuf<double>& out = c.io_out;
+        out.ensure(B.nint() * nev);
         mlg::deinterleave(c, B, nr, nev, nullptr, u_out.get(), 1, out.get());
         out.download(coeffs_out, B.nint() * nev, c.stream);
       }

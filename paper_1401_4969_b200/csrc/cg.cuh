@@ -80,6 +80,7 @@ class CgBatch {
   DevBuf<CgSys> sys_d;
   DevBuf<CgTile> tiles_d;
   DevBuf<CgCtl> ctl_d;
+  DevBuf<unsigned> counters;  // per-system tile arrival counters (last-tile reduction)
   DevBuf<double> X, R, P0, P1, Q, partA, partB;
 };
 

@@ -604,6 +604,7 @@ static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-
 struct Workspace {
   CgBatch local, strip;
   DevBuf<double> corr;
+  DevBuf<double> aug_ctmp, aug_uu_a, aug_uu_b, aug_cp, aug_c0;
   DevBuf<double> u, res, glued, au, bu, full, mfull, load, tmp_c0, tmp_c1, a_cu, b_cu;
   DevBuf<double> part, dots, dense_a, dense_b, eigw, work, sign;
   DevBuf<AbsMax> amax;
@@ -629,6 +630,7 @@ Ctx::Ctx(const Config& config) : cfg(config) {
 Ctx::~Ctx() {
   ws.reset();
   levels.clear();
+  for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
   if (solver) cusolverDnDestroy(solver);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -972,7 +974,8 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
 
   // Dependence drop through the cached coarse Cholesky (corrector.cpp:285-292).
   std::vector<double> bcu(static_cast<std::size_t>(mc) * nr), csol(bcu.size());
-  DevBuf<double> ctmp(bcu.size());
+  DevBuf<double>& ctmp = w.aug_ctmp;
+  ctmp.ensure(bcu.size());
   MLG_CUDA(cudaMemcpyAsync(ctmp.get(), w.b_cu.get(), sizeof(double) * bcu.size(),
                            cudaMemcpyDeviceToDevice, c.stream));
   cusolverDnDpotrs(c.solver, CUBLAS_FILL_MODE_LOWER, mc, k_in, c.coarse_bchol.get(), mc,
@@ -994,7 +997,10 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
 
   w.keep.ensure(8);
   w.keep.upload(keep.data(), keep.size(), c.stream);
-  DevBuf<double> uu_a(nr * nr), uu_b(nr * nr);
+  DevBuf<double>& uu_a = w.aug_uu_a;
+  DevBuf<double>& uu_b = w.aug_uu_b;
+  uu_a.ensure(nr * nr);
+  uu_b.ensure(nr * nr);
   uu_a.upload(a_uu.data(), a_uu.size(), c.stream);
   uu_b.upload(b_uu.data(), b_uu.size(), c.stream);
   w.dense_a.ensure(static_cast<std::size_t>(dim) * dim);
@@ -1018,11 +1024,13 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
               coarse_part.begin() + static_cast<long>(i) * mc);
     for (int l = 0; l < k; ++l) coef[i * 8 + l] = pairs[i].vec[mc + l];
   }
-  DevBuf<double> cp(coarse_part.size());
+  DevBuf<double>& cp = w.aug_cp;
+  cp.ensure(coarse_part.size());
   cp.upload(coarse_part.data(), coarse_part.size(), c.stream);
   w.coef.ensure(64);
   w.coef.upload(coef.data(), 64, c.stream);
-  DevBuf<double> c0(L0.ndofs() * nr);
+  DevBuf<double>& c0 = w.aug_c0;
+  c0.ensure(L0.ndofs() * nr);
   NR_DISPATCH(nr, k_interleave, grid_for(L0.ndofs(), kB), L0.nx, L0.ny, nev, cp.get(), 1,
               c0.get());
   w.full.ensure(nd * nr);

@@ -72,6 +72,11 @@ struct Level {
   DevBuf<Stencil> stA, stM;
   DevBuf<double> dinv;
   DevBuf<unsigned char> strip_mask;  // built lazily (1 = interior dof of the strip)
+  // All interior rows of A (and 1/A_ii) bitwise identical: the CG kernels then
+  // take the stencil from kernel parameters (constant-coefficient lattice).
+  int uniform = 0;
+  Stencil ust{0.0, 0.0, 0.0, 0.0};
+  double udinv = 0.0;
 
   std::int64_t ndofs() const { return static_cast<std::int64_t>(nx + 1) * (ny + 1); }
   std::int64_t nint() const { return static_cast<std::int64_t>(nx - 1) * (ny - 1); }
@@ -84,6 +89,7 @@ struct StepTimes {
   int ka_launches = 0;
   double ka_rows = 0;    // summed active rows over those launches
   long long kernel_launches = 0;
+  int ka_uniform = 0;  // the CG ran the constant-coefficient (no stencil stream) variant
   long long launch_base = 0;  // launch_counter() at the start of the step
 };
 
@@ -134,12 +140,23 @@ class Ctx {
   void ensure_coarse_dense();
 
   // Scratch (grow-only) owned by the context.
+  DevBuf<double> io_in, io_out, io_u_in, io_u_out;  // C-ABI step marshalling
   DevBuf<unsigned char> scratch;
   void* scratch_bytes(std::size_t n) {
     scratch.ensure(n);
     return scratch.get();
   }
   std::shared_ptr<void> ws;  // corrector.cu Workspace (CG pools, step vectors)
+  // Pooled timing events (created once, reused by every profiled launch).
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t event(std::size_t i) {
+    while (ev_pool.size() <= i) {
+      cudaEvent_t e;
+      MLG_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[i];
+  }
   bool profile = false;  // record CUDA events around the local-solve SpMV kernel
   StepTimes times;
 };

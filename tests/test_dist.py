@@ -57,3 +57,4 @@ def test_ka_bytes_model():
     assert bench.ka_bytes_per_row(1) == 72
     assert bench.ka_bytes_per_row(4) == 168
     assert bench.ka_bytes_per_row(3) == 168
+    assert bench.ka_bytes_per_row(4, True) == 128

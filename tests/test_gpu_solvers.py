@@ -161,6 +161,24 @@ def test_step_is_deterministic(mlg, oracle_ref):
         assert np.array_equal(pa.coeffs.view(np.uint64), pb.coeffs.view(np.uint64))
 
 
+def test_uniform_stencil_fast_path_is_bitwise_general_path(mlg, monkeypatch):
+    """The constant-coefficient CG path (stencil from kernel parameters) and the
+    general per-row path give bitwise identical steps."""
+    def run():
+        cfg = mlg.RunConfig(domain=mlg.DomainRect(0.0, 1.0, 0.0, 1.0), H=1 / 8, delta=1 / 8, m=4,
+                            n_levels=4, nev=4)
+        with mlg.Hierarchy(cfg) as hy:
+            lam, pairs, matched, times = mlg.multilevel_correction(hy)
+        return lam, pairs
+    monkeypatch.setenv("MLG_GENERAL_STENCIL", "1")
+    lam_g, p_g = run()
+    monkeypatch.delenv("MLG_GENERAL_STENCIL")
+    lam_u, p_u = run()
+    assert np.array_equal(lam_g, lam_u)
+    for a, b in zip(p_g, p_u):
+        assert np.array_equal(a.coeffs.view(np.uint64), b.coeffs.view(np.uint64))
+
+
 def test_config_errors(mlg):
     bad = [dict(m=3), dict(delta=1.0), dict(H=0.3), dict(nev=0), dict(degree=3),
            dict(example="helmholtz"), dict(workers=0)]
