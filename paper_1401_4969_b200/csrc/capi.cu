@@ -323,7 +323,7 @@ int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const dou
     mlg::interleave(c, F, 1, 1, u.get(), 0, ui.get());
     mlg::residual(c, F, 1, ui.get(), &lambda, res.get());
     std::vector<mlg::SolveReport> rep;
-    mlg::local_solves(c, F, 1, res.get(), cg_tol, 0, &rep, j);
+    mlg::local_solves(c, F, 1, 1, res.get(), cg_tol, 0, &rep, j);
     const mlg::CgBatch& b = mlg::local_batch(c);
     const mlg::CgSys s = b.systems()[0];
     std::vector<double> x(static_cast<std::size_t>(s.nrows));
@@ -364,7 +364,7 @@ int mlg_interface_solve(mlg_ctx* ctx, int level, double lambda, const double* u_
     bool empty = false;
     mlg::Lam lam{};
     lam.v[0] = lambda;
-    mlg::strip_solve(c, F, 1, ui.get(), lam, glued.get(), cg_tol, 0, &rep, &empty);
+    mlg::strip_solve(c, F, 1, 1, ui.get(), lam, glued.get(), cg_tol, 0, &rep, &empty);
     glued.download(glued_full, nd, c.stream);
     c.sync();
     if (report) {

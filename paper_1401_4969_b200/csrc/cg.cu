@@ -1,29 +1,33 @@
-// Batched Jacobi-PCG (sparse.cpp:199-258) for lattice-window systems.
+// Batched Jacobi-PCG (sparse.cpp:199-258) for lattice-window systems: ONE
+// launch per CG iteration for all systems of a batch.
 //
-// One CG iteration = 2 streaming launches on the context stream:
-//   k_cg_a  p = z + beta p (z = D^-1 r), q = A p with the window/mask-restricted
-//           7-point stencil in the reference's column order, partial p.q per
-//           tile -- or, for a right-hand side whose recurrence residual met the
-//           tolerance, the true residual b - A x (the reference's confirmation
-//           step, sparse.cpp:232-246);  the last tile of each system to finish
-//           reduces the partials and sets alpha = rho / p.q.
-//   k_cg_b  x += alpha p, r -= alpha q, partial r.r and r.z;  the last tile of
-//           each system sets beta, tests convergence and picks the next mode.
+// Iteration scheme (the one-reduction rearrangement of PCG; same iterates in
+// exact arithmetic, reductions in a fixed order):  launch k applies the
+// pending update of iteration k-1 and prepares iteration k in a single sweep:
+//     q_old = A p_old              (recomputed, never stored)
+//     r = r - alpha q_old,  x = x + alpha p_old,  z = D^-1 r
+//     p = z + beta p_old,   q = A p
+//     partials  r.r, r.z, p.q, q.z, q.D^-1 q
+// The tile that finishes last reduces the partials of its system and sets
+// alpha = rho / p.q with rho = r.z (exact), rho_next = rho - 2 alpha q.z +
+// alpha^2 q.D^-1q (so beta = rho_next / rho is known before the next sweep),
+// and applies the reference's stopping rule: ||r|| <= tol ||b|| triggers a
+// true-residual launch (b - A x; restart from it if it fails, sparse.cpp:232-246).
+// Per row and iteration this moves x, r, p in and out (48 B) instead of the
+// 80 B of the classic two-kernel form, and needs one launch instead of two.
 //
 // Memory pattern (B200): each warp sweeps a 32-column strip of its window
-// upwards with a 3-row register window (S, C, N) and loads the next rows in
-// groups (UNR rows per group, all loads of a group issued back to back).  Every
-// r, p, D^-1 and stencil value is read from HBM once per iteration (coalesced
-// 32 x NR x 8 B per row segment); the E/W/NE/SW neighbours come from warp
-// shuffles, so the L1 carries ~1x the DRAM traffic instead of 7x.  Lanes 1..30
-// produce output, lanes 0 and 31 are the strip's halo columns.  When the
-// level's interior stiffness rows are bitwise identical (UNI: constant-
-// coefficient lattice) the stencil and D^-1 come from kernel parameters.
+// upwards; the two stencil applications use a 4-row register window of the old
+// iterate and a 3-row window of the new p, neighbours in x from warp shuffles,
+// so every value is read from HBM once per iteration.  Lanes 2..29 produce
+// output; lanes 0,1,30,31 are the strip's 2-deep halo.  When the level's
+// interior stiffness rows are bitwise identical (UNI: constant-coefficient
+// lattice) the stencil and D^-1 come from kernel parameters.
 //
 // Partial sums are reduced in a fixed order by whichever tile finishes last
-// (no floating-point atomics), so results are run-to-run bitwise deterministic
-// (SURVEY finding 10).  Every (system, rhs) keeps its own scalars and stops
-// independently; tiles of finished systems are dropped between chunks.
+// (no floating-point atomics): results are run-to-run bitwise deterministic
+// (SURVEY finding 10).  Every system stops independently; tiles of finished
+// systems are dropped between chunks.
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -37,16 +41,39 @@ namespace {
 constexpr int kBlock = CgBatch::kBlock;
 constexpr unsigned kFull = 0xffffffffu;
 
-// One lattice row of a lane's column inside the register window.
-template <int NR, bool UNI>
-struct RowV {
-  double v[NR];
+struct SweepArgs {
+  const Stencil* st;
+  const double* dinv;
+  int nxp1;
+  const unsigned char* mask;  // non-null: system restricted to the strip
+  StripGeom sg;               // closed form of that restriction (no mask loads)
+  Stencil ust;                // interior stencil when the level is uniform
+  double udinv;
+};
+
+// Strip membership of fine lattice point (ix, iy): not in the closed inner
+// region G_j of its block (decomp.cpp:73-80, 204-211); G_j never touches an
+// interior block side, so the block found by division is the only candidate.
+__device__ __forceinline__ bool in_strip(const StripGeom& g, int ix, int iy) {
+  const int bx = min(ix / (g.bw * g.scale), g.side - 1);
+  const int by = min(iy / (g.bh * g.scale), g.side - 1);
+  const int x0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+  const int x1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+  const int y0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+  const int y1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+  return !(ix >= x0 && ix <= x1 && iy >= y0 && iy <= y1);
+}
+
+// Old iterate at one row of the lane's column.
+struct ORow {
+  double p, r, x, dv;
   Stencil st;
   int in;
 };
-template <int NR>
-struct RowV<NR, true> {  // constant-coefficient lattice: no per-row stencil
-  double v[NR];
+// New p (and z) at one row.
+struct NRow {
+  double p, z, dv;
+  Stencil st;
   int in;
 };
 
@@ -62,7 +89,7 @@ __device__ __forceinline__ Task task_of(const CgSys& S, int t) {
   k.valid = task < S.ntasks;
   const int rb = k.valid ? task / S.nstrips : 0;
   const int strip = k.valid ? task % S.nstrips : 0;
-  k.col = strip * kCgCols - 1 + lane;
+  k.col = strip * kCgCols - 2 + lane;
   k.ly0 = rb * S.krows;
   k.ly1 = min(k.ly0 + S.krows, S.h);
   return k;
@@ -70,174 +97,119 @@ __device__ __forceinline__ Task task_of(const CgSys& S, int t) {
 
 __device__ __forceinline__ bool out_lane(const CgSys& S, const Task& k) {
   const int lane = threadIdx.x & 31;
-  return k.valid && lane >= 1 && lane <= kCgCols && k.col < S.w;
-}
-
-struct SweepArgs {
-  const Stencil* st;
-  const double* dinv;
-  int nxp1;
-  const unsigned char* mask;
-  Stencil ust;  // interior stencil when the level is uniform
-  double udinv;
-};
-
-template <int NR, bool UNI>
-__device__ __forceinline__ void zero_row(RowV<NR, UNI>& o) {
-#pragma unroll
-  for (int r = 0; r < NR; ++r) o.v[r] = 0.0;
-  if constexpr (!UNI) o.st = Stencil{0.0, 0.0, 0.0, 0.0};
-  o.in = 0;
-}
-
-template <int NR, bool UNI>
-__device__ __forceinline__ const Stencil& row_st(const RowV<NR, UNI>& o, const SweepArgs& A) {
-  if constexpr (UNI) {
-    return A.ust;
-  } else {
-    return o.st;
-  }
-}
-
-// Row product of the window-restricted matrix at the C row of the register
-// window, terms in CSR column order SW,S,W,C,E,N,NE (sparse.cpp:69-76).  A
-// coefficient is only used when its neighbour is inside the system, i.e. an
-// interior row, so the uniform stencil is exact there.
-template <int NR, bool UNI>
-__device__ __forceinline__ void window_row_product(const RowV<NR, UNI>& S_,
-                                                   const RowV<NR, UNI>& C_,
-                                                   const RowV<NR, UNI>& N_, const SweepArgs& A,
-                                                   double (&q)[NR]) {
-  const Stencil& cs = row_st(C_, A);
-  const Stencil& ss = row_st(S_, A);
-  const double wa = UNI ? A.ust.e : __shfl_up_sync(kFull, cs.e, 1);
-  const double swa = UNI ? A.ust.ne : __shfl_up_sync(kFull, ss.ne, 1);
-  const int win = __shfl_up_sync(kFull, C_.in, 1);
-  const int ein = __shfl_down_sync(kFull, C_.in, 1);
-  const int swin = __shfl_up_sync(kFull, S_.in, 1);
-  const int nein = __shfl_down_sync(kFull, N_.in, 1);
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const double wv = __shfl_up_sync(kFull, C_.v[r], 1);
-    const double ev = __shfl_down_sync(kFull, C_.v[r], 1);
-    const double swv = __shfl_up_sync(kFull, S_.v[r], 1);
-    const double nev = __shfl_down_sync(kFull, N_.v[r], 1);
-    double a = 0.0;
-    if (swin) a = xadd(a, xmul(swa, swv));
-    if (S_.in) a = xadd(a, xmul(ss.n, S_.v[r]));
-    if (win) a = xadd(a, xmul(wa, wv));
-    a = xadd(a, xmul(cs.c, C_.v[r]));
-    if (ein) a = xadd(a, xmul(cs.e, ev));
-    if (N_.in) a = xadd(a, xmul(cs.n, N_.v[r]));
-    if (nein) a = xadd(a, xmul(cs.ne, nev));
-    q[r] = a;
-  }
+  return k.valid && lane >= 2 && lane < 2 + kCgCols && k.col < S.w;
 }
 
 template <bool UNI>
-__device__ __forceinline__ double dinv_at(const SweepArgs& A, long long g) {
-  if constexpr (UNI) {
-    return A.udinv;
-  } else {
-    return A.dinv[g];
+__device__ __forceinline__ void load_old(const CgSys& S, const SweepArgs& A, int col, int ly,
+                                         const double* Rc, const double* Pc, const double* X,
+                                         ORow& o) {
+  o.p = o.r = o.x = 0.0;
+  o.in = 0;
+  if constexpr (!UNI) {
+    o.st = Stencil{0.0, 0.0, 0.0, 0.0};
+    o.dv = 0.0;
   }
-}
-
-// Loads row ly (ly outside [lo, hi) -> empty row) of this lane's column:
-// in-system flag, stencil and the source value (p_new = z + beta p for
-// kModeNormal, x for kModeCheck).
-template <int NR, int MODE, bool UNI>
-__device__ __forceinline__ void load_row(const CgSys& S, const SweepArgs& A, int col, int ly,
-                                         const double* R, const double* P, const double* X,
-                                         const double (&beta)[NR], const bool (&rst)[NR],
-                                         RowV<NR, UNI>& o) {
-  const bool inside = col >= 0 && col < S.w && ly >= 0 && ly < S.h;
-  if (!inside) {
-    zero_row<NR, UNI>(o);
-    return;
-  }
+  if (col < 0 || col >= S.w || ly < 0 || ly >= S.h) return;
   const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + col);
-  if (A.mask && !A.mask[g]) {
-    zero_row<NR, UNI>(o);
-    return;
-  }
+  if (A.mask && !in_strip(A.sg, S.x0 + col, S.y0 + ly)) return;
   o.in = 1;
-  if constexpr (!UNI) o.st = A.st[g];
-  const long long v = (S.voff + static_cast<long long>(ly) * S.w + col) * NR;
-  if (MODE == kModeNormal) {
-    double rv[NR], pv[NR];
-    ldv<NR>(R + v, rv);
-    ldv<NR>(P + v, pv);
-    const double dv = dinv_at<UNI>(A, g);
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const double z = xmul(dv, rv[r]);
-      o.v[r] = rst[r] ? z : xadd(z, xmul(beta[r], pv[r]));
-    }
-  } else {
-    ldv<NR>(X + v, o.v);
+  if constexpr (!UNI) {
+    o.st = A.st[g];
+    o.dv = A.dinv[g];
   }
+  const long long v = S.voff + static_cast<long long>(ly) * S.w + col;
+  o.p = Pc[v];
+  o.r = Rc[v];
+  o.x = X[v];
 }
 
-enum Phase { kPhaseInit = 0, kPhaseA = 1, kPhaseB = 2 };
+// Row product of the window-restricted matrix at the centre row of a 3-row
+// register window, terms in CSR column order SW,S,W,C,E,N,NE (sparse.cpp:69-76),
+// each rounded separately.  A coefficient is only used when its neighbour is
+// inside the system (an interior row), so the uniform stencil is exact there.
+template <bool UNI>
+__device__ __forceinline__ double product(double sv, const Stencil& sst, int sin_, double cv,
+                                          const Stencil& cst, int cin, double nv, int nin,
+                                          const SweepArgs& A) {
+  const Stencil& cs = UNI ? A.ust : cst;
+  const double sn = UNI ? A.ust.n : sst.n;
+  const double wa = UNI ? A.ust.e : __shfl_up_sync(kFull, cst.e, 1);
+  const double swa = UNI ? A.ust.ne : __shfl_up_sync(kFull, sst.ne, 1);
+  const int win = __shfl_up_sync(kFull, cin, 1);
+  const int ein = __shfl_down_sync(kFull, cin, 1);
+  const int swin = __shfl_up_sync(kFull, sin_, 1);
+  const int nein = __shfl_down_sync(kFull, nin, 1);
+  const double wv = __shfl_up_sync(kFull, cv, 1);
+  const double ev = __shfl_down_sync(kFull, cv, 1);
+  const double swv = __shfl_up_sync(kFull, sv, 1);
+  const double nev = __shfl_down_sync(kFull, nv, 1);
+  double a = 0.0;
+  if (swin) a = xadd(a, xmul(swa, swv));
+  if (sin_) a = xadd(a, xmul(sn, sv));
+  if (win) a = xadd(a, xmul(wa, wv));
+  a = xadd(a, xmul(cs.c, cv));
+  if (ein) a = xadd(a, xmul(cs.e, ev));
+  if (nin) a = xadd(a, xmul(cs.n, nv));
+  if (nein) a = xadd(a, xmul(cs.ne, nev));
+  return a;
+}
 
-// Scalar recurrences of cg_solve for one (system, rhs) after a phase's
-// reduction (a0, a1) -- sparse.cpp:199-258.
+enum Phase { kPhaseInit = 0, kPhaseIter = 1 };
+
+// Scalar recurrences of cg_solve for one system after a launch's reduction.
 template <int PH>
-__device__ __forceinline__ void update_ctl(CgCtl& c, double a0, double a1, double tol, int maxit) {
+__device__ __forceinline__ void update_ctl(CgCtl& c, const double (&a)[kCgDots], double tol,
+                                           int maxit) {
   if (PH == kPhaseInit) {
-    c.bnorm = sqrt(a0);
+    c.bnorm = sqrt(a[0]);
     c.iters = 0;
-    c.alpha = c.beta = 0.0;
-    c.mode_b = kModeSkip;
+    c.alpha = c.beta = c.rho = 0.0;
+    c.restart = 1;
     if (c.bnorm == 0.0) {  // sparse.cpp:208-212
       c.status = kConverged;
       c.final_res = 0.0;
-      c.mode_a = kModeSkip;
+      c.mode = kModeSkip;
     } else {
       c.status = kRunning;
-      c.rho = a1;
+      c.mode = kModeNormal;
+    }
+    return;
+  }
+  if (c.mode == kModeNormal) {
+    const bool updated = !c.restart;
+    if (updated) c.iters += 1;
+    if (updated && (sqrt(a[0]) <= tol * c.bnorm || c.iters >= maxit)) {
+      c.mode = kModeCheck;  // confirm with the true residual (sparse.cpp:232-246)
+      return;
+    }
+    const double pq = a[2];
+    if (pq <= 0.0) {  // sparse.cpp:225-226
+      c.status = kIndefinite;
+      c.mode = kModeSkip;
+      return;
+    }
+    const double rho = a[1];
+    const double alpha = rho / pq;
+    const double rho_next = rho - 2.0 * alpha * a[3] + alpha * alpha * a[4];
+    c.alpha = alpha;
+    c.beta = rho_next / rho;
+    c.rho = rho;
+    c.restart = 0;
+  } else if (c.mode == kModeCheck) {
+    const double true_rel = sqrt(a[0]) / c.bnorm;
+    if (true_rel <= tol) {
+      c.status = kConverged;
+      c.final_res = true_rel;
+      c.mode = kModeSkip;
+    } else if (c.iters >= maxit) {
+      c.status = kNotConverged;  // sparse.cpp:255-257
+      c.final_res = true_rel;
+      c.mode = kModeSkip;
+    } else {  // restart from the true residual: p = z, no pending update
       c.restart = 1;
-      c.mode_a = kModeNormal;
-    }
-  } else if (PH == kPhaseA) {
-    if (c.mode_a == kModeNormal) {
-      const double pq = a0;
-      if (pq <= 0.0) {  // sparse.cpp:225-226
-        c.status = kIndefinite;
-        c.mode_a = c.mode_b = kModeSkip;
-      } else {
-        c.alpha = c.rho / pq;
-        c.mode_b = kModeNormal;
-        c.mode_a = kModeSkip;
-      }
-    } else if (c.mode_a == kModeCheck) {  // true-residual confirmation (sparse.cpp:232-246)
-      const double true_rel = sqrt(a0) / c.bnorm;
-      if (true_rel <= tol) {
-        c.status = kConverged;
-        c.final_res = true_rel;
-        c.mode_a = c.mode_b = kModeSkip;
-      } else if (c.iters >= maxit) {
-        c.status = kNotConverged;  // sparse.cpp:255-257
-        c.final_res = true_rel;
-        c.mode_a = c.mode_b = kModeSkip;
-      } else {
-        c.rho = a1;
-        c.restart = 1;
-        c.mode_a = kModeNormal;
-        c.mode_b = kModeSkip;
-      }
-    }
-  } else if (c.mode_b == kModeNormal) {  // kPhaseB
-    c.iters += 1;
-    c.mode_b = kModeSkip;
-    if (sqrt(a0) <= tol * c.bnorm || c.iters >= maxit) {
-      c.mode_a = kModeCheck;
-    } else {
-      c.beta = a1 / c.rho;
-      c.rho = a1;
-      c.restart = 0;
-      c.mode_a = kModeNormal;
+      c.alpha = c.beta = 0.0;
+      c.mode = kModeNormal;
     }
   }
 }
@@ -252,10 +224,11 @@ struct Finish {
 // Block partial -> partials[tile]; the last tile of the system to arrive sums
 // all partials of the system in tile order (fixed, deterministic) and
 // advances its scalars.
-template <int NR, int PH>
-__device__ __forceinline__ void finish_tile(const CgSys& S, int sys, int t, double (&acc)[2 * NR],
-                                            const Finish& F) {
-  block_reduce_store<2 * NR, kBlock>(acc, F.part + static_cast<long long>(S.toff + t) * 2 * NR);
+template <int PH>
+__device__ __forceinline__ void finish_tile(const CgSys& S, int sys, int t,
+                                            double (&acc)[kCgDots], const Finish& F) {
+  block_reduce_store<kCgDots, kBlock>(acc,
+                                      F.part + static_cast<long long>(S.toff + t) * kCgDots);
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
@@ -266,226 +239,141 @@ __device__ __forceinline__ void finish_tile(const CgSys& S, int sys, int t, doub
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < NR; r += kCgWarps) {
-    double a0 = 0.0, a1 = 0.0;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double a[kCgDots];
+#pragma unroll
+    for (int q = 0; q < kCgDots; ++q) a[q] = 0.0;
     for (int tt = lane; tt < S.ntiles; tt += 32) {
-      const double* p = F.part + (static_cast<long long>(S.toff + tt) * NR + r) * 2;
-      a0 += __ldcg(p);
-      a1 += __ldcg(p + 1);
+      const double* p = F.part + static_cast<long long>(S.toff + tt) * kCgDots;
+#pragma unroll
+      for (int q = 0; q < kCgDots; ++q) a[q] += __ldcg(p + q);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(kFull, a0, o);
-      a1 += __shfl_xor_sync(kFull, a1, o);
-    }
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < kCgDots; ++q) a[q] += __shfl_xor_sync(kFull, a[q], o);
     if (lane == 0) {
-      CgCtl c = F.ctl[sys * NR + r];
-      update_ctl<PH>(c, a0, a1, F.tol, S.maxit);
-      F.ctl[sys * NR + r] = c;
+      CgCtl c = F.ctl[sys];
+      update_ctl<PH>(c, a, F.tol, S.maxit);
+      F.ctl[sys] = c;
+      F.counter[sys] = 0u;
     }
   }
-  if (threadIdx.x == 0) F.counter[sys] = 0u;
 }
 
-template <int NR, bool UNI>
+template <bool UNI>
 __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTile* tiles,
-                                                    SweepArgs A, const double* bsrc, double* X,
-                                                    double* R, Finish F) {
+                                                    SweepArgs A, const double* bsrc,
+                                                    int bstride, double* X, double* R,
+                                                    Finish F) {
   const CgTile tl = tiles[blockIdx.x];
   const CgSys S = sys[tl.sys];
   const Task k = task_of(S, tl.t);
-  double acc[2 * NR];
-#pragma unroll
-  for (int q = 0; q < 2 * NR; ++q) acc[q] = 0.0;
+  double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
   if (out_lane(S, k)) {
     for (int ly = k.ly0; ly < k.ly1; ++ly) {
       const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
-      const long long v = (S.voff + static_cast<long long>(ly) * S.w + k.col) * NR;
-      double b[NR], z0[NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) z0[r] = 0.0;
-      stv<NR>(X + v, z0);
-      if (A.mask && !A.mask[g]) {
-        stv<NR>(R + v, z0);
+      const long long v = S.voff + static_cast<long long>(ly) * S.w + k.col;
+      X[v] = 0.0;
+      if (A.mask && !in_strip(A.sg, S.x0 + k.col, S.y0 + ly)) {
+        R[v] = 0.0;
         continue;
       }
-      ldv<NR>(bsrc + g * NR, b);
-      const double dv = dinv_at<UNI>(A, g);
-      stv<NR>(R + v, b);
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        acc[2 * r] += b[r] * b[r];
-        acc[2 * r + 1] += b[r] * xmul(dv, b[r]);
-      }
+      const double b = bsrc[g * bstride + S.rhs];
+      R[v] = b;
+      acc[0] += b * b;
     }
   }
-  finish_tile<NR, kPhaseInit>(S, tl.sys, tl.t, acc, F);
+  finish_tile<kPhaseInit>(S, tl.sys, tl.t, acc, F);
 }
 
-// Rows per load group of the normal sweep: narrow batches are latency-bound
-// and need several rows in flight per warp.
-template <int NR, bool UNI>
-struct Unroll {
-  static constexpr int value = NR == 1 ? 4 : (NR == 2 ? 2 : (UNI ? 2 : 1));
-};
-
-template <int NR, bool UNI>
-__global__ void __launch_bounds__(kBlock, 4)
-    k_cg_a(const CgSys* sys, const CgTile* tiles, SweepArgs A, const double* bsrc,
-           const double* __restrict__ X, double* __restrict__ R, const double* __restrict__ Pin,
-           double* __restrict__ Pout, double* __restrict__ Q, Finish F) {
+template <bool UNI>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_iter(const CgSys* sys, const CgTile* tiles, SweepArgs A, const double* bsrc,
+              int bstride, double* __restrict__ X, const double* __restrict__ Rc,
+              double* __restrict__ Rn, const double* __restrict__ Pc, double* __restrict__ Pn,
+              Finish F) {
   const CgTile tl = tiles[blockIdx.x];
   const CgSys S = sys[tl.sys];
-  __shared__ double s_beta[NR];
-  __shared__ int s_mode[NR], s_restart[NR];
-  if (threadIdx.x < NR) {
-    const CgCtl c = F.ctl[tl.sys * NR + threadIdx.x];
-    s_beta[threadIdx.x] = c.beta;
-    s_mode[threadIdx.x] = c.mode_a;
-    s_restart[threadIdx.x] = c.restart;
-  }
+  __shared__ CgCtl s_c;
+  if (threadIdx.x == 0) s_c = F.ctl[tl.sys];
   __syncthreads();
-  bool any_normal = false, any_check = false;
-  double beta[NR];
-  bool rst[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    any_normal |= s_mode[r] == kModeNormal;
-    any_check |= s_mode[r] == kModeCheck;
-    beta[r] = s_beta[r];
-    rst[r] = s_restart[r] != 0;
-  }
-  if (!any_normal && !any_check) return;  // uniform across the system's tiles
+  const int mode = s_c.mode;
+  if (mode == kModeSkip) return;  // uniform across the system's tiles
+  const double al = s_c.alpha, be = s_c.beta;
+  const bool rst = s_c.restart != 0;
   const Task k = task_of(S, tl.t);
   const bool out = out_lane(S, k);
-  double acc[2 * NR];
-#pragma unroll
-  for (int q = 0; q < 2 * NR; ++q) acc[q] = 0.0;
-  if (any_normal && k.valid) {
-    constexpr int U = Unroll<NR, UNI>::value;
-    using Row = RowV<NR, UNI>;
-    Row S_, C_, N_;
-    load_row<NR, kModeNormal, UNI>(S, A, k.col, k.ly0 - 1, R, Pin, X, beta, rst, S_);
-    load_row<NR, kModeNormal, UNI>(S, A, k.col, k.ly0, R, Pin, X, beta, rst, C_);
-    load_row<NR, kModeNormal, UNI>(S, A, k.col, k.ly0 + 1, R, Pin, X, beta, rst, N_);
-    for (int ly = k.ly0; ly < k.ly1; ly += U) {
-      Row G[U];  // rows ly+2 .. ly+U+1, loads issued together
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int row = ly + 2 + u;
-        load_row<NR, kModeNormal, UNI>(S, A, k.col, row <= k.ly1 ? row : -1, R, Pin, X, beta,
-                                       rst, G[u]);
+  double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (k.valid && mode == kModeNormal) {
+    ORow a, b, c, d;  // old iterate at rows n-1, n, n+1 (and n+2 in flight)
+    NRow s, m;        // new p at rows n-2, n-1
+    load_old<UNI>(S, A, k.col, k.ly0 - 2, Rc, Pc, X, a);
+    load_old<UNI>(S, A, k.col, k.ly0 - 1, Rc, Pc, X, b);
+    load_old<UNI>(S, A, k.col, k.ly0, Rc, Pc, X, c);
+    s.in = m.in = 0;
+    s.p = s.z = m.p = m.z = 0.0;
+    s.dv = m.dv = 0.0;
+    s.st = m.st = Stencil{0.0, 0.0, 0.0, 0.0};
+    for (int n = k.ly0 - 1; n <= k.ly1; ++n) {  // warp-uniform trip count
+      load_old<UNI>(S, A, k.col, n + 2 <= k.ly1 + 1 ? n + 2 : -1, Rc, Pc, X, d);
+      // stage 1 at row n: pending update, z, new p
+      double rn = b.r, xn = b.x;
+      if (!rst) {
+        const double qo = product<UNI>(a.p, a.st, a.in, b.p, b.st, b.in, c.p, c.in, A);
+        rn = xsub(b.r, xmul(al, qo));
+        xn = xadd(b.x, xmul(al, b.p));
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int yy = ly + u;
-        if (yy < k.ly1) {  // warp-uniform
-          double q[NR];
-          window_row_product<NR, UNI>(S_, C_, N_, A, q);
-          if (out && C_.in) {
-            const long long v = (S.voff + static_cast<long long>(yy) * S.w + k.col) * NR;
-            stv<NR>(Pout + v, C_.v);
-            stv<NR>(Q + v, q);
-#pragma unroll
-            for (int r = 0; r < NR; ++r) acc[2 * r] += C_.v[r] * q[r];
-          }
+      const double dv = UNI ? A.udinv : b.dv;
+      NRow t;
+      t.z = xmul(dv, rn);
+      t.p = rst ? t.z : xadd(t.z, xmul(be, b.p));
+      t.dv = dv;
+      t.st = b.st;
+      t.in = b.in;
+      if (out && b.in && n >= k.ly0 && n < k.ly1) {
+        const long long v = S.voff + static_cast<long long>(n) * S.w + k.col;
+        X[v] = xn;
+        Rn[v] = rn;
+        Pn[v] = t.p;
+        acc[0] += rn * rn;
+        acc[1] += rn * t.z;
+      }
+      // stage 2 at row n-1: q = A p_new, dots for alpha and the rho recurrence
+      if (n - 1 >= k.ly0) {
+        const double q = product<UNI>(s.p, s.st, s.in, m.p, m.st, m.in, t.p, t.in, A);
+        if (out && m.in) {
+          acc[2] += m.p * q;
+          acc[3] += q * m.z;
+          acc[4] += q * xmul(m.dv, q);
         }
-        S_ = C_;
-        C_ = N_;
-        N_ = G[u];
       }
+      s = m;
+      m = t;
+      a = b;
+      b = c;
+      c = d;
     }
-  }
-  if (any_check && k.valid) {
-    // True residual r = b - A x for the right-hand sides under confirmation.
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-      if (s_mode[r] == kModeCheck) acc[2 * r] = acc[2 * r + 1] = 0.0;
-    RowV<NR, UNI> S_, C_, N_;
-    load_row<NR, kModeCheck, UNI>(S, A, k.col, k.ly0 - 1, R, Pin, X, beta, rst, S_);
-    load_row<NR, kModeCheck, UNI>(S, A, k.col, k.ly0, R, Pin, X, beta, rst, C_);
+  } else if (k.valid) {  // kModeCheck: r = b - A x (x is current: updated in place)
+    ORow a, b, c;
+    load_old<UNI>(S, A, k.col, k.ly0 - 1, Rc, Pc, X, a);
+    load_old<UNI>(S, A, k.col, k.ly0, Rc, Pc, X, b);
     for (int ly = k.ly0; ly < k.ly1; ++ly) {
-      load_row<NR, kModeCheck, UNI>(S, A, k.col, ly + 1, R, Pin, X, beta, rst, N_);
-      double ax[NR];
-      window_row_product<NR, UNI>(S_, C_, N_, A, ax);
-      if (out && C_.in) {
+      load_old<UNI>(S, A, k.col, ly + 1, Rc, Pc, X, c);
+      const double ax = product<UNI>(a.x, a.st, a.in, b.x, b.st, b.in, c.x, c.in, A);
+      if (out && b.in) {
         const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
-        const long long v = (S.voff + static_cast<long long>(ly) * S.w + k.col) * NR;
-        double b[NR], rv[NR];
-        ldv<NR>(bsrc + g * NR, b);
-        ldv<NR>(R + v, rv);
-        const double dv = dinv_at<UNI>(A, g);
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          if (s_mode[r] != kModeCheck) continue;
-          const double rt = xsub(b[r], ax[r]);
-          rv[r] = rt;
-          acc[2 * r] += rt * rt;
-          acc[2 * r + 1] += rt * xmul(dv, rt);
-        }
-        stv<NR>(R + v, rv);
+        const long long v = S.voff + static_cast<long long>(ly) * S.w + k.col;
+        const double rt = xsub(bsrc[g * bstride + S.rhs], ax);
+        Rn[v] = rt;
+        acc[0] += rt * rt;
       }
-      S_ = C_;
-      C_ = N_;
+      a = b;
+      b = c;
     }
   }
-  finish_tile<NR, kPhaseA>(S, tl.sys, tl.t, acc, F);
-}
-
-template <int NR, bool UNI>
-__global__ void __launch_bounds__(kBlock)
-    k_cg_b(const CgSys* sys, const CgTile* tiles, SweepArgs A, double* __restrict__ X,
-           double* __restrict__ R, const double* __restrict__ P, const double* __restrict__ Q,
-           Finish F) {
-  const CgTile tl = tiles[blockIdx.x];
-  const CgSys S = sys[tl.sys];
-  __shared__ double s_alpha[NR];
-  __shared__ int s_mode[NR];
-  if (threadIdx.x < NR) {
-    const CgCtl c = F.ctl[tl.sys * NR + threadIdx.x];
-    s_alpha[threadIdx.x] = c.alpha;
-    s_mode[threadIdx.x] = c.mode_b;
-  }
-  __syncthreads();
-  bool any = false, upd[NR];
-  double alpha[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    upd[r] = s_mode[r] == kModeNormal;
-    any |= upd[r];
-    alpha[r] = s_alpha[r];
-  }
-  if (!any) return;  // uniform across the system's tiles
-  const Task k = task_of(S, tl.t);
-  double acc[2 * NR];
-#pragma unroll
-  for (int q = 0; q < 2 * NR; ++q) acc[q] = 0.0;
-  if (out_lane(S, k)) {
-#pragma unroll 4
-    for (int ly = k.ly0; ly < k.ly1; ++ly) {
-      const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
-      if (A.mask && !A.mask[g]) continue;
-      const long long v = (S.voff + static_cast<long long>(ly) * S.w + k.col) * NR;
-      double x[NR], r[NR], p[NR], q[NR];
-      ldv<NR>(X + v, x);
-      ldv<NR>(R + v, r);
-      ldv<NR>(P + v, p);
-      ldv<NR>(Q + v, q);
-      const double dv = dinv_at<UNI>(A, g);
-#pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        if (!upd[j]) continue;
-        x[j] = xadd(x[j], xmul(alpha[j], p[j]));
-        r[j] = xsub(r[j], xmul(alpha[j], q[j]));
-        acc[2 * j] += r[j] * r[j];
-        acc[2 * j + 1] += r[j] * xmul(dv, r[j]);
-      }
-      stv<NR>(X + v, x);
-      stv<NR>(R + v, r);
-    }
-  }
-  finish_tile<NR, kPhaseB>(S, tl.sys, tl.t, acc, F);
+  finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
 }
 
 SweepArgs sweep_args(const Level& L, const unsigned char* mask) {
@@ -494,66 +382,28 @@ SweepArgs sweep_args(const Level& L, const unsigned char* mask) {
   A.dinv = L.dinv.get();
   A.nxp1 = L.nx + 1;
   A.mask = mask;
+  A.sg = L.strip_geom;
   A.ust = L.ust;
   A.udinv = L.udinv;
   return A;
 }
 
-template <int NR>
-void launch_init(bool uni, unsigned ntiles, cudaStream_t st, const CgSys* sys,
-                 const CgTile* tiles, const SweepArgs& A, const double* bsrc, double* X,
-                 double* R, const Finish& F) {
-  if (uni)
-    k_cg_init<NR, true><<<ntiles, kBlock, 0, st>>>(sys, tiles, A, bsrc, X, R, F);
-  else
-    k_cg_init<NR, false><<<ntiles, kBlock, 0, st>>>(sys, tiles, A, bsrc, X, R, F);
-}
-template <int NR>
-void launch_a(bool uni, unsigned ntiles, cudaStream_t st, const CgSys* sys, const CgTile* tiles,
-              const SweepArgs& A, const double* bsrc, const double* X, double* R,
-              const double* Pin, double* Pout, double* Q, const Finish& F) {
-  if (uni)
-    k_cg_a<NR, true><<<ntiles, kBlock, 0, st>>>(sys, tiles, A, bsrc, X, R, Pin, Pout, Q, F);
-  else
-    k_cg_a<NR, false><<<ntiles, kBlock, 0, st>>>(sys, tiles, A, bsrc, X, R, Pin, Pout, Q, F);
-}
-template <int NR>
-void launch_b(bool uni, unsigned ntiles, cudaStream_t st, const CgSys* sys, const CgTile* tiles,
-              const SweepArgs& A, double* X, double* R, const double* P, const double* Q,
-              const Finish& F) {
-  if (uni)
-    k_cg_b<NR, true><<<ntiles, kBlock, 0, st>>>(sys, tiles, A, X, R, P, Q, F);
-  else
-    k_cg_b<NR, false><<<ntiles, kBlock, 0, st>>>(sys, tiles, A, X, R, P, Q, F);
-}
-
-#define MLG_NR_DISPATCH(nr, fn, ...)                                      \
-  do {                                                                    \
-    switch (nr) {                                                         \
-      case 1: fn<1>(__VA_ARGS__); break;                                  \
-      case 2: fn<2>(__VA_ARGS__); break;                                  \
-      case 4: fn<4>(__VA_ARGS__); break;                                  \
-      case 8: fn<8>(__VA_ARGS__); break;                                  \
-      default: throw ConfigError("unsupported right-hand-side batch width"); \
-    }                                                                     \
-  } while (0)
-
 }  // namespace
 
-void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems, int nr_,
-                    const unsigned char* mask_, const double* bsrc_) {
+void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
+                    const unsigned char* mask_, const double* bsrc_, int bstride_) {
   L = &lev;
-  nr = nr_;
   mask = mask_;
   bsrc = bsrc_;
+  bstride = bstride_;
   total_rows = 0;
   total_tiles = 0;
   long long all_rows = 0;
   for (const CgSys& s : systems) all_rows += static_cast<long long>(s.w) * s.h;
   // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
-  // must still offer >= ~4k warps (148 SMs x ~28 resident) to hide latency.
+  // must still offer >= ~8k warps (148 SMs x ~56 resident) to hide latency.
   const int krows = static_cast<int>(
-      std::min<long long>(kCgRows, std::max<long long>(16, all_rows / (kCgCols * 4096LL))));
+      std::min<long long>(kCgRows, std::max<long long>(16, all_rows / (kCgCols * 8192LL))));
   for (CgSys& s : systems) {
     s.nrows = s.w * s.h;
     s.voff = total_rows;
@@ -568,17 +418,16 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems, int nr
     total_tiles += s.ntiles;
   }
   sys_h = std::move(systems);
-  const std::size_t nv = static_cast<std::size_t>(total_rows) * nr;
+  const std::size_t nv = static_cast<std::size_t>(total_rows);
   X.ensure(nv);
-  R.ensure(nv);
+  R0.ensure(nv);
+  R1.ensure(nv);
   P0.ensure(nv);
   P1.ensure(nv);
-  Q.ensure(nv);
-  partA.ensure(static_cast<std::size_t>(total_tiles) * 2 * nr);
-  partB.ensure(static_cast<std::size_t>(total_tiles) * 2 * nr);
+  part.ensure(static_cast<std::size_t>(total_tiles) * kCgDots);
   sys_d.ensure(sys_h.size());
   sys_d.upload(sys_h.data(), sys_h.size(), c.stream);
-  ctl_d.ensure(sys_h.size() * nr);
+  ctl_d.ensure(sys_h.size());
   ctl_d.zero(c.stream);
   counters.ensure(sys_h.size());
   counters.zero(c.stream);
@@ -608,56 +457,57 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
   cudaStream_t st = c.stream;
   const bool uni = L->uniform != 0;
   const SweepArgs A = sweep_args(*L, mask);
-  const Finish FA{partA.get(), counters.get(), ctl_d.get(), tol};
-  const Finish FB{partB.get(), counters.get(), ctl_d.get(), tol};
+  const Finish F{part.get(), counters.get(), ctl_d.get(), tol};
+  double *rc = R0.get(), *rn = R1.get(), *pc = P0.get(), *pn = P1.get();
 
-  MLG_NR_DISPATCH(nr, launch_init, uni, static_cast<unsigned>(tiles.size()), st, sys_d.get(),
-                  tiles_d.get(), A, bsrc, X.get(), R.get(), FA);
+  if (uni)
+    k_cg_init<true><<<static_cast<unsigned>(tiles.size()), kBlock, 0, st>>>(
+        sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, F);
+  else
+    k_cg_init<false><<<static_cast<unsigned>(tiles.size()), kBlock, 0, st>>>(
+        sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, F);
   MLG_LAUNCH_CHECK();
 
-  std::vector<CgCtl> ctl(static_cast<std::size_t>(nsys) * nr);
-  double* pin = P0.get();
-  double* pout = P1.get();
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<CgCtl> ctl(static_cast<std::size_t>(nsys));
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
   int chunk = 16;
   long long iter_count = 0;
   while (true) {
     for (int it = 0; it < chunk && !tiles.empty(); ++it) {
       const unsigned nt = static_cast<unsigned>(tiles.size());
-      // Kernel timing evidence: every 4th local-solve SpMV launch is bracketed
-      // by pooled CUDA events (cheap enough not to starve the stream).
+      // Kernel timing evidence: every 4th launch of the local solves is
+      // bracketed by pooled CUDA events (cheap enough not to starve the stream).
       const bool prof = c.profile && mask == nullptr && (iter_count++ % 4 == 0);
+      cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (prof) {
         c.times.ka_rows += static_cast<double>(active_rows);
         ev0 = c.event(2 * evs.size());
         ev1 = c.event(2 * evs.size() + 1);
         MLG_CUDA(cudaEventRecord(ev0, st));
       }
-      MLG_NR_DISPATCH(nr, launch_a, uni, nt, st, sys_d.get(), tiles_d.get(), A, bsrc, X.get(),
-                      R.get(), pin, pout, Q.get(), FA);
+      if (uni)
+        k_cg_iter<true><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc, bstride,
+                                               X.get(), rc, rn, pc, pn, F);
+      else
+        k_cg_iter<false><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc, bstride,
+                                                X.get(), rc, rn, pc, pn, F);
       MLG_LAUNCH_CHECK();
       if (prof) {
         MLG_CUDA(cudaEventRecord(ev1, st));
         evs.emplace_back(ev0, ev1);
       }
-      MLG_NR_DISPATCH(nr, launch_b, uni, nt, st, sys_d.get(), tiles_d.get(), A, X.get(), R.get(),
-                      pout, Q.get(), FB);
-      MLG_LAUNCH_CHECK();
-      std::swap(pin, pout);
+      std::swap(rc, rn);
+      std::swap(pc, pn);
     }
     ctl_d.download(ctl.data(), ctl.size(), st);
     c.sync();
     bool running = false;
     bool changed = false;
     for (int s = 0; s < nsys; ++s) {
-      bool sys_running = false;
-      for (int r = 0; r < nr; ++r) {
-        const CgCtl& k = ctl[static_cast<std::size_t>(s) * nr + r];
-        if (k.status == kIndefinite)
-          throw SolverError("cg_solve: matrix is not positive definite (p'Mp <= 0)");
-        if (k.status == kRunning) sys_running = true;
-      }
+      const CgCtl& k = ctl[static_cast<std::size_t>(s)];
+      if (k.status == kIndefinite)
+        throw SolverError("cg_solve: matrix is not positive definite (p'Mp <= 0)");
+      const bool sys_running = k.status == kRunning;
       if (active[s] && !sys_running) {
         active[s] = 0;
         changed = true;
@@ -668,13 +518,11 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     if (changed) rebuild(active);
     chunk = std::min(64, chunk * 2);
   }
-  if (!evs.empty()) {
-    for (auto& e : evs) {
-      float ms = 0.f;
-      MLG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
-      c.times.ka_ms_sum += ms;
-      c.times.ka_launches += 1;
-    }
+  for (auto& e : evs) {
+    float ms = 0.f;
+    MLG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+    c.times.ka_ms_sum += ms;
+    c.times.ka_launches += 1;
   }
   c.times.ka_uniform = uni ? 1 : 0;
   CgResult res;

@@ -1,9 +1,9 @@
 // Batched Jacobi-PCG over many lattice-window systems at once (the local
-// Dirichlet solves of all subdomains x eigenvectors, or the strip solve).
-// Semantics are the reference's cg_solve (sparse.cpp:199-258), per system and
-// per right-hand side: x0 = 0; zero rhs returns after 0 iterations; stop when
-// ||r|| <= tol ||b|| *confirmed by the true residual* (else restart from it);
-// maxit = 10 n; p'Ap <= 0 is an error; non-convergence is reported.
+// Dirichlet solves of all subdomains x eigenvectors, or the strip solves).
+// Semantics are the reference's cg_solve (sparse.cpp:199-258), per system:
+// x0 = 0; zero rhs returns after 0 iterations; stop when ||r|| <= tol ||b||
+// *confirmed by the true residual* (else restart from it); maxit = 10 n;
+// p'Ap <= 0 is an error; non-convergence is reported.
 #pragma once
 
 #include <vector>
@@ -12,18 +12,20 @@
 
 namespace mlg {
 
-// A system is a rectangular window [x0, x0+w) x [y0, y0+h) of the fine
-// full lattice (interior dofs only) optionally restricted by a byte mask; its
+// A system is a rectangular window [x0, x0+w) x [y0, y0+h) of the fine full
+// lattice (interior dofs only), optionally restricted by a byte mask, for ONE
+// right-hand side (lane `rhs` of the rhs-interleaved source vector); its
 // matrix is the window (mask) restriction of the level's stiffness, exactly
 // extract_submatrix (sparse.cpp:156-174).  Vectors are window-compact,
-// row-major, NR right-hand sides interleaved.
+// row-major.
 //
-// Work decomposition: a warp task is one column strip (32 lanes covering 30
-// output columns plus one halo column each side) of kCgRows window rows,
-// swept bottom to top with a 3-row register window; a CTA ("tile") runs
-// kCgWarps consecutive tasks of one system and owns one partial-sum slot.
+// Work decomposition: a warp task is one column strip (32 lanes covering
+// kCgCols output columns plus a 2-column halo each side) of `krows` window
+// rows, swept bottom to top; a CTA ("tile") runs kCgWarps consecutive tasks of
+// one system and owns one partial-sum slot.
 struct CgSys {
   int x0, y0, w, h;
+  int rhs;         // lane of the rhs-interleaved source (b) vector
   long long voff;  // first row in the pooled vectors
   int toff;        // first tile id (partials index)
   int ntiles;
@@ -39,18 +41,19 @@ struct CgTile {
 
 struct CgCtl {
   double alpha, beta, rho, bnorm, final_res;
-  int mode_a, mode_b, iters, status, restart, pad;
+  int mode, restart, iters, status;
 };
 
 enum : int { kModeSkip = 0, kModeNormal = 1, kModeCheck = 2 };
 enum : int { kRunning = 0, kConverged = 1, kNotConverged = 2, kIndefinite = 3 };
 
 constexpr int kCgWarps = 4;     // warps (tasks) per CTA
-constexpr int kCgCols = 30;     // output columns per warp task
+constexpr int kCgCols = 28;     // output columns per warp task (2 halo lanes each side)
 constexpr int kCgRows = 64;     // max window rows per warp task
+constexpr int kCgDots = 5;      // partial sums per tile
 
 struct CgResult {
-  std::vector<SolveReport> reports;  // [sys * nr + rhs]
+  std::vector<SolveReport> reports;  // [sys]
   int iters_max = 0;
 };
 
@@ -59,21 +62,21 @@ class CgBatch {
   static constexpr int kBlock = 32 * kCgWarps;
 
   // Lays out systems (computing voff/toff/ntiles) and sizes the pools.
-  void setup(Ctx& c, const Level& L, std::vector<CgSys> systems, int nr,
-             const unsigned char* mask, const double* bsrc);
+  // bsrc: rhs-interleaved full-lattice source, bstride = its lane count.
+  void setup(Ctx& c, const Level& L, std::vector<CgSys> systems, const unsigned char* mask,
+             const double* bsrc, int bstride);
   // Runs to completion; throws SolverError for p'Ap <= 0.
   CgResult solve(Ctx& c, double tol, int maxit_override = 0);
 
   const double* x() const { return X.get(); }
-  double* x_mut() { return X.get(); }
   const std::vector<CgSys>& systems() const { return sys_h; }
   const CgSys* sys_dev() const { return sys_d.get(); }
-  int nr = 1;
 
  private:
   const Level* L = nullptr;
   const unsigned char* mask = nullptr;
   const double* bsrc = nullptr;
+  int bstride = 1;
   std::vector<CgSys> sys_h;
   long long total_rows = 0;
   int total_tiles = 0;
@@ -81,7 +84,7 @@ class CgBatch {
   DevBuf<CgTile> tiles_d;
   DevBuf<CgCtl> ctl_d;
   DevBuf<unsigned> counters;  // per-system tile arrival counters (last-tile reduction)
-  DevBuf<double> X, R, P0, P1, Q, partA, partB;
+  DevBuf<double> X, R0, R1, P0, P1, part;
 };
 
 }  // namespace mlg

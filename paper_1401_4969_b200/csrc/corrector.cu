@@ -226,9 +226,10 @@ __global__ void k_strip_mask(int nx, int ny, PartDev P, unsigned char* mask) {
 }
 
 // glued = u + e_j on the closed G_j (bitwise, corrector.cpp:223-231); 0 elsewhere.
-// e_j comes from the batched local CG (window-compact X of system j) ...
+// e_j of eigenvector r comes from the batched local CG: system j*nev + r
+// (window-compact X) ...
 template <int NR>
-__global__ void k_glue_cg(int nx, int ny, PartDev P, const CgSys* sys, const double* X,
+__global__ void k_glue_cg(int nx, int ny, PartDev P, int nev, const CgSys* sys, const double* X,
                           const double* u, double* glued) {
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(nx + 1) * (ny + 1)) return;
@@ -239,13 +240,15 @@ __global__ void k_glue_cg(int nx, int ny, PartDev P, const CgSys* sys, const dou
   if (ix > 0 && iy > 0 && ix < nx && iy < ny) {
     const int j = inner_owner(P, ix, iy);
     if (j >= 0) {
-      const CgSys S = sys[j];
-      const long long i = static_cast<long long>(iy - S.y0) * S.w + (ix - S.x0);
-      double uu[NR], e[NR];
+      double uu[NR];
       ldv<NR>(u + d * NR, uu);
-      ldv<NR>(X + (S.voff + i) * NR, e);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) y[r] = xadd(uu[r], e[r]);
+      for (int r = 0; r < NR; ++r) {
+        if (r >= nev) break;
+        const CgSys S = sys[j * nev + r];
+        const long long i = static_cast<long long>(iy - S.y0) * S.w + (ix - S.x0);
+        y[r] = xadd(uu[r], X[S.voff + i]);
+      }
     }
   }
   stv<NR>(glued + d * NR, y);
@@ -265,16 +268,20 @@ __global__ void k_glue_full(int nx, int ny, PartDev P, long long ndofs, const do
   glued[d] = y;
 }
 
+// glued[strip dofs, lane r] = x of strip system r (same window for all r).
 template <int NR>
-__global__ void k_strip_scatter(int nx, const CgSys* sys, const unsigned char* mask,
+__global__ void k_strip_scatter(int nx, int nev, const CgSys* sys, const unsigned char* mask,
                                 const double* X, double* glued) {
-  const CgSys S = sys[0];
+  const CgSys S0 = sys[0];
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (i >= S.nrows) return;
-  const long long d = static_cast<long long>(S.y0 + i / S.w) * (nx + 1) + (S.x0 + i % S.w);
+  if (i >= S0.nrows) return;
+  const long long d = static_cast<long long>(S0.y0 + i / S0.w) * (nx + 1) + (S0.x0 + i % S0.w);
   if (!mask[d]) return;
   double x[NR];
-  ldv<NR>(X + (S.voff + i) * NR, x);
+  ldv<NR>(glued + d * NR, x);
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    if (r < nev) x[r] = X[sys[r].voff + i];
   stv<NR>(glued + d * NR, x);
 }
 
@@ -896,14 +903,23 @@ static std::string fmt_report(const SolveReport& r) {
          std::to_string(r.final_residual) + ")";
 }
 
-// All local corrections e_{i,j} in one batched CG; e_j of rhs lane i lives in
-// the window-compact X of system j (never expanded to N-length vectors).
-int local_solves(Ctx& c, const Level& F, int nr, const double* res, double tol, int maxit,
-                 std::vector<SolveReport>* reports, int only_j) {
+// All local corrections e_{i,j} in one batched CG: system j*nev + i solves
+// subdomain j for eigenvector i (lane i of the interleaved residual); e_{i,j}
+// lives in its window-compact X (never expanded to N-length vectors).
+int local_solves(Ctx& c, const Level& F, int nr, int nev, const double* res, double tol,
+                 int maxit, std::vector<SolveReport>* reports, int only_j) {
   Workspace& w = W(c);
-  std::vector<CgSys> sys = local_systems(c, F.level);
-  if (only_j >= 0) sys = {sys.at(only_j)};
-  w.local.setup(c, F, std::move(sys), nr, nullptr, res);
+  const std::vector<CgSys> win = local_systems(c, F.level);
+  std::vector<CgSys> sys;
+  for (int j = 0; j < c.part.m; ++j) {
+    if (only_j >= 0 && j != only_j) continue;
+    for (int i = 0; i < nev; ++i) {
+      CgSys s = win[j];
+      s.rhs = i;
+      sys.push_back(s);
+    }
+  }
+  w.local.setup(c, F, std::move(sys), nullptr, res, nr);
   const CgResult r = w.local.solve(c, tol, maxit);
   if (reports) *reports = r.reports;
   return r.iters_max;
@@ -911,6 +927,14 @@ int local_solves(Ctx& c, const Level& F, int nr, const double* res, double tol, 
 
 void ensure_strip_mask(Ctx& c, Level& F) {
   if (!F.strip_mask.empty()) return;
+  StripGeom& g = F.strip_geom;
+  g.side = c.part.side;
+  g.bw = c.part.nx0 / c.part.side;
+  g.bh = c.part.ny0 / c.part.side;
+  g.dc = c.part.delta_cells;
+  g.nx0 = c.part.nx0;
+  g.ny0 = c.part.ny0;
+  g.scale = 1 << F.level;
   F.strip_mask.alloc(F.ndofs());
   k_strip_mask<<<grid_for(F.ndofs(), kB), kB, 0, c.stream>>>(F.nx, F.ny, part_dev(c, F.level),
                                                              F.strip_mask.get());
@@ -918,8 +942,9 @@ void ensure_strip_mask(Ctx& c, Level& F) {
 }
 
 // Step 2 after gluing: strip solve on the interior window masked to the strip.
-int strip_solve(Ctx& c, Level& F, int nr, const double* u, const Lam& lam, double* glued,
-                double tol, int maxit, std::vector<SolveReport>* reports, bool* empty) {
+int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const Lam& lam,
+                double* glued, double tol, int maxit, std::vector<SolveReport>* reports,
+                bool* empty) {
   Workspace& w = W(c);
   ensure_strip_mask(c, F);
   bool any_strip = false;
@@ -932,17 +957,22 @@ int strip_solve(Ctx& c, Level& F, int nr, const double* u, const Lam& lam, doubl
   w.load.ensure(F.ndofs() * nr);
   NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.nx, F.ny, F.stA.get(), F.stM.get(), u,
               glued, lam, w.load.get(), F.strip_mask.get());
-  CgSys s{};
-  s.x0 = 1;
-  s.y0 = 1;
-  s.w = F.nx - 1;
-  s.h = F.ny - 1;
-  w.strip.setup(c, F, {s}, nr, F.strip_mask.get(), w.load.get());
+  std::vector<CgSys> sys;
+  for (int i = 0; i < nev; ++i) {
+    CgSys s{};
+    s.x0 = 1;
+    s.y0 = 1;
+    s.w = F.nx - 1;
+    s.h = F.ny - 1;
+    s.rhs = i;
+    sys.push_back(s);
+  }
+  const long long rows = static_cast<long long>(F.nx - 1) * (F.ny - 1);
+  w.strip.setup(c, F, std::move(sys), F.strip_mask.get(), w.load.get(), nr);
   const CgResult r = w.strip.solve(c, tol, maxit);
   if (reports) *reports = r.reports;
-  NR_DISPATCH(nr, k_strip_scatter, grid_for(static_cast<long long>(s.w) * s.h, kB), F.nx,
-              w.strip.sys_dev(), F.strip_mask.get(), w.strip.x(),
-              glued);
+  NR_DISPATCH(nr, k_strip_scatter, grid_for(rows, kB), F.nx, nev, w.strip.sys_dev(),
+              F.strip_mask.get(), w.strip.x(), glued);
   return r.iters_max;
 }
 
@@ -1094,10 +1124,11 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
   NR_DISPATCH(nr, k_residual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), w.u.get(),
               w.u.get(), lam, w.res.get(), nullptr);
   std::vector<SolveReport> lrep;
-  out.times.local_iters_max = local_solves(c, F, nr, w.res.get(), c.cfg.cg_tol, 0, &lrep);
+  out.times.local_iters_max =
+      local_solves(c, F, nr, nev, w.res.get(), c.cfg.cg_tol, 0, &lrep);
   for (int i = 0; i < nev; ++i)  // task order i*m + j (parallel_tasks with one worker)
     for (int j = 0; j < c.part.m; ++j) {
-      const SolveReport& r = lrep[static_cast<std::size_t>(j) * nr + i];
+      const SolveReport& r = lrep[static_cast<std::size_t>(j) * nev + i];
       if (!r.converged)
         throw SolverError("subdomain " + std::to_string(j + 1) + " solve did not converge " +
                           fmt_report(r));
@@ -1105,13 +1136,13 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
   Timer t1(c.stream);
 
   w.glued.ensure(nd * nr);
-  NR_DISPATCH(nr, k_glue_cg, grid_for(nd, kB), F.nx, F.ny, part_dev(c, to),
-              w.local.sys_dev(), w.local.x(), w.u.get(),
-              w.glued.get());
+  NR_DISPATCH(nr, k_glue_cg, grid_for(nd, kB), F.nx, F.ny, part_dev(c, to), nev,
+              w.local.sys_dev(), w.local.x(), w.u.get(), w.glued.get());
   std::vector<SolveReport> srep;
   bool empty = false;
   out.times.strip_iters_max =
-      strip_solve(c, F, nr, w.u.get(), lam, w.glued.get(), c.cfg.cg_tol, 0, &srep, &empty);
+      strip_solve(c, F, nr, nev, w.u.get(), lam, w.glued.get(), c.cfg.cg_tol, 0, &srep,
+                  &empty);
   for (int i = 0; i < nev && !empty; ++i)
     if (!srep[i].converged)
       throw SolverError("strip solve did not converge " + fmt_report(srep[i]));

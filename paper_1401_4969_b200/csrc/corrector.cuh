@@ -30,12 +30,14 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
 std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double* glued, int nev,
                               DevBuf<double>& u_out);
 
-int local_solves(Ctx& c, const Level& F, int nr, const double* res, double tol, int maxit,
-                 std::vector<SolveReport>* reports, int only_j = -1);
+// Batched local solves; reports[j * nev + i] for subdomain j, eigenvector i.
+int local_solves(Ctx& c, const Level& F, int nr, int nev, const double* res, double tol,
+                 int maxit, std::vector<SolveReport>* reports, int only_j = -1);
 // The batched local CG of the last local_solves call (X holds e_j per window).
 const CgBatch& local_batch(Ctx& c);
-int strip_solve(Ctx& c, Level& F, int nr, const double* u, const struct Lam& lam, double* glued,
-                double tol, int maxit, std::vector<SolveReport>* reports, bool* empty);
+int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const struct Lam& lam,
+                double* glued, double tol, int maxit, std::vector<SolveReport>* reports,
+                bool* empty);
 void ensure_strip_mask(Ctx& c, Level& F);
 void prolong_chain(Ctx& c, int nr, const double* src, int from, int to, double* dst);
 const double* restrict_chain(Ctx& c, int nr, const double* src, int from, int slot);

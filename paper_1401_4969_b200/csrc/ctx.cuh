@@ -31,6 +31,12 @@ struct alignas(32) Stencil {
   double c, e, n, ne;
 };
 
+// Closed form of the strip (interior dofs outside every closed G_j) at one
+// level: block grid, overlap cells and the fine/coarse scale 2^level.
+struct StripGeom {
+  int side = 1, bw = 1, bh = 1, dc = 0, nx0 = 1, ny0 = 1, scale = 1;
+};
+
 struct Config {
   double x_min = -1.0, x_max = 1.0, y_min = -1.0, y_max = 1.0;
   double H = 0.25;
@@ -72,6 +78,7 @@ struct Level {
   DevBuf<Stencil> stA, stM;
   DevBuf<double> dinv;
   DevBuf<unsigned char> strip_mask;  // built lazily (1 = interior dof of the strip)
+  StripGeom strip_geom;              // same set in closed form (set with the mask)
   // All interior rows of A (and 1/A_ii) bitwise identical: the CG kernels then
   // take the stencil from kernel parameters (constant-coefficient lattice).
   int uniform = 0;
