@@ -155,6 +155,121 @@ __device__ __forceinline__ double product(double sv, const Stencil& sst, int sin
   return a;
 }
 
+// ---- interior fast path (constant-coefficient lattice) ----------------------
+// A warp task whose 32 columns and rows ly0-2 .. ly1+1 all lie inside its
+// system needs no bounds, mask or presence tests: every neighbour exists and
+// the row product is the full 7-term sum (same terms, same order, same
+// rounding as the general path).
+
+// Closed rectangle [xa,xb] x [ya,yb] (fine lattice) entirely inside the strip.
+__device__ __forceinline__ bool rect_in_strip(const StripGeom& g, int xa, int xb, int ya,
+                                              int yb) {
+  const int bxa = min(xa / (g.bw * g.scale), g.side - 1);
+  const int bxb = min(xb / (g.bw * g.scale), g.side - 1);
+  const int bya = min(ya / (g.bh * g.scale), g.side - 1);
+  const int byb = min(yb / (g.bh * g.scale), g.side - 1);
+  for (int bx = bxa; bx <= bxb; ++bx)
+    for (int by = bya; by <= byb; ++by) {
+      const int x0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+      const int x1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+      const int y0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+      const int y1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+      if (xa <= x1 && xb >= x0 && ya <= y1 && yb >= y0) return false;
+    }
+  return true;
+}
+
+__device__ __forceinline__ bool task_interior(const CgSys& S, const SweepArgs& A, const Task& k) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = k.col - lane;  // column of lane 0 (warp-uniform)
+  if (c0 < 0 || c0 + 31 >= S.w || k.ly0 - 2 < 0 || k.ly1 + 1 >= S.h) return false;
+  if (A.mask)
+    return rect_in_strip(A.sg, S.x0 + c0, S.x0 + c0 + 31, S.y0 + k.ly0 - 2, S.y0 + k.ly1 + 1);
+  return true;
+}
+
+__device__ __forceinline__ double product_full(double sv, double cv, double nv,
+                                               const Stencil& u) {
+  const double wv = __shfl_up_sync(kFull, cv, 1);
+  const double ev = __shfl_down_sync(kFull, cv, 1);
+  const double swv = __shfl_up_sync(kFull, sv, 1);
+  const double nev = __shfl_down_sync(kFull, nv, 1);
+  double a = xadd(0.0, xmul(u.ne, swv));
+  a = xadd(a, xmul(u.n, sv));
+  a = xadd(a, xmul(u.e, wv));
+  a = xadd(a, xmul(u.c, cv));
+  a = xadd(a, xmul(u.e, ev));
+  a = xadd(a, xmul(u.n, nv));
+  a = xadd(a, xmul(u.ne, nev));
+  return a;
+}
+
+__device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const SweepArgs& A,
+                                                     const Task& k, double al, double be,
+                                                     bool rst, double* __restrict__ X,
+                                                     const double* __restrict__ Rc,
+                                                     double* __restrict__ Rn,
+                                                     const double* __restrict__ Pc,
+                                                     double* __restrict__ Pn,
+                                                     double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  const bool out = lane >= 2 && lane < 2 + kCgCols;
+  const int w = S.w;
+  double* __restrict__ Xs = X + S.voff + k.col;
+  const double* __restrict__ Rs = Rc + S.voff + k.col;
+  double* __restrict__ Rns = Rn + S.voff + k.col;
+  const double* __restrict__ Ps = Pc + S.voff + k.col;
+  double* __restrict__ Pns = Pn + S.voff + k.col;
+  const Stencil u = A.ust;
+  const double dv = A.udinv;
+  // old p at rows n-1, n, n+1; r and x at row n (+ next rows in flight)
+  int idx = (k.ly0 - 2) * w;
+  double pa = Ps[idx], pb = Ps[idx + w], pc = Ps[idx + 2 * w];
+  double rb = Rs[idx + w], xb = Xs[idx + w];
+  double rc = Rs[idx + 2 * w], xc = Xs[idx + 2 * w];
+  double sp = 0.0, mp = 0.0, mz = 0.0;
+  for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
+    const int in = n * w;  // row n
+    const int i2 = in + 2 * w;
+    const double pd = n + 2 <= k.ly1 + 1 ? Ps[i2] : 0.0;
+    const double rd = n + 2 <= k.ly1 + 1 ? Rs[i2] : 0.0;
+    const double xd = n + 2 <= k.ly1 + 1 ? Xs[i2] : 0.0;
+    double rn = rb, xn = xb;
+    if (!rst) {
+      const double qo = product_full(pa, pb, pc, u);
+      rn = xsub(rb, xmul(al, qo));
+      xn = xadd(xb, xmul(al, pb));
+    }
+    const double tz = xmul(dv, rn);
+    const double tp = rst ? tz : xadd(tz, xmul(be, pb));
+    if (out && n >= k.ly0 && n < k.ly1) {
+      Xs[in] = xn;
+      Rns[in] = rn;
+      Pns[in] = tp;
+      acc[0] += rn * rn;
+      acc[1] += rn * tz;
+    }
+    if (n - 1 >= k.ly0) {
+      const double q = product_full(sp, mp, tp, u);
+      if (out) {
+        acc[2] += mp * q;
+        acc[3] += q * mz;
+        acc[4] += q * xmul(dv, q);
+      }
+    }
+    sp = mp;
+    mp = tp;
+    mz = tz;
+    pa = pb;
+    pb = pc;
+    pc = pd;
+    rb = rc;
+    xb = xc;
+    rc = rd;
+    xc = xd;
+  }
+}
+
 enum Phase { kPhaseInit = 0, kPhaseIter = 1 };
 
 // Scalar recurrences of cg_solve for one system after a launch's reduction.
@@ -306,7 +421,11 @@ __global__ void __launch_bounds__(kBlock)
   const Task k = task_of(S, tl.t);
   const bool out = out_lane(S, k);
   double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  if (k.valid && mode == kModeNormal) {
+  bool fast = false;
+  if constexpr (UNI) fast = k.valid && mode == kModeNormal && task_interior(S, A, k);
+  if (fast) {
+    fused_sweep_interior(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
+  } else if (k.valid && mode == kModeNormal) {
     ORow a, b, c, d;  // old iterate at rows n-1, n, n+1 (and n+2 in flight)
     NRow s, m;        // new p at rows n-2, n-1
     load_old<UNI>(S, A, k.col, k.ly0 - 2, Rc, Pc, X, a);
