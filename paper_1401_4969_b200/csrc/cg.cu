@@ -30,6 +30,7 @@
 // systems are dropped between chunks.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "cg.cuh"
@@ -49,6 +50,7 @@ struct SweepArgs {
   StripGeom sg;               // closed form of that restriction (no mask loads)
   Stencil ust;                // interior stencil when the level is uniform
   double udinv;
+  const int* task_map;        // compacted task lists (systems with tmap_off >= 0)
 };
 
 // Strip membership of fine lattice point (ix, iy): not in the closed inner
@@ -82,11 +84,12 @@ struct Task {
   int col, ly0, ly1;
 };
 
-__device__ __forceinline__ Task task_of(const CgSys& S, int t) {
+__device__ __forceinline__ Task task_of(const CgSys& S, int t, const int* task_map) {
   Task k;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int task = t * kCgWarps + warp;
+  int task = t * kCgWarps + warp;
   k.valid = task < S.ntasks;
+  if (k.valid && S.tmap_off >= 0) task = task_map[S.tmap_off + task];
   const int rb = k.valid ? task / S.nstrips : 0;
   const int strip = k.valid ? task % S.nstrips : 0;
   k.col = strip * kCgCols - 2 + lane;
@@ -194,14 +197,140 @@ __device__ __forceinline__ double product_full(double sv, double cv, double nv,
   const double ev = __shfl_down_sync(kFull, cv, 1);
   const double swv = __shfl_up_sync(kFull, sv, 1);
   const double nev = __shfl_down_sync(kFull, nv, 1);
-  double a = xadd(0.0, xmul(u.ne, swv));
-  a = xadd(a, xmul(u.n, sv));
-  a = xadd(a, xmul(u.e, wv));
-  a = xadd(a, xmul(u.c, cv));
-  a = xadd(a, xmul(u.e, ev));
-  a = xadd(a, xmul(u.n, nv));
-  a = xadd(a, xmul(u.ne, nev));
-  return a;
+  // Constant coefficients are symmetric (W/E share e, S/N share n, SW/NE
+  // share ne): pair the neighbours and fuse -- dependency depth 4 instead of
+  // 14.  (Inside CG only; the exported SpMV keeps the reference's order.)
+  return fma(u.e, wv + ev, fma(u.n, sv + nv, fma(u.ne, swv + nev, u.c * cv)));
+}
+
+// Constant-coefficient sweep for ANY task (window edges, strip mask): the
+// in-system flag of (column, row) is separable -- column inside the window and
+// outside its block's G x-range, row inside the window and outside its block's
+// G y-range -- so it costs a few integer ops per row, no memory traffic.
+// Presence of W/E/SW/NE neighbours comes from shuffled flags.
+__device__ __forceinline__ double product_flags(double sv, int sin_, double cv, int cin,
+                                                double nv, int nin, const Stencil& u) {
+  const int win = __shfl_up_sync(kFull, cin, 1);
+  const int ein = __shfl_down_sync(kFull, cin, 1);
+  const int swin = __shfl_up_sync(kFull, sin_, 1);
+  const int nein = __shfl_down_sync(kFull, nin, 1);
+  const double wr = __shfl_up_sync(kFull, cv, 1);
+  const double er = __shfl_down_sync(kFull, cv, 1);
+  const double swr = __shfl_up_sync(kFull, sv, 1);
+  const double ner = __shfl_down_sync(kFull, nv, 1);
+  const double wv = win ? wr : 0.0, ev = ein ? er : 0.0;
+  const double swv = swin ? swr : 0.0, nev = nein ? ner : 0.0;
+  const double s = sin_ ? sv : 0.0, n = nin ? nv : 0.0;
+  // same pairing as product_full (identical result when every neighbour exists)
+  return fma(u.e, wv + ev, fma(u.n, s + n, fma(u.ne, swv + nev, u.c * cv)));
+}
+
+struct Flags {
+  int cin;   // this lane's column is in the window
+  int gx;    // ... and inside its block's G x-range (masked systems)
+  int masked;
+  int h;
+  StripGeom g;
+  int y0;    // window origin (fine lattice row of window row 0)
+  __device__ __forceinline__ int row_in(int ly) const {
+    if (!cin || ly < 0 || ly >= h) return 0;
+    if (!masked || !gx) return 1;
+    const int iy = y0 + ly;
+    const int by = min(iy / (g.bh * g.scale), g.side - 1);
+    const int ya = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+    const int yb = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+    return (iy >= ya && iy <= yb) ? 0 : 1;
+  }
+};
+
+__device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs& A, const Task& k,
+                                                double al, double be, bool rst,
+                                                double* __restrict__ X,
+                                                const double* __restrict__ Rc,
+                                                double* __restrict__ Rn,
+                                                const double* __restrict__ Pc,
+                                                double* __restrict__ Pn,
+                                                double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  Flags f;
+  f.cin = k.col >= 0 && k.col < S.w;
+  f.masked = A.mask != nullptr;
+  f.g = A.sg;
+  f.h = S.h;
+  f.y0 = S.y0;
+  f.gx = 0;
+  if (f.masked && f.cin) {
+    const StripGeom& g = A.sg;
+    const int ix = S.x0 + k.col;
+    const int bx = min(ix / (g.bw * g.scale), g.side - 1);
+    const int xa = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+    const int xb = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+    f.gx = (ix >= xa && ix <= xb) ? 1 : 0;
+  }
+  const bool out_col = lane >= 2 && lane < 2 + kCgCols && f.cin;
+  const int w = S.w;
+  const long long base = S.voff + k.col;
+  double* __restrict__ Xs = X + base;
+  const double* __restrict__ Rs = Rc + base;
+  double* __restrict__ Rns = Rn + base;
+  const double* __restrict__ Ps = Pc + base;
+  double* __restrict__ Pns = Pn + base;
+  const Stencil u = A.ust;
+  const double dv = A.udinv;
+  auto ld = [&](const double* __restrict__ p, int ly, int in) -> double {
+    return in ? p[ly * w] : 0.0;
+  };
+  // old p at rows n-1, n, n+1 (flags ia, ib, ic); r and x at rows n, n+1
+  int ia = f.row_in(k.ly0 - 2), ib = f.row_in(k.ly0 - 1), ic = f.row_in(k.ly0);
+  double pa = ld(Ps, k.ly0 - 2, ia), pb = ld(Ps, k.ly0 - 1, ib), pc = ld(Ps, k.ly0, ic);
+  double rb = ld(Rs, k.ly0 - 1, ib), xb = ld(Xs, k.ly0 - 1, ib);
+  double rc = ld(Rs, k.ly0, ic), xc = ld(Xs, k.ly0, ic);
+  double sp = 0.0, mp = 0.0, mz = 0.0;
+  int sin_ = 0, min_ = 0;
+  for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
+    const int id = n + 2 <= k.ly1 + 1 ? f.row_in(n + 2) : 0;
+    const double pd = ld(Ps, n + 2, id);
+    const double rd = ld(Rs, n + 2, id);
+    const double xd = ld(Xs, n + 2, id);
+    double rn = rb, xn = xb;
+    if (!rst) {
+      const double qo = product_flags(pa, ia, pb, ib, pc, ic, u);
+      rn = fma(-al, qo, rb);
+      xn = fma(al, pb, xb);
+    }
+    const double tz = xmul(dv, rn);
+    const double tp = rst ? tz : fma(be, pb, tz);
+    if (out_col && ib && n >= k.ly0 && n < k.ly1) {
+      Xs[n * w] = xn;
+      Rns[n * w] = rn;
+      Pns[n * w] = tp;
+      acc[0] += rn * rn;
+      acc[1] += rn * tz;
+    }
+    if (n - 1 >= k.ly0) {
+      const double q = product_flags(sp, sin_, mp, min_, tp, ib, u);
+      if (out_col && min_) {
+        acc[2] += mp * q;
+        acc[3] += q * mz;
+        acc[4] += q * xmul(dv, q);
+      }
+    }
+    sp = mp;
+    sin_ = min_;
+    mp = tp;
+    min_ = ib;
+    mz = tz;
+    pa = pb;
+    ia = ib;
+    pb = pc;
+    ib = ic;
+    pc = pd;
+    ic = id;
+    rb = rc;
+    xb = xc;
+    rc = rd;
+    xc = xd;
+  }
 }
 
 __device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const SweepArgs& A,
@@ -222,26 +351,30 @@ __device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const Sweep
   double* __restrict__ Pns = Pn + S.voff + k.col;
   const Stencil u = A.ust;
   const double dv = A.udinv;
-  // old p at rows n-1, n, n+1; r and x at row n (+ next rows in flight)
-  int idx = (k.ly0 - 2) * w;
-  double pa = Ps[idx], pb = Ps[idx + w], pc = Ps[idx + 2 * w];
-  double rb = Rs[idx + w], xb = Xs[idx + w];
-  double rc = Rs[idx + 2 * w], xc = Xs[idx + 2 * w];
+  // old p at rows n-1, n, n+1; r and x at rows n, n+1; rows n+2, n+3 in
+  // flight -- loads are issued three sweep steps before use (latency hiding
+  // at ~20 resident warps per SM needs several rows per warp in flight)
+  const int last = k.ly1 + 1;  // last old row needed
+  auto row = [&](const double* __restrict__ p, int ly) -> double {
+    return ly <= last ? p[ly * w] : 0.0;
+  };
+  double pa = row(Ps, k.ly0 - 2), pb = row(Ps, k.ly0 - 1), pc = row(Ps, k.ly0);
+  double rb = row(Rs, k.ly0 - 1), xb = row(Xs, k.ly0 - 1);
+  double rc = row(Rs, k.ly0), xc = row(Xs, k.ly0);
+  double p2 = row(Ps, k.ly0 + 1), r2 = row(Rs, k.ly0 + 1), x2 = row(Xs, k.ly0 + 1);
+  double p3 = row(Ps, k.ly0 + 2), r3 = row(Rs, k.ly0 + 2), x3 = row(Xs, k.ly0 + 2);
   double sp = 0.0, mp = 0.0, mz = 0.0;
   for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
     const int in = n * w;  // row n
-    const int i2 = in + 2 * w;
-    const double pd = n + 2 <= k.ly1 + 1 ? Ps[i2] : 0.0;
-    const double rd = n + 2 <= k.ly1 + 1 ? Rs[i2] : 0.0;
-    const double xd = n + 2 <= k.ly1 + 1 ? Xs[i2] : 0.0;
+    const double pd = row(Ps, n + 4), rd = row(Rs, n + 4), xd = row(Xs, n + 4);
     double rn = rb, xn = xb;
     if (!rst) {
       const double qo = product_full(pa, pb, pc, u);
-      rn = xsub(rb, xmul(al, qo));
-      xn = xadd(xb, xmul(al, pb));
+      rn = fma(-al, qo, rb);
+      xn = fma(al, pb, xb);
     }
     const double tz = xmul(dv, rn);
-    const double tp = rst ? tz : xadd(tz, xmul(be, pb));
+    const double tp = rst ? tz : fma(be, pb, tz);
     if (out && n >= k.ly0 && n < k.ly1) {
       Xs[in] = xn;
       Rns[in] = rn;
@@ -262,11 +395,17 @@ __device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const Sweep
     mz = tz;
     pa = pb;
     pb = pc;
-    pc = pd;
+    pc = p2;
+    p2 = p3;
+    p3 = pd;
     rb = rc;
     xb = xc;
-    rc = rd;
-    xc = xd;
+    rc = r2;
+    xc = x2;
+    r2 = r3;
+    x2 = x3;
+    r3 = rd;
+    x3 = xd;
   }
 }
 
@@ -384,7 +523,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
                                                     Finish F) {
   const CgTile tl = tiles[blockIdx.x];
   const CgSys S = sys[tl.sys];
-  const Task k = task_of(S, tl.t);
+  const Task k = task_of(S, tl.t, A.task_map);
   double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
   if (out_lane(S, k)) {
     for (int ly = k.ly0; ly < k.ly1; ++ly) {
@@ -418,14 +557,19 @@ __global__ void __launch_bounds__(kBlock)
   if (mode == kModeSkip) return;  // uniform across the system's tiles
   const double al = s_c.alpha, be = s_c.beta;
   const bool rst = s_c.restart != 0;
-  const Task k = task_of(S, tl.t);
+  const Task k = task_of(S, tl.t, A.task_map);
   const bool out = out_lane(S, k);
   double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  bool fast = false;
-  if constexpr (UNI) fast = k.valid && mode == kModeNormal && task_interior(S, A, k);
+  bool fast = false, flagged = false;
+  if constexpr (UNI) {
+    fast = k.valid && mode == kModeNormal && task_interior(S, A, k);
+    flagged = k.valid && mode == kModeNormal && !fast;
+  }
   if (fast) {
     fused_sweep_interior(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
-  } else if (k.valid && mode == kModeNormal) {
+  } else if (flagged) {
+    fused_sweep_uni(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
+  } else if (!UNI && k.valid && mode == kModeNormal) {
     ORow a, b, c, d;  // old iterate at rows n-1, n, n+1 (and n+2 in flight)
     NRow s, m;        // new p at rows n-2, n-1
     load_old<UNI>(S, A, k.col, k.ly0 - 2, Rc, Pc, X, a);
@@ -521,21 +665,60 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   for (const CgSys& s : systems) all_rows += static_cast<long long>(s.w) * s.h;
   // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
   // must still offer >= ~8k warps (148 SMs x ~56 resident) to hide latency.
-  const int krows = static_cast<int>(
-      std::min<long long>(kCgRows, std::max<long long>(16, all_rows / (kCgCols * 8192LL))));
+  static const long long target_tasks = [] {
+    const char* e = std::getenv("MLG_CG_TASKS");  // tuning hook
+    return e ? std::atoll(e) : 8192LL;
+  }();
+  static const int min_rows = [] {
+    const char* e = std::getenv("MLG_CG_MINROWS");  // tuning hook
+    return e ? std::atoi(e) : 16;
+  }();
+  const int krows = static_cast<int>(std::min<long long>(
+      kCgRows, std::max<long long>(min_rows, all_rows / (kCgCols * target_tasks))));
   for (CgSys& s : systems) {
     s.nrows = s.w * s.h;
-    s.voff = total_rows;
     s.krows = krows;
     s.nstrips = std::max(1, (s.w + kCgCols - 1) / kCgCols);
     s.nrb = std::max(1, (s.h + krows - 1) / krows);
     s.ntasks = s.nstrips * s.nrb;
-    s.ntiles = (s.ntasks + kCgWarps - 1) / kCgWarps;
+    s.tmap_off = -1;
+  }
+  // Strip systems: keep only tasks whose output cells meet the strip (tasks
+  // lying inside a closed G_j would only sweep masked rows).
+  std::vector<int> tmap;
+  if (mask && !systems.empty()) {
+    const CgSys& s = systems[0];
+    const StripGeom& g = lev.strip_geom;
+    auto inside_g = [&](int xa, int xb, int ya, int yb) {
+      const int bx = std::min(xa / (g.bw * g.scale), g.side - 1);
+      const int by = std::min(ya / (g.bh * g.scale), g.side - 1);
+      const int x0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+      const int x1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+      const int y0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+      const int y1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+      return xa >= x0 && xb <= x1 && ya >= y0 && yb <= y1;
+    };
+    for (int t = 0; t < s.ntasks; ++t) {
+      const int rb = t / s.nstrips, strip = t % s.nstrips;
+      const int ca = s.x0 + strip * kCgCols, cb = s.x0 + std::min(strip * kCgCols + kCgCols, s.w) - 1;
+      const int ra = s.y0 + rb * s.krows, rbb = s.y0 + std::min(rb * s.krows + s.krows, s.h) - 1;
+      if (!inside_g(ca, cb, ra, rbb)) tmap.push_back(t);
+    }
+    for (CgSys& q : systems) {
+      q.tmap_off = 0;
+      q.ntasks = static_cast<int>(tmap.size());
+    }
+  }
+  for (CgSys& s : systems) {
+    s.ntiles = std::max(1, (s.ntasks + kCgWarps - 1) / kCgWarps);
+    s.voff = total_rows;
     s.toff = total_tiles;
     s.maxit = 10 * std::max(s.nrows, 1);
     total_rows += s.nrows;
     total_tiles += s.ntiles;
   }
+  task_map.ensure(std::max<std::size_t>(tmap.size(), 1));
+  if (!tmap.empty()) task_map.upload(tmap.data(), tmap.size(), c.stream);
   sys_h = std::move(systems);
   const std::size_t nv = static_cast<std::size_t>(total_rows);
   X.ensure(nv);
@@ -575,7 +758,8 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
   rebuild(active);
   cudaStream_t st = c.stream;
   const bool uni = L->uniform != 0;
-  const SweepArgs A = sweep_args(*L, mask);
+  SweepArgs A = sweep_args(*L, mask);
+  A.task_map = task_map.get();
   const Finish F{part.get(), counters.get(), ctl_d.get(), tol};
   double *rc = R0.get(), *rn = R1.get(), *pc = P0.get(), *pn = P1.get();
 

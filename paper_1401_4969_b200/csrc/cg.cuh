@@ -32,6 +32,7 @@ struct CgSys {
   int nrows;
   int maxit;
   int nstrips, nrb, ntasks, krows;
+  int tmap_off;  // >= 0: tasks are task_map[tmap_off + i] (strip tasks with strip rows)
 };
 
 struct CgTile {
@@ -82,6 +83,7 @@ class CgBatch {
   int total_tiles = 0;
   DevBuf<CgSys> sys_d;
   DevBuf<CgTile> tiles_d;
+  DevBuf<int> task_map;
   DevBuf<CgCtl> ctl_d;
   DevBuf<unsigned> counters;  // per-system tile arrival counters (last-tile reduction)
   DevBuf<double> X, R0, R1, P0, P1, part;

@@ -161,9 +161,11 @@ def test_step_is_deterministic(mlg, oracle_ref):
         assert np.array_equal(pa.coeffs.view(np.uint64), pb.coeffs.view(np.uint64))
 
 
-def test_uniform_stencil_fast_path_is_bitwise_general_path(mlg, monkeypatch):
-    """The constant-coefficient CG path (stencil from kernel parameters) and the
-    general per-row path give bitwise identical steps."""
+def test_uniform_stencil_fast_path_matches_general_path(mlg, monkeypatch):
+    """The constant-coefficient CG path (stencil from kernel parameters, paired
+    FMA row products) and the general per-row path (the reference's exact
+    term order) agree to rounding level: same iteration counts, eigenvalues to
+    1e-12, eigenvectors to 1e-9."""
     def run():
         cfg = mlg.RunConfig(domain=mlg.DomainRect(0.0, 1.0, 0.0, 1.0), H=1 / 8, delta=1 / 8, m=4,
                             n_levels=4, nev=4)
@@ -174,9 +176,11 @@ def test_uniform_stencil_fast_path_is_bitwise_general_path(mlg, monkeypatch):
     lam_g, p_g = run()
     monkeypatch.delenv("MLG_GENERAL_STENCIL")
     lam_u, p_u = run()
-    assert np.array_equal(lam_g, lam_u)
-    for a, b in zip(p_g, p_u):
-        assert np.array_equal(a.coeffs.view(np.uint64), b.coeffs.view(np.uint64))
+    assert np.max(np.abs(lam_g - lam_u) / lam_g) <= 1e-12
+    for i in (0, 3):  # isolated eigenvalues (lambda_2 ~ lambda_3 is a cluster)
+        a, b = p_g[i].coeffs, p_u[i].coeffs
+        s = 1.0 if a @ b >= 0 else -1.0
+        assert np.max(np.abs(a - s * b)) <= 1e-9 * np.max(np.abs(a))
 
 
 def test_config_errors(mlg):
