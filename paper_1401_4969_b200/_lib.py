@@ -6,10 +6,11 @@ import-time call `lib()` raises, and every API entry point fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libmlg_b200.so"
+LIB_PATH = Path(os.environ.get("MLG_LIB", Path(__file__).resolve().parent / "libmlg_b200.so"))
 
 c_int_p = C.POINTER(C.c_int)
 c_double_p = C.POINTER(C.c_double)

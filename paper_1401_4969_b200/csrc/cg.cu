@@ -333,6 +333,52 @@ __device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs&
   }
 }
 
+// True residual r = b - A x of a constant-coefficient system (x current).
+__device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs& A,
+                                                const Task& k, const double* bsrc, int bstride,
+                                                const double* __restrict__ X,
+                                                double* __restrict__ Rn,
+                                                double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  Flags f;
+  f.cin = k.col >= 0 && k.col < S.w;
+  f.masked = A.mask != nullptr;
+  f.g = A.sg;
+  f.h = S.h;
+  f.y0 = S.y0;
+  f.gx = 0;
+  if (f.masked && f.cin) {
+    const StripGeom& g = A.sg;
+    const int ix = S.x0 + k.col;
+    const int bx = min(ix / (g.bw * g.scale), g.side - 1);
+    const int xa = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+    const int xb = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+    f.gx = (ix >= xa && ix <= xb) ? 1 : 0;
+  }
+  const bool out_col = lane >= 2 && lane < 2 + kCgCols && f.cin;
+  const long long base = S.voff + k.col;
+  const double* __restrict__ Xs = X + base;
+  double* __restrict__ Rns = Rn + base;
+  auto ld = [&](int ly, int in) -> double { return in ? Xs[static_cast<long long>(ly) * S.w] : 0.0; };
+  int ia = f.row_in(k.ly0 - 1), ib = f.row_in(k.ly0);
+  double xa = ld(k.ly0 - 1, ia), xb = ld(k.ly0, ib);
+  for (int ly = k.ly0; ly < k.ly1; ++ly) {
+    const int ic = f.row_in(ly + 1);
+    const double xc = ld(ly + 1, ic);
+    const double ax = product_flags(xa, ia, xb, ib, xc, ic, A.ust);
+    if (out_col && ib) {
+      const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
+      const double rt = bsrc[g * bstride + S.rhs] - ax;
+      Rns[static_cast<long long>(ly) * S.w] = rt;
+      acc[0] += rt * rt;
+    }
+    xa = xb;
+    ia = ib;
+    xb = xc;
+    ib = ic;
+  }
+}
+
 __device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const SweepArgs& A,
                                                      const Task& k, double al, double be,
                                                      bool rst, double* __restrict__ X,
@@ -364,6 +410,7 @@ __device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const Sweep
   double p2 = row(Ps, k.ly0 + 1), r2 = row(Rs, k.ly0 + 1), x2 = row(Xs, k.ly0 + 1);
   double p3 = row(Ps, k.ly0 + 2), r3 = row(Rs, k.ly0 + 2), x3 = row(Xs, k.ly0 + 2);
   double sp = 0.0, mp = 0.0, mz = 0.0;
+#pragma unroll 2
   for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
     const int in = n * w;  // row n
     const double pd = row(Ps, n + 4), rd = row(Rs, n + 4), xd = row(Xs, n + 4);
@@ -542,8 +589,11 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
   finish_tile<kPhaseInit>(S, tl.sys, tl.t, acc, F);
 }
 
+#ifndef MLG_CG_MINBLOCKS
+#define MLG_CG_MINBLOCKS 5
+#endif
 template <bool UNI>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS)
     k_cg_iter(const CgSys* sys, const CgTile* tiles, SweepArgs A, const double* bsrc,
               int bstride, double* __restrict__ X, const double* __restrict__ Rc,
               double* __restrict__ Rn, const double* __restrict__ Pc, double* __restrict__ Pn,
@@ -618,6 +668,8 @@ __global__ void __launch_bounds__(kBlock)
       b = c;
       c = d;
     }
+  } else if (UNI && k.valid) {  // kModeCheck, constant coefficients: r = b - A x
+    check_sweep_uni(S, A, k, bsrc, bstride, X, Rn, acc);
   } else if (k.valid) {  // kModeCheck: r = b - A x (x is current: updated in place)
     ORow a, b, c;
     load_old<UNI>(S, A, k.col, k.ly0 - 1, Rc, Pc, X, a);
@@ -673,8 +725,40 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
     const char* e = std::getenv("MLG_CG_MINROWS");  // tuning hook
     return e ? std::atoi(e) : 16;
   }();
-  const int krows = static_cast<int>(std::min<long long>(
+  int krows = static_cast<int>(std::min<long long>(
       kCgRows, std::max<long long>(min_rows, all_rows / (kCgCols * target_tasks))));
+  // Wave quantisation: every tile costs ~(krows + 3) row steps and the grid
+  // runs in waves of `resident` tiles, so pick the row count that minimises
+  // waves x (krows + 3) among the candidates at or below the first choice.
+  {
+    static const int resident = [] {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg_iter<true>, kBlock, 0);
+      return std::max(1, sms * std::max(per, 1));
+    }();
+    auto tiles_for = [&](int kr) {
+      long long t = 0;
+      for (const CgSys& s : systems) {
+        const long long ns = std::max(1, (s.w + kCgCols - 1) / kCgCols);
+        const long long nb = std::max(1, (s.h + kr - 1) / kr);
+        t += (ns * nb + kCgWarps - 1) / kCgWarps;
+      }
+      return t;
+    };
+    double best = 1e300;
+    int best_k = krows;
+    for (int kr = std::max(8, krows / 2); kr <= krows; ++kr) {
+      const long long waves = (tiles_for(kr) + resident - 1) / resident;
+      const double cost = static_cast<double>(waves) * (kr + 3);
+      if (cost < best - 1e-9) {
+        best = cost;
+        best_k = kr;
+      }
+    }
+    krows = best_k;
+  }
   for (CgSys& s : systems) {
     s.nrows = s.w * s.h;
     s.krows = krows;
