@@ -191,6 +191,16 @@ __device__ __forceinline__ bool task_interior(const CgSys& S, const SweepArgs& A
   return true;
 }
 
+// Task whose stencil rectangle (clamped to the window) avoids G entirely:
+// every point it touches is either in the system or outside the window.
+__device__ __forceinline__ bool task_unmasked(const CgSys& S, const SweepArgs& A, const Task& k) {
+  if (!A.mask) return true;
+  const int lane = threadIdx.x & 31;
+  const int c0 = max(k.col - lane, 0), c1 = min(k.col - lane + 31, S.w - 1);
+  const int r0 = max(k.ly0 - 2, 0), r1 = min(k.ly1 + 1, S.h - 1);
+  return rect_in_strip(A.sg, S.x0 + c0, S.x0 + c1, S.y0 + r0, S.y0 + r1);
+}
+
 __device__ __forceinline__ double product_full(double sv, double cv, double nv,
                                                const Stencil& u) {
   const double wv = __shfl_up_sync(kFull, cv, 1);
@@ -379,7 +389,9 @@ __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs&
   }
 }
 
-__device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const SweepArgs& A,
+// Register-prefetch sweep (rows n+2, n+3 in flight in registers): best when
+// the batch's vectors are L2-resident (short latency, few rows needed in flight).
+__device__ __forceinline__ void sweep_interior_regs(const CgSys& S, const SweepArgs& A,
                                                      const Task& k, double al, double be,
                                                      bool rst, double* __restrict__ X,
                                                      const double* __restrict__ Rc,
@@ -455,6 +467,132 @@ __device__ __forceinline__ void fused_sweep_interior(const CgSys& S, const Sweep
     x3 = xd;
   }
 }
+
+// ---- asynchronous row pipeline for interior tasks ---------------------------
+// Every lane streams its column through a private ring of kD shared-memory
+// slots with cp.async (8 B per lane and array, LDGSTS): rows n+2 .. n+kD-1 of
+// p, r and x are in flight while row n is computed, so each warp keeps ~3(kD-2)
+// independent requests outstanding without holding them in registers.  A lane
+// only ever reads back what it copied itself, so the per-thread
+// cp.async.wait_group is the only synchronisation needed.  A slot is refilled
+// at the end of the iteration that consumed it (its values are already in
+// registers), so a copy can never overwrite unread data.
+#ifndef MLG_CG_D
+#define MLG_CG_D 8
+#endif
+#ifndef MLG_CG_ASYNC_MINBLOCKS
+#define MLG_CG_ASYNC_MINBLOCKS 6
+#endif
+constexpr int kD = MLG_CG_D;
+static_assert((kD & (kD - 1)) == 0 && kD >= 4, "ring depth must be a power of two >= 4");
+
+struct RowRing {
+  double v[kD][3][32];  // [slot][p, r, x][lane]
+};
+
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// EDGE: the task touches the window boundary.  Lanes whose column lies outside
+// the window and rows outside it read zeros (the slot is zero-filled instead of
+// copied) and their new p is forced to zero, which reproduces the flagged
+// product exactly (an absent neighbour contributes a literal 0 to the same
+// paired-FMA chain).
+template <bool RST, bool EDGE>
+__device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, const Task& k,
+                                            double al, double be, double* __restrict__ X,
+                                            const double* __restrict__ Rc,
+                                            double* __restrict__ Rn,
+                                            const double* __restrict__ Pc,
+                                            double* __restrict__ Pn, double (&acc)[kCgDots],
+                                            RowRing& ring) {
+  const int lane = threadIdx.x & 31;
+  const bool cval = !EDGE || (k.col >= 0 && k.col < S.w);
+  const bool out = lane >= 2 && lane < 2 + kCgCols && cval;
+  const int w = S.w;
+  const int h = S.h;
+  const long long base = S.voff + k.col;
+  double* __restrict__ Xs = X + base;
+  const double* __restrict__ Rs = Rc + base;
+  double* __restrict__ Rns = Rn + base;
+  const double* __restrict__ Ps = Pc + base;
+  double* __restrict__ Pns = Pn + base;
+  const Stencil u = A.ust;
+  const double dv = A.udinv;
+  const int last = k.ly1 + 1;  // last old row needed
+  auto issue = [&](int row) {  // one commit group per row, empty past the end
+    if (row <= last) {
+      const int s = row & (kD - 1);
+      if (!EDGE || (cval && row >= 0 && row < h)) {
+        const long long o = static_cast<long long>(row) * w;
+        cp_async8(&ring.v[s][0][lane], Ps + o);
+        cp_async8(&ring.v[s][1][lane], Rs + o);
+        cp_async8(&ring.v[s][2][lane], Xs + o);
+      } else {
+        ring.v[s][0][lane] = 0.0;
+        ring.v[s][1][lane] = 0.0;
+        ring.v[s][2][lane] = 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < kD; ++i) issue(k.ly0 - 2 + i);
+  cp_async_wait<kD - 2>();  // rows ly0-2, ly0-1 landed
+  double pa = ring.v[(k.ly0 - 2) & (kD - 1)][0][lane];
+  double pb = ring.v[(k.ly0 - 1) & (kD - 1)][0][lane];
+  issue(k.ly0 - 2 + kD);  // slot of row ly0-2 consumed
+  double sp = 0.0, mp = 0.0, mz = 0.0;
+  for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
+    // issued up to row n+kD-1; row n+1 must have landed
+    cp_async_wait<kD - 2>();
+    const int sc = n & (kD - 1);
+    const double pc = ring.v[(n + 1) & (kD - 1)][0][lane];
+    const double rb = ring.v[sc][1][lane];
+    const double xb = ring.v[sc][2][lane];
+    double rn = rb, xn = xb;
+    if (!RST) {
+      const double qo = product_full(pa, pb, pc, u);
+      rn = fma(-al, qo, rb);
+      xn = fma(al, pb, xb);
+    }
+    const double tz = xmul(dv, rn);
+    double tp = RST ? tz : fma(be, pb, tz);
+    if (EDGE && !(cval && n >= 0 && n < h)) tp = 0.0;
+    if (out && n >= k.ly0 && n < k.ly1) {
+      const long long o = static_cast<long long>(n) * w;
+      Xs[o] = xn;
+      Rns[o] = rn;
+      Pns[o] = tp;
+      acc[0] += rn * rn;
+      acc[1] += rn * tz;
+    }
+    // stage 2 at row n-1 (computed unconditionally: no branch around shuffles)
+    const double q = product_full(sp, mp, tp, u);
+    if (out && n - 1 >= k.ly0) {
+      acc[2] += mp * q;
+      acc[3] += q * mz;
+      acc[4] += q * xmul(dv, q);
+    }
+    sp = mp;
+    mp = tp;
+    mz = tz;
+    pa = pb;
+    pb = pc;
+    issue(n + kD);  // refill slot n (its p, r, x are consumed)
+  }
+  cp_async_wait<0>();
+}
+
 
 enum Phase { kPhaseInit = 0, kPhaseIter = 1 };
 
@@ -592,8 +730,8 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
 #ifndef MLG_CG_MINBLOCKS
 #define MLG_CG_MINBLOCKS 5
 #endif
-template <bool UNI>
-__global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS)
+template <bool UNI, bool ASYNC>
+__global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBLOCKS : MLG_CG_MINBLOCKS) * 4 / kCgWarps)
     k_cg_iter(const CgSys* sys, const CgTile* tiles, SweepArgs A, const double* bsrc,
               int bstride, double* __restrict__ X, const double* __restrict__ Rc,
               double* __restrict__ Rn, const double* __restrict__ Pc, double* __restrict__ Pn,
@@ -601,6 +739,7 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS)
   const CgTile tl = tiles[blockIdx.x];
   const CgSys S = sys[tl.sys];
   __shared__ CgCtl s_c;
+  extern __shared__ RowRing s_ring[];  // kCgWarps rings (ASYNC only)
   if (threadIdx.x == 0) s_c = F.ctl[tl.sys];
   __syncthreads();
   const int mode = s_c.mode;
@@ -610,13 +749,30 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS)
   const Task k = task_of(S, tl.t, A.task_map);
   const bool out = out_lane(S, k);
   double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  bool fast = false, flagged = false;
+  bool fast = false, edge = false, flagged = false;
   if constexpr (UNI) {
     fast = k.valid && mode == kModeNormal && task_interior(S, A, k);
-    flagged = k.valid && mode == kModeNormal && !fast;
+    if (ASYNC && k.valid && mode == kModeNormal && !fast && task_unmasked(S, A, k)) {
+      edge = true;
+    }
+    flagged = k.valid && mode == kModeNormal && !fast && !edge;
   }
   if (fast) {
-    fused_sweep_interior(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
+    if constexpr (ASYNC) {
+      RowRing& ring = s_ring[threadIdx.x >> 5];
+      if (rst)
+        sweep_async<true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+      else
+        sweep_async<false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+    } else {
+      sweep_interior_regs(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
+    }
+  } else if (ASYNC && edge) {
+    RowRing& ring = s_ring[threadIdx.x >> 5];
+    if (rst)
+      sweep_async<true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+    else
+      sweep_async<false, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
   } else if (flagged) {
     fused_sweep_uni(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
   } else if (!UNI && k.valid && mode == kModeNormal) {
@@ -691,6 +847,32 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS)
   finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
 }
 
+constexpr int kRingBytes = kCgWarps * static_cast<int>(sizeof(RowRing));
+
+// Resident CTAs per GPU of the CG iteration kernel (register or async variant).
+int resident_tiles(bool async) {
+  static const int res[2] = {[] {
+                               int dev = 0, sms = 0, per = 0;
+                               cudaGetDevice(&dev);
+                               cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                               cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                   &per, k_cg_iter<true, false>, kBlock, 0);
+                               return std::max(1, sms * std::max(per, 1));
+                             }(),
+                             [] {
+                               int dev = 0, sms = 0, per = 0;
+                               cudaGetDevice(&dev);
+                               cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                               cudaFuncSetAttribute(k_cg_iter<true, true>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    kRingBytes);
+                               cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                   &per, k_cg_iter<true, true>, kBlock, kRingBytes);
+                               return std::max(1, sms * std::max(per, 1));
+                             }()};
+  return res[async ? 1 : 0];
+}
+
 SweepArgs sweep_args(const Level& L, const unsigned char* mask) {
   SweepArgs A{};
   A.st = L.stA.get();
@@ -715,6 +897,15 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   total_tiles = 0;
   long long all_rows = 0;
   for (const CgSys& s : systems) all_rows += static_cast<long long>(s.w) * s.h;
+  // Vectors that outgrow L2 stream from HBM: use the asynchronous row pipeline
+  // (deep prefetch in shared memory); L2-resident batches keep the register
+  // pipeline (lower latency, fewer instructions).
+  static const int async_env = [] {
+    const char* e = std::getenv("MLG_CG_ASYNC");  // A/B hook: 0 / 1
+    return e ? std::atoi(e) : -1;
+  }();
+  use_async = lev.uniform != 0 &&
+              (async_env >= 0 ? async_env != 0 : all_rows * 48 > (128LL << 20));
   // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
   // must still offer >= ~8k warps (148 SMs x ~56 resident) to hide latency.
   static const long long target_tasks = [] {
@@ -731,13 +922,7 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   // runs in waves of `resident` tiles, so pick the row count that minimises
   // waves x (krows + 3) among the candidates at or below the first choice.
   {
-    static const int resident = [] {
-      int dev = 0, sms = 0, per = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg_iter<true>, kBlock, 0);
-      return std::max(1, sms * std::max(per, 1));
-    }();
+    const int resident = resident_tiles(use_async);
     auto tiles_for = [&](int kr) {
       long long t = 0;
       for (const CgSys& s : systems) {
@@ -872,12 +1057,15 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
         ev1 = c.event(2 * evs.size() + 1);
         MLG_CUDA(cudaEventRecord(ev0, st));
       }
-      if (uni)
-        k_cg_iter<true><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc, bstride,
-                                               X.get(), rc, rn, pc, pn, F);
+      if (uni && use_async)
+        k_cg_iter<true, true><<<nt, kBlock, kRingBytes, st>>>(
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, F);
+      else if (uni)
+        k_cg_iter<true, false><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc,
+                                                      bstride, X.get(), rc, rn, pc, pn, F);
       else
-        k_cg_iter<false><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc, bstride,
-                                                X.get(), rc, rn, pc, pn, F);
+        k_cg_iter<false, false><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc,
+                                                       bstride, X.get(), rc, rn, pc, pn, F);
       MLG_LAUNCH_CHECK();
       if (prof) {
         MLG_CUDA(cudaEventRecord(ev1, st));

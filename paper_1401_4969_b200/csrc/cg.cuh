@@ -48,7 +48,10 @@ struct CgCtl {
 enum : int { kModeSkip = 0, kModeNormal = 1, kModeCheck = 2 };
 enum : int { kRunning = 0, kConverged = 1, kNotConverged = 2, kIndefinite = 3 };
 
-constexpr int kCgWarps = 4;     // warps (tasks) per CTA
+#ifndef MLG_CG_WARPS
+#define MLG_CG_WARPS 4
+#endif
+constexpr int kCgWarps = MLG_CG_WARPS;  // warps (tasks) per CTA
 constexpr int kCgCols = 28;     // output columns per warp task (2 halo lanes each side)
 constexpr int kCgRows = 64;     // max window rows per warp task
 constexpr int kCgDots = 5;      // partial sums per tile
@@ -78,6 +81,7 @@ class CgBatch {
   const unsigned char* mask = nullptr;
   const double* bsrc = nullptr;
   int bstride = 1;
+  bool use_async = false;  // HBM-streaming batches: shared-memory row pipeline
   std::vector<CgSys> sys_h;
   long long total_rows = 0;
   int total_tiles = 0;
