@@ -44,16 +44,14 @@ WORKLOADS = {
 FALLBACK_HBM = 6650.0
 
 
-def nr_for(nev):
-    return 1 if nev <= 1 else 2 if nev <= 2 else 4 if nev <= 4 else 8
-
-
-def ka_bytes_per_row(nev, uniform=False):
-    """Algorithmic bytes of one local-solve SpMV launch (k_cg_a) per active row:
-    stencil {C,E,N,NE} 32 B + D^-1 8 B (none when the level's interior stencil
-    is uniform and comes from kernel parameters), and per rhs lane r, p_old read
-    and p_new, q written (4 x 8 B); neighbours come from registers/shuffles."""
-    return (0 if uniform else 40) + 32 * nr_for(nev)
+def cg_bytes_per_row(uniform=False):
+    """Algorithmic HBM bytes per window row of one CG iteration launch (k_cg_iter,
+    the fused one-reduction PCG sweep): update mode reads x, r, p and writes x, r,
+    p (6 x 8 B = 48 B); true-residual mode reads x and b and writes r (24 B).
+    Non-uniform levels add the stencil {C,E,N,NE} and D^-1 (40 B); on uniform
+    levels they are kernel parameters.  Stencil neighbours come from registers
+    and warp shuffles, so nothing else is re-read.  Returns (update, check)."""
+    return (48, 24) if uniform else (88, 64)
 
 
 # ----------------------------------------------------------------- helpers ---
@@ -115,7 +113,7 @@ def measured_peak():
 
 
 def ncu_traffic(workload):
-    """Per-row DRAM traffic of k_cg_a from the committed ncu --set full summary."""
+    """Per-row DRAM traffic of k_cg_iter from the committed ncu --set full summary."""
     p = ROOT / "profiles" / "ka_traffic.json"
     try:
         d = json.loads(p.read_text())
@@ -283,18 +281,22 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
     ka_ms = sum(t.spmv_kernel_ms for t in tims)
     ka_n = sum(t.spmv_launches for t in tims)
     ka_rows = sum(t.spmv_rows for t in tims)
+    ka_chk = sum(t.spmv_check_rows for t in tims)
     if ka_n:
-        bpr = ka_bytes_per_row(nev, tims[-1].spmv_uniform_stencil)
-        achieved = ka_rows * bpr / (ka_ms * 1e-3) / 1e9
+        bpr, bpc = cg_bytes_per_row(tims[-1].spmv_uniform_stencil)
+        ka_bytes = ka_rows * bpr + ka_chk * bpc
+        achieved = ka_bytes / (ka_ms * 1e-3) / 1e9
         peak, peak_src = measured_peak()
         tr = ncu_traffic(workload)
         out["roofline"] = {
-            "kernel": "k_cg_a (local-solve fused p-update + window SpMV + p.q)",
+            "kernel": "k_cg_iter (local solves: fused PCG sweep, one launch per iteration)",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
-            "traffic": None if tr is None else tr * ka_rows / ka_n,
-            "algorithmic_bytes_per_launch": ka_rows / ka_n * bpr,
-            "bytes_per_row": bpr, "uniform_stencil": bool(tims[-1].spmv_uniform_stencil),
+            "traffic": None if tr is None else tr * (ka_rows + ka_chk) / ka_n,
+            "algorithmic_bytes_per_launch": ka_bytes / ka_n,
+            "bytes_per_row": bpr, "bytes_per_check_row": bpc,
+            "rows_per_launch": (ka_rows + ka_chk) / ka_n,
+            "uniform_stencil": bool(tims[-1].spmv_uniform_stencil),
             "avg_launch_ms": ka_ms / ka_n, "launches": int(ka_n),
             "share_of_step": ka_ms * 1e-3 / sum(step_s),
         }

@@ -78,14 +78,17 @@ typedef struct mlg_step_timings {
   double local_seconds, iface_seconds, aug_seconds; /* CUDA events, as StepTimings */
   double build_seconds;                             /* extend_to + region data of the step */
   int local_iterations_max, strip_iterations_max;
-  double spmv_kernel_ms;   /* summed device time of the local-solve SpMV kernel (profiling on) */
+  double spmv_kernel_ms;   /* summed device time of the sampled local-solve CG iteration
+                              launches (k_cg_iter, profiling on) */
   int64_t spmv_launches;   /* number of such launches */
-  double spmv_rows;        /* summed active rows over those launches */
+  double spmv_rows;        /* window rows those launches swept in CG-update mode (counted
+                              on the device) */
   int64_t kernel_launches; /* CG kernel launches of the step */
   double step_seconds;     /* CUDA events on the context stream around the whole call,
                               host<->device copies included for the host-array variant */
-  int spmv_uniform_stencil; /* 1: stencil/D^-1 taken from kernel parameters (bytes/row
-                               of the SpMV kernel = 32*NR instead of 40 + 32*NR) */
+  int spmv_uniform_stencil; /* 1: stencil/D^-1 taken from kernel parameters (no
+                               coefficient stream: 48 B/row instead of 88) */
+  double spmv_check_rows;  /* rows the same launches swept in true-residual mode */
 } mlg_step_timings;
 
 const char* mlg_last_error(void);

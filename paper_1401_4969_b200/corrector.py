@@ -83,13 +83,14 @@ class StepTimings:  # corrector.hpp:97-101 (+ device evidence)
     kernel_launches: int = 0
     step_seconds: float = 0.0
     spmv_uniform_stencil: bool = False
+    spmv_check_rows: float = 0.0
 
     @classmethod
     def from_c(cls, t: MlgStepTimings) -> "StepTimings":
         return cls(t.local_seconds, t.iface_seconds, t.aug_seconds, t.build_seconds,
                    t.local_iterations_max, t.strip_iterations_max, t.spmv_kernel_ms,
                    t.spmv_launches, t.spmv_rows, t.kernel_launches, t.step_seconds,
-                   bool(t.spmv_uniform_stencil))
+                   bool(t.spmv_uniform_stencil), t.spmv_check_rows)
 
 
 @dataclass

@@ -60,6 +60,7 @@ void fill_timings(mlg_step_timings* t, const mlg::StepTimes& s, const mlg::Ctx& 
   t->spmv_kernel_ms = c.times.ka_ms_sum;
   t->spmv_launches = c.times.ka_launches;
   t->spmv_rows = c.times.ka_rows;
+  t->spmv_check_rows = c.times.ka_check_rows;
   t->kernel_launches = mlg::launch_counter().load() - c.times.launch_base;
   t->spmv_uniform_stencil = c.times.ka_uniform;
 }
@@ -68,6 +69,7 @@ void reset_kernel_stats(mlg::Ctx& c) {
   c.times.ka_ms_sum = 0;
   c.times.ka_launches = 0;
   c.times.ka_rows = 0;
+  c.times.ka_check_rows = 0;
   c.times.kernel_launches = 0;
   c.times.launch_base = mlg::launch_counter().load();
 }

@@ -30,8 +30,11 @@
 // systems are dropped between chunks.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "cg.cuh"
 #include "stencil.cuh"
@@ -41,6 +44,17 @@ namespace {
 
 constexpr int kBlock = CgBatch::kBlock;
 constexpr unsigned kFull = 0xffffffffu;
+
+// Iterate loads.  The persistent kernel (CG) re-reads rows that other CTAs
+// rewrote in an earlier iteration of the same launch, so it must bypass the
+// (non-coherent) L1: ld.global.cg.
+template <bool CG>
+__device__ __forceinline__ double ldv(const double* p) {
+  if constexpr (CG)
+    return __ldcg(p);
+  else
+    return *p;
+}
 
 struct SweepArgs {
   const Stencil* st;
@@ -191,16 +205,6 @@ __device__ __forceinline__ bool task_interior(const CgSys& S, const SweepArgs& A
   return true;
 }
 
-// Task whose stencil rectangle (clamped to the window) avoids G entirely:
-// every point it touches is either in the system or outside the window.
-__device__ __forceinline__ bool task_unmasked(const CgSys& S, const SweepArgs& A, const Task& k) {
-  if (!A.mask) return true;
-  const int lane = threadIdx.x & 31;
-  const int c0 = max(k.col - lane, 0), c1 = min(k.col - lane + 31, S.w - 1);
-  const int r0 = max(k.ly0 - 2, 0), r1 = min(k.ly1 + 1, S.h - 1);
-  return rect_in_strip(A.sg, S.x0 + c0, S.x0 + c1, S.y0 + r0, S.y0 + r1);
-}
-
 __device__ __forceinline__ double product_full(double sv, double cv, double nv,
                                                const Stencil& u) {
   const double wv = __shfl_up_sync(kFull, cv, 1);
@@ -240,9 +244,9 @@ struct Flags {
   int gx;    // ... and inside its block's G x-range (masked systems)
   int masked;
   int h;
-  StripGeom g;
   int y0;    // window origin (fine lattice row of window row 0)
-  __device__ __forceinline__ int row_in(int ly) const {
+  // g: the kernel parameter's StripGeom (read in place, not copied)
+  __device__ __forceinline__ int row_in(int ly, const StripGeom& g) const {
     if (!cin || ly < 0 || ly >= h) return 0;
     if (!masked || !gx) return 1;
     const int iy = y0 + ly;
@@ -253,19 +257,10 @@ struct Flags {
   }
 };
 
-__device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs& A, const Task& k,
-                                                double al, double be, bool rst,
-                                                double* __restrict__ X,
-                                                const double* __restrict__ Rc,
-                                                double* __restrict__ Rn,
-                                                const double* __restrict__ Pc,
-                                                double* __restrict__ Pn,
-                                                double (&acc)[kCgDots]) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ Flags make_flags(const CgSys& S, const SweepArgs& A, const Task& k) {
   Flags f;
   f.cin = k.col >= 0 && k.col < S.w;
   f.masked = A.mask != nullptr;
-  f.g = A.sg;
   f.h = S.h;
   f.y0 = S.y0;
   f.gx = 0;
@@ -277,6 +272,20 @@ __device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs&
     const int xb = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
     f.gx = (ix >= xa && ix <= xb) ? 1 : 0;
   }
+  return f;
+}
+
+template <bool CG>
+__device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs& A, const Task& k,
+                                                double al, double be, bool rst,
+                                                double* __restrict__ X,
+                                                const double* __restrict__ Rc,
+                                                double* __restrict__ Rn,
+                                                const double* __restrict__ Pc,
+                                                double* __restrict__ Pn,
+                                                double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  const Flags f = make_flags(S, A, k);
   const bool out_col = lane >= 2 && lane < 2 + kCgCols && f.cin;
   const int w = S.w;
   const long long base = S.voff + k.col;
@@ -288,17 +297,17 @@ __device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs&
   const Stencil u = A.ust;
   const double dv = A.udinv;
   auto ld = [&](const double* __restrict__ p, int ly, int in) -> double {
-    return in ? p[ly * w] : 0.0;
+    return in ? ldv<CG>(p + ly * w) : 0.0;
   };
   // old p at rows n-1, n, n+1 (flags ia, ib, ic); r and x at rows n, n+1
-  int ia = f.row_in(k.ly0 - 2), ib = f.row_in(k.ly0 - 1), ic = f.row_in(k.ly0);
+  int ia = f.row_in(k.ly0 - 2, A.sg), ib = f.row_in(k.ly0 - 1, A.sg), ic = f.row_in(k.ly0, A.sg);
   double pa = ld(Ps, k.ly0 - 2, ia), pb = ld(Ps, k.ly0 - 1, ib), pc = ld(Ps, k.ly0, ic);
   double rb = ld(Rs, k.ly0 - 1, ib), xb = ld(Xs, k.ly0 - 1, ib);
   double rc = ld(Rs, k.ly0, ic), xc = ld(Xs, k.ly0, ic);
   double sp = 0.0, mp = 0.0, mz = 0.0;
   int sin_ = 0, min_ = 0;
   for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
-    const int id = n + 2 <= k.ly1 + 1 ? f.row_in(n + 2) : 0;
+    const int id = n + 2 <= k.ly1 + 1 ? f.row_in(n + 2, A.sg) : 0;
     const double pd = ld(Ps, n + 2, id);
     const double rd = ld(Rs, n + 2, id);
     const double xd = ld(Xs, n + 2, id);
@@ -344,36 +353,25 @@ __device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs&
 }
 
 // True residual r = b - A x of a constant-coefficient system (x current).
+template <bool CG>
 __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs& A,
                                                 const Task& k, const double* bsrc, int bstride,
                                                 const double* __restrict__ X,
                                                 double* __restrict__ Rn,
                                                 double (&acc)[kCgDots]) {
   const int lane = threadIdx.x & 31;
-  Flags f;
-  f.cin = k.col >= 0 && k.col < S.w;
-  f.masked = A.mask != nullptr;
-  f.g = A.sg;
-  f.h = S.h;
-  f.y0 = S.y0;
-  f.gx = 0;
-  if (f.masked && f.cin) {
-    const StripGeom& g = A.sg;
-    const int ix = S.x0 + k.col;
-    const int bx = min(ix / (g.bw * g.scale), g.side - 1);
-    const int xa = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
-    const int xb = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
-    f.gx = (ix >= xa && ix <= xb) ? 1 : 0;
-  }
+  const Flags f = make_flags(S, A, k);
   const bool out_col = lane >= 2 && lane < 2 + kCgCols && f.cin;
   const long long base = S.voff + k.col;
   const double* __restrict__ Xs = X + base;
   double* __restrict__ Rns = Rn + base;
-  auto ld = [&](int ly, int in) -> double { return in ? Xs[static_cast<long long>(ly) * S.w] : 0.0; };
-  int ia = f.row_in(k.ly0 - 1), ib = f.row_in(k.ly0);
+  auto ld = [&](int ly, int in) -> double {
+    return in ? ldv<CG>(Xs + static_cast<long long>(ly) * S.w) : 0.0;
+  };
+  int ia = f.row_in(k.ly0 - 1, A.sg), ib = f.row_in(k.ly0, A.sg);
   double xa = ld(k.ly0 - 1, ia), xb = ld(k.ly0, ib);
   for (int ly = k.ly0; ly < k.ly1; ++ly) {
-    const int ic = f.row_in(ly + 1);
+    const int ic = f.row_in(ly + 1, A.sg);
     const double xc = ld(ly + 1, ic);
     const double ax = product_flags(xa, ia, xb, ib, xc, ic, A.ust);
     if (out_col && ib) {
@@ -389,82 +387,207 @@ __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs&
   }
 }
 
-// Register-prefetch sweep (rows n+2, n+3 in flight in registers): best when
-// the batch's vectors are L2-resident (short latency, few rows needed in flight).
-__device__ __forceinline__ void sweep_interior_regs(const CgSys& S, const SweepArgs& A,
-                                                     const Task& k, double al, double be,
-                                                     bool rst, double* __restrict__ X,
-                                                     const double* __restrict__ Rc,
-                                                     double* __restrict__ Rn,
-                                                     const double* __restrict__ Pc,
-                                                     double* __restrict__ Pn,
-                                                     double (&acc)[kCgDots]) {
+// Register-prefetch sweep (rows n+2 .. n+4 in flight in registers): the path
+// for L2-resident batches (short latency, few rows needed in flight).
+//   EDGE = false: the task's stencil rectangle lies inside its system; no
+//     tests at all.  Every lane accumulates its dot-product terms and the
+//     halo lanes' sums are dropped at the end, so the only per-row predicate
+//     guards the three stores (predicated, not branched).
+//   EDGE = true: window-edge / strip-boundary task.  Points outside the system
+//     read as zero and get new p = 0, which reproduces the flagged product
+//     bit for bit (an absent neighbour contributes a literal 0 to the same
+//     paired-FMA chain); row loads are clamped into the window.
+// The first (stage 1 only) and last (stage 2 only) steps are peeled, so the
+// steady-state loop carries no row tests either.
+template <bool RST, bool EDGE, bool CG>
+__device__ __forceinline__ void sweep_regs(const CgSys& S, const SweepArgs& A, const Task& k,
+                                           double al, double be, double* __restrict__ X,
+                                           const double* __restrict__ Rc,
+                                           double* __restrict__ Rn,
+                                           const double* __restrict__ Pc,
+                                           double* __restrict__ Pn, double (&acc)[kCgDots]) {
   const int lane = threadIdx.x & 31;
-  const bool out = lane >= 2 && lane < 2 + kCgCols;
+  const Flags f = make_flags(S, A, k);  // EDGE only
+  const bool own = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
   const int w = S.w;
-  double* __restrict__ Xs = X + S.voff + k.col;
-  const double* __restrict__ Rs = Rc + S.voff + k.col;
-  double* __restrict__ Rns = Rn + S.voff + k.col;
-  const double* __restrict__ Ps = Pc + S.voff + k.col;
-  double* __restrict__ Pns = Pn + S.voff + k.col;
+  const int col = EDGE ? min(max(k.col, 0), w - 1) : k.col;  // address-safe column
+  const long long base = S.voff + col;
+  double* __restrict__ Xs = X + base;
+  const double* __restrict__ Rs = Rc + base;
+  double* __restrict__ Rns = Rn + base;
+  const double* __restrict__ Ps = Pc + base;
+  double* __restrict__ Pns = Pn + base;
   const Stencil u = A.ust;
   const double dv = A.udinv;
-  // old p at rows n-1, n, n+1; r and x at rows n, n+1; rows n+2, n+3 in
-  // flight -- loads are issued three sweep steps before use (latency hiding
-  // at ~20 resident warps per SM needs several rows per warp in flight)
-  const int last = k.ly1 + 1;  // last old row needed
-  auto row = [&](const double* __restrict__ p, int ly) -> double {
-    return ly <= last ? p[ly * w] : 0.0;
+  const int rlo = EDGE ? 0 : k.ly0 - 2;                   // first row that exists
+  const int rhi = EDGE ? min(k.ly1 + 1, S.h - 1) : k.ly1 + 1;  // last row needed & existing
+  struct V {
+    double p, r, x;
+    bool in;
   };
-  double pa = row(Ps, k.ly0 - 2), pb = row(Ps, k.ly0 - 1), pc = row(Ps, k.ly0);
-  double rb = row(Rs, k.ly0 - 1), xb = row(Xs, k.ly0 - 1);
-  double rc = row(Rs, k.ly0), xc = row(Xs, k.ly0);
-  double p2 = row(Ps, k.ly0 + 1), r2 = row(Rs, k.ly0 + 1), x2 = row(Xs, k.ly0 + 1);
-  double p3 = row(Ps, k.ly0 + 2), r3 = row(Rs, k.ly0 + 2), x3 = row(Xs, k.ly0 + 2);
+  auto load = [&](int row) {
+    V v;
+    const long long o = static_cast<long long>(min(max(row, rlo), rhi)) * w;
+    v.p = ldv<CG>(Ps + o);
+    v.r = ldv<CG>(Rs + o);
+    v.x = ldv<CG>(Xs + o);
+    v.in = true;
+    if constexpr (EDGE) {
+      v.in = f.row_in(row, A.sg) != 0;
+      if (!v.in) v.p = v.r = v.x = 0.0;
+    }
+    return v;
+  };
+  V a = load(k.ly0 - 2), b = load(k.ly0 - 1), c = load(k.ly0);
+  V d1 = load(k.ly0 + 1), d2 = load(k.ly0 + 2);
   double sp = 0.0, mp = 0.0, mz = 0.0;
-#pragma unroll 2
-  for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
-    const int in = n * w;  // row n
-    const double pd = row(Ps, n + 4), rd = row(Rs, n + 4), xd = row(Xs, n + 4);
-    double rn = rb, xn = xb;
-    if (!rst) {
-      const double qo = product_full(pa, pb, pc, u);
-      rn = fma(-al, qo, rb);
-      xn = fma(al, pb, xb);
+  bool m_in = false;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+  auto step = [&](int n, auto store, auto stage2) {
+    const V nx = load(n + 4);  // window: a..d2 = rows n-1 .. n+3
+    double rn = b.r, xn = b.x;
+    if constexpr (!RST) {
+      const double qo = product_full(a.p, b.p, c.p, u);
+      rn = fma(-al, qo, b.r);
+      xn = fma(al, b.p, b.x);
     }
     const double tz = xmul(dv, rn);
-    const double tp = rst ? tz : fma(be, pb, tz);
-    if (out && n >= k.ly0 && n < k.ly1) {
-      Xs[in] = xn;
-      Rns[in] = rn;
-      Pns[in] = tp;
-      acc[0] += rn * rn;
-      acc[1] += rn * tz;
+    double tp = RST ? tz : fma(be, b.p, tz);
+    if constexpr (EDGE)
+      if (!b.in) tp = 0.0;
+    if constexpr (decltype(store)::value) {
+      if (own && b.in) {
+        const long long o = static_cast<long long>(n) * w;
+        Xs[o] = xn;
+        Rns[o] = rn;
+        Pns[o] = tp;
+      }
+      if (!EDGE || (own && b.in)) {
+        a0 += rn * rn;
+        a1 += rn * tz;
+      }
     }
-    if (n - 1 >= k.ly0) {
+    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
       const double q = product_full(sp, mp, tp, u);
-      if (out) {
-        acc[2] += mp * q;
-        acc[3] += q * mz;
-        acc[4] += q * xmul(dv, q);
+      if (!EDGE || (own && m_in)) {
+        a2 += mp * q;
+        a3 += q * mz;
+        a4 += q * xmul(dv, q);
       }
     }
     sp = mp;
     mp = tp;
     mz = tz;
-    pa = pb;
-    pb = pc;
-    pc = p2;
-    p2 = p3;
-    p3 = pd;
-    rb = rc;
-    xb = xc;
-    rc = r2;
-    xc = x2;
-    r2 = r3;
-    x2 = x3;
-    r3 = rd;
-    x3 = xd;
+    m_in = b.in;
+    a = b;
+    b = c;
+    c = d1;
+    d1 = d2;
+    d2 = nx;
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  step(k.ly0 - 1, F{}, F{});
+  step(k.ly0, T{}, F{});
+  for (int n = k.ly0 + 1; n < k.ly1; ++n) step(n, T{}, T{});
+  step(k.ly1, F{}, T{});
+  if (EDGE || own) {  // halo lanes' terms are dropped (EDGE: never accumulated)
+    acc[0] += a0;
+    acc[1] += a1;
+    acc[2] += a2;
+    acc[3] += a3;
+    acc[4] += a4;
+  }
+}
+
+// Interior register sweep with running row pointers (no per-row index math:
+// the pooled vectors carry kCgPadRows rows of padding, so prefetches past a
+// window read padding or the next system and are never used).  LAP: the
+// level's interior stencil is the 5-point Laplacian {4, -1, -1, 0} with
+// D^-1 = 1/4 (P1 on the right-triangle lattice): constants are immediates and
+// the zero SW/NE pair is skipped -- fma(0, s, y) == y for finite s, so the
+// row product is bitwise the generic paired-FMA product.
+template <bool LAP>
+__device__ __forceinline__ double product_int(double sv, double cv, double nv, const Stencil& u) {
+  const double wv = __shfl_up_sync(kFull, cv, 1);
+  const double ev = __shfl_down_sync(kFull, cv, 1);
+  if constexpr (LAP) {
+    return fma(-1.0, wv + ev, fma(-1.0, sv + nv, 4.0 * cv));
+  } else {
+    const double swv = __shfl_up_sync(kFull, sv, 1);
+    const double nev = __shfl_down_sync(kFull, nv, 1);
+    return fma(u.e, wv + ev, fma(u.n, sv + nv, fma(u.ne, swv + nev, u.c * cv)));
+  }
+}
+
+template <bool RST, bool CG, bool LAP>
+__device__ __forceinline__ void sweep_int(const CgSys& S, const SweepArgs& A, const Task& k,
+                                          double al, double be, double* __restrict__ X,
+                                          const double* __restrict__ Rc,
+                                          double* __restrict__ Rn,
+                                          const double* __restrict__ Pc,
+                                          double* __restrict__ Pn, double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  const bool own = lane >= 2 && lane < 2 + kCgCols;
+  const long long w = S.w;
+  long long lo = S.voff + k.col + (k.ly0 - 2) * w;  // next row to load (starts at ly0-2)
+  long long so = lo + 2 * w;                         // next row to store (starts at ly0)
+  const Stencil u = A.ust;
+  const double dv = LAP ? 0.25 : A.udinv;
+  struct V {
+    double p, r, x;
+  };
+  auto load = [&]() {
+    V v{ldv<CG>(Pc + lo), ldv<CG>(Rc + lo), ldv<CG>(X + lo)};
+    lo += w;
+    return v;
+  };
+  V a = load(), b = load(), c = load(), d1 = load(), d2 = load();  // rows ly0-2 .. ly0+2
+  double sp = 0.0, mp = 0.0, mz = 0.0;
+  auto step = [&](auto store, auto stage2) {
+    const V nx = load();  // row n+4
+    double rn = b.r, xn = b.x;
+    if constexpr (!RST) {
+      const double qo = product_int<LAP>(a.p, b.p, c.p, u);
+      rn = fma(-al, qo, b.r);
+      xn = fma(al, b.p, b.x);
+    }
+    const double tz = xmul(dv, rn);
+    const double tp = RST ? tz : fma(be, b.p, tz);
+    if constexpr (decltype(store)::value) {
+      if (own) {
+        X[so] = xn;
+        Rn[so] = rn;
+        Pn[so] = tp;
+      }
+      so += w;
+      acc[0] += rn * rn;
+      acc[1] += rn * tz;
+    }
+    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
+      const double q = product_int<LAP>(sp, mp, tp, u);
+      acc[2] += mp * q;
+      acc[3] += q * mz;
+      acc[4] += q * xmul(dv, q);
+    }
+    sp = mp;
+    mp = tp;
+    mz = tz;
+    a = b;
+    b = c;
+    c = d1;
+    d1 = d2;
+    d2 = nx;
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  step(F{}, F{});  // row ly0-1: stage 1 only
+  step(T{}, F{});  // row ly0
+  for (int n = k.ly0 + 1; n < k.ly1; ++n) step(T{}, T{});
+  step(F{}, T{});  // row ly1: stage 2 for ly1-1
+  if (!own) {      // the halo lanes' terms are dropped (acc is fresh per tile)
+#pragma unroll
+    for (int q = 0; q < kCgDots; ++q) acc[q] = 0.0;
   }
 }
 
@@ -502,11 +625,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// EDGE: the task touches the window boundary.  Lanes whose column lies outside
-// the window and rows outside it read zeros (the slot is zero-filled instead of
-// copied) and their new p is forced to zero, which reproduces the flagged
-// product exactly (an absent neighbour contributes a literal 0 to the same
-// paired-FMA chain).
+// EDGE: the task touches the window boundary or (strip systems) the inner
+// regions G.  Points outside the system -- column or row outside the window,
+// or inside G (separable test, Flags) -- read zeros (the slot is zero-filled
+// instead of copied) and their new p is forced to zero, which reproduces the
+// flagged product exactly (an absent neighbour contributes a literal 0 to the
+// same paired-FMA chain).
 template <bool RST, bool EDGE>
 __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, const Task& k,
                                             double al, double be, double* __restrict__ X,
@@ -516,10 +640,9 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
                                             double* __restrict__ Pn, double (&acc)[kCgDots],
                                             RowRing& ring) {
   const int lane = threadIdx.x & 31;
-  const bool cval = !EDGE || (k.col >= 0 && k.col < S.w);
-  const bool out = lane >= 2 && lane < 2 + kCgCols && cval;
+  const Flags f = make_flags(S, A, k);  // EDGE only
+  const bool out = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
   const int w = S.w;
-  const int h = S.h;
   const long long base = S.voff + k.col;
   double* __restrict__ Xs = X + base;
   const double* __restrict__ Rs = Rc + base;
@@ -532,7 +655,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
   auto issue = [&](int row) {  // one commit group per row, empty past the end
     if (row <= last) {
       const int s = row & (kD - 1);
-      if (!EDGE || (cval && row >= 0 && row < h)) {
+      if (!EDGE || f.row_in(row, A.sg)) {
         const long long o = static_cast<long long>(row) * w;
         cp_async8(&ring.v[s][0][lane], Ps + o);
         cp_async8(&ring.v[s][1][lane], Rs + o);
@@ -552,6 +675,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
   double pb = ring.v[(k.ly0 - 1) & (kD - 1)][0][lane];
   issue(k.ly0 - 2 + kD);  // slot of row ly0-2 consumed
   double sp = 0.0, mp = 0.0, mz = 0.0;
+  bool min_ = false;  // row n-1 in the system
   for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
     // issued up to row n+kD-1; row n+1 must have landed
     cp_async_wait<kD - 2>();
@@ -567,8 +691,9 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     }
     const double tz = xmul(dv, rn);
     double tp = RST ? tz : fma(be, pb, tz);
-    if (EDGE && !(cval && n >= 0 && n < h)) tp = 0.0;
-    if (out && n >= k.ly0 && n < k.ly1) {
+    const bool nin = !EDGE || f.row_in(n, A.sg);
+    if (!nin) tp = 0.0;
+    if (out && nin && n >= k.ly0 && n < k.ly1) {
       const long long o = static_cast<long long>(n) * w;
       Xs[o] = xn;
       Rns[o] = rn;
@@ -578,7 +703,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     }
     // stage 2 at row n-1 (computed unconditionally: no branch around shuffles)
     const double q = product_full(sp, mp, tp, u);
-    if (out && n - 1 >= k.ly0) {
+    if (out && min_ && n - 1 >= k.ly0) {
       acc[2] += mp * q;
       acc[3] += q * mz;
       acc[4] += q * xmul(dv, q);
@@ -586,6 +711,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     sp = mp;
     mp = tp;
     mz = tz;
+    min_ = nin;
     pa = pb;
     pb = pc;
     issue(n + kD);  // refill slot n (its p, r, x are consumed)
@@ -658,7 +784,24 @@ struct Finish {
   unsigned* counter;
   CgCtl* ctl;
   double tol;
+  unsigned long long* rows;  // sampled launches: [update-mode rows, check-mode rows]
+  int* active;               // systems still running (decremented when one stops)
 };
+
+// Scalars of a system as last written by any CTA (L2, not a stale L1 line).
+__device__ __forceinline__ CgCtl load_ctl(const CgCtl* p) {
+  CgCtl c;
+  c.alpha = __ldcg(&p->alpha);
+  c.beta = __ldcg(&p->beta);
+  c.rho = __ldcg(&p->rho);
+  c.bnorm = __ldcg(&p->bnorm);
+  c.final_res = __ldcg(&p->final_res);
+  c.mode = __ldcg(&p->mode);
+  c.restart = __ldcg(&p->restart);
+  c.iters = __ldcg(&p->iters);
+  c.status = __ldcg(&p->status);
+  return c;
+}
 
 // Block partial -> partials[tile]; the last tile of the system to arrive sums
 // all partials of the system in tile order (fixed, deterministic) and
@@ -678,25 +821,41 @@ __device__ __forceinline__ void finish_tile(const CgSys& S, int sys, int t,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
+  // All threads of the last tile sum the system's tile partials (thread t takes
+  // tiles t, t + kBlock, ...; then a fixed tree): the order is fixed, so the
+  // scalars are bitwise reproducible, and the latency is ~ntiles/kBlock loads.
+  {
     double a[kCgDots];
 #pragma unroll
     for (int q = 0; q < kCgDots; ++q) a[q] = 0.0;
-    for (int tt = lane; tt < S.ntiles; tt += 32) {
+    for (int tt = threadIdx.x; tt < S.ntiles; tt += kBlock) {
       const double* p = F.part + static_cast<long long>(S.toff + tt) * kCgDots;
 #pragma unroll
       for (int q = 0; q < kCgDots; ++q) a[q] += __ldcg(p + q);
     }
+    __shared__ double s_red[kCgWarps][kCgDots];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int q = 0; q < kCgDots; ++q) a[q] += __shfl_xor_sync(kFull, a[q], o);
-    if (lane == 0) {
-      CgCtl c = F.ctl[sys];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < kCgDots; ++q) s_red[warp][q] = a[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < kCgDots; ++q) {
+        double v = 0.0;
+        for (int w = 0; w < kCgWarps; ++w) v += s_red[w][q];
+        a[q] = v;
+      }
+      CgCtl c = load_ctl(F.ctl + sys);
+      const bool was_running = PH == kPhaseInit || c.status == kRunning;
       update_ctl<PH>(c, a, F.tol, S.maxit);
       F.ctl[sys] = c;
       F.counter[sys] = 0u;
+      if (was_running && c.status != kRunning) atomicSub(F.active, 1);
     }
   }
 }
@@ -730,31 +889,25 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
 #ifndef MLG_CG_MINBLOCKS
 #define MLG_CG_MINBLOCKS 5
 #endif
-template <bool UNI, bool ASYNC>
-__global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBLOCKS : MLG_CG_MINBLOCKS) * 4 / kCgWarps)
-    k_cg_iter(const CgSys* sys, const CgTile* tiles, SweepArgs A, const double* bsrc,
-              int bstride, double* __restrict__ X, const double* __restrict__ Rc,
-              double* __restrict__ Rn, const double* __restrict__ Pc, double* __restrict__ Pn,
-              Finish F) {
-  const CgTile tl = tiles[blockIdx.x];
-  const CgSys S = sys[tl.sys];
-  __shared__ CgCtl s_c;
-  extern __shared__ RowRing s_ring[];  // kCgWarps rings (ASYNC only)
-  if (threadIdx.x == 0) s_c = F.ctl[tl.sys];
-  __syncthreads();
-  const int mode = s_c.mode;
+// One tile (kCgWarps warp tasks of one system) of one CG iteration.  PERSIST:
+// called from the persistent kernel (L1-bypassing iterate loads, rows counted
+// in `rows_acc` instead of per-launch atomics).
+template <bool UNI, bool ASYNC, bool PERSIST, bool LAP>
+__device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mode, double al,
+                                        double be, bool rst, const SweepArgs& A,
+                                        const double* bsrc, int bstride, double* __restrict__ X,
+                                        const double* __restrict__ Rc, double* __restrict__ Rn,
+                                        const double* __restrict__ Pc, double* __restrict__ Pn,
+                                        const Finish& F, RowRing* s_ring,
+                                        unsigned long long& rows_acc) {
   if (mode == kModeSkip) return;  // uniform across the system's tiles
-  const double al = s_c.alpha, be = s_c.beta;
-  const bool rst = s_c.restart != 0;
   const Task k = task_of(S, tl.t, A.task_map);
   const bool out = out_lane(S, k);
   double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
   bool fast = false, edge = false, flagged = false;
   if constexpr (UNI) {
     fast = k.valid && mode == kModeNormal && task_interior(S, A, k);
-    if (ASYNC && k.valid && mode == kModeNormal && !fast && task_unmasked(S, A, k)) {
-      edge = true;
-    }
+    edge = ASYNC && k.valid && mode == kModeNormal && !fast;
     flagged = k.valid && mode == kModeNormal && !fast && !edge;
   }
   if (fast) {
@@ -765,7 +918,10 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
       else
         sweep_async<false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
     } else {
-      sweep_interior_regs(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
+      if (rst)
+        sweep_int<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+      else
+        sweep_int<false, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
     }
   } else if (ASYNC && edge) {
     RowRing& ring = s_ring[threadIdx.x >> 5];
@@ -774,7 +930,10 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
     else
       sweep_async<false, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
   } else if (flagged) {
-    fused_sweep_uni(S, A, k, al, be, rst, X, Rc, Rn, Pc, Pn, acc);
+    if (rst)
+      sweep_regs<true, true, PERSIST>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+    else
+      sweep_regs<false, true, PERSIST>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
   } else if (!UNI && k.valid && mode == kModeNormal) {
     ORow a, b, c, d;  // old iterate at rows n-1, n, n+1 (and n+2 in flight)
     NRow s, m;        // new p at rows n-2, n-1
@@ -825,7 +984,7 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
       c = d;
     }
   } else if (UNI && k.valid) {  // kModeCheck, constant coefficients: r = b - A x
-    check_sweep_uni(S, A, k, bsrc, bstride, X, Rn, acc);
+    check_sweep_uni<PERSIST>(S, A, k, bsrc, bstride, X, Rn, acc);
   } else if (k.valid) {  // kModeCheck: r = b - A x (x is current: updated in place)
     ORow a, b, c;
     load_old<UNI>(S, A, k.col, k.ly0 - 1, Rc, Pc, X, a);
@@ -844,8 +1003,131 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
       b = c;
     }
   }
+  if (F.rows && k.valid && A.mask == nullptr) {  // roofline evidence (unmasked systems)
+    const unsigned n = __reduce_add_sync(kFull, out ? static_cast<unsigned>(k.ly1 - k.ly0) : 0u);
+    if (PERSIST) {  // packed: update rows low 40 bits, check rows high 24 bits / 2^40
+      rows_acc += mode == kModeCheck ? (1ull * n) << 40 : 1ull * n;
+    } else if ((threadIdx.x & 31) == 0) {
+      atomicAdd(F.rows + (mode == kModeCheck ? 1 : 0), 1ull * n);
+    }
+  }
   finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
 }
+
+template <bool UNI, bool ASYNC, bool LAP>
+__global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBLOCKS : MLG_CG_MINBLOCKS) * 4 / kCgWarps)
+    k_cg_iter(const CgSys* sys, const CgTile* tiles, SweepArgs A, const double* bsrc,
+              int bstride, double* __restrict__ X, const double* __restrict__ Rc,
+              double* __restrict__ Rn, const double* __restrict__ Pc, double* __restrict__ Pn,
+              Finish F) {
+  const CgTile tl = tiles[blockIdx.x];
+  const CgSys S = sys[tl.sys];
+  __shared__ CgCtl s_c;
+  extern __shared__ RowRing s_ring[];  // kCgWarps rings (ASYNC only)
+  if (threadIdx.x == 0) s_c = F.ctl[tl.sys];
+  __syncthreads();
+  unsigned long long rows_acc = 0;
+  cg_tile<UNI, ASYNC, false, LAP>(S, tl, s_c.mode, s_c.alpha, s_c.beta, s_c.restart != 0, A, bsrc,
+                             bstride, X, Rc, Rn, Pc, Pn, F, s_ring, rows_acc);
+}
+
+// ---- persistent variant: all iterations of a batch in one launch -----------
+// For batches whose iterates are L2-resident the per-launch ramp/drain
+// dominates; here every CTA keeps a fixed set of <= kPersistTiles tiles and the
+// iterations are separated by a grid barrier (co-residency guaranteed by the
+// cooperative launch).  Same tile bodies, same reductions (the last tile of a
+// system advances its scalars before arriving at the barrier), so the iterates
+// are identical to the multi-launch path.
+constexpr int kPersistTiles = 8;
+
+struct GridSync {
+  unsigned* count;  // arrivals at the current barrier
+  unsigned* gen;    // barrier generation
+  int* active;      // systems still running
+  int max_iters;    // safety bound (every system stops by maxit)
+};
+
+__device__ __forceinline__ void grid_sync(const GridSync& G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = G.gen;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(G.count, 1u) == gridDim.x - 1) {
+      atomicExch(G.count, 0u);
+      __threadfence();
+      atomicAdd(G.gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+#ifdef MLG_CG_TRACE
+__device__ unsigned long long g_trace[4096][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) \
+  if (it == MLG_CG_TRACE && threadIdx.x == 0 && blockIdx.x < 4096) g_trace[blockIdx.x][slot] = gtimer()
+#else
+#define TRACE(slot)
+#endif
+
+template <bool UNI, bool LAP>
+__global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS * 4 / kCgWarps)
+    k_cg_persist(const CgSys* sys, const CgTile* tiles, int ntiles, SweepArgs A,
+                 const double* bsrc, int bstride, double* __restrict__ X, double* R0,
+                 double* R1, double* P0, double* P1, Finish F, GridSync G) {
+  __shared__ CgSys s_sys[kPersistTiles];
+  __shared__ CgTile s_tl[kPersistTiles];
+  __shared__ int s_mode[kPersistTiles], s_rst[kPersistTiles];
+  __shared__ double s_al[kPersistTiles], s_be[kPersistTiles];
+  __shared__ int s_active;
+  const int mine = (ntiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1;
+  if (threadIdx.x < mine) {
+    const CgTile t = tiles[blockIdx.x + threadIdx.x * gridDim.x];
+    s_tl[threadIdx.x] = t;
+    s_sys[threadIdx.x] = sys[t.sys];
+  }
+  unsigned long long rows_acc = 0;
+  for (int it = 0; it < G.max_iters; ++it) {
+    const bool odd = it & 1;
+    TRACE(0);
+    if (threadIdx.x < mine) {  // scalars written by other CTAs: read through L2
+      const CgCtl* c = F.ctl + s_tl[threadIdx.x].sys;
+      s_mode[threadIdx.x] = __ldcg(&c->mode);
+      s_rst[threadIdx.x] = __ldcg(&c->restart);
+      s_al[threadIdx.x] = __ldcg(&c->alpha);
+      s_be[threadIdx.x] = __ldcg(&c->beta);
+    }
+    __syncthreads();
+    TRACE(1);
+    for (int i = 0; i < mine; ++i) {
+      cg_tile<UNI, false, true, LAP>(s_sys[i], s_tl[i], s_mode[i], s_al[i], s_be[i], s_rst[i] != 0, A,
+                                bsrc, bstride, X, odd ? R1 : R0, odd ? R0 : R1, odd ? P1 : P0,
+                                odd ? P0 : P1, F, nullptr, rows_acc);
+      __syncthreads();  // shared scratch of the tile body is reused
+      if (i < 4) TRACE(2 + i);
+    }
+    TRACE(6);
+    grid_sync(G);
+    TRACE(7);
+    if (threadIdx.x == 0) s_active = __ldcg(G.active);
+    __syncthreads();
+    if (s_active == 0) break;
+  }
+  if (F.rows && (threadIdx.x & 31) == 0 && rows_acc) {
+    atomicAdd(F.rows, rows_acc & ((1ull << 40) - 1));
+    atomicAdd(F.rows + 1, rows_acc >> 40);
+  }
+}
+
+
 
 constexpr int kRingBytes = kCgWarps * static_cast<int>(sizeof(RowRing));
 
@@ -856,21 +1138,32 @@ int resident_tiles(bool async) {
                                cudaGetDevice(&dev);
                                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
                                cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                   &per, k_cg_iter<true, false>, kBlock, 0);
+                                   &per, k_cg_iter<true, false, true>, kBlock, 0);
                                return std::max(1, sms * std::max(per, 1));
                              }(),
                              [] {
                                int dev = 0, sms = 0, per = 0;
                                cudaGetDevice(&dev);
                                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                               cudaFuncSetAttribute(k_cg_iter<true, true>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    kRingBytes);
+                               for (auto fn : {k_cg_iter<true, true, true>, k_cg_iter<true, true, false>})
+                                 cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      kRingBytes);
                                cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                   &per, k_cg_iter<true, true>, kBlock, kRingBytes);
+                                   &per, k_cg_iter<true, true, true>, kBlock, kRingBytes);
                                return std::max(1, sms * std::max(per, 1));
                              }()};
   return res[async ? 1 : 0];
+}
+
+int resident_persist() {
+  static const int res = [] {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cg_persist<true, true>, kBlock, 0);
+    return std::max(1, sms * std::max(per, 1));
+  }();
+  return res;
 }
 
 SweepArgs sweep_args(const Level& L, const unsigned char* mask) {
@@ -906,6 +1199,12 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   }();
   use_async = lev.uniform != 0 &&
               (async_env >= 0 ? async_env != 0 : all_rows * 48 > (128LL << 20));
+  // L2-resident constant-coefficient batches: one persistent launch per solve.
+  static const int persist_env = [] {
+    const char* e = std::getenv("MLG_CG_PERSIST");  // A/B hook: 0 / 1
+    return e ? std::atoi(e) : 1;
+  }();
+  use_persist = lev.uniform != 0 && !use_async && persist_env != 0;
   // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
   // must still offer >= ~8k warps (148 SMs x ~56 resident) to hide latency.
   static const long long target_tasks = [] {
@@ -916,13 +1215,18 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
     const char* e = std::getenv("MLG_CG_MINROWS");  // tuning hook
     return e ? std::atoi(e) : 16;
   }();
+  static const int max_rows_async = [] {
+    const char* e = std::getenv("MLG_CG_MAXROWS");  // tuning hook
+    return e ? std::atoi(e) : kCgRowsAsync;
+  }();
+  const int max_rows = use_async ? max_rows_async : kCgRows;
   int krows = static_cast<int>(std::min<long long>(
-      kCgRows, std::max<long long>(min_rows, all_rows / (kCgCols * target_tasks))));
+      max_rows, std::max<long long>(min_rows, all_rows / (kCgCols * target_tasks))));
   // Wave quantisation: every tile costs ~(krows + 3) row steps and the grid
   // runs in waves of `resident` tiles, so pick the row count that minimises
   // waves x (krows + 3) among the candidates at or below the first choice.
   {
-    const int resident = resident_tiles(use_async);
+    const int resident = use_persist ? resident_persist() : resident_tiles(use_async);
     auto tiles_for = [&](int kr) {
       long long t = 0;
       for (const CgSys& s : systems) {
@@ -943,6 +1247,8 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
       }
     }
     krows = best_k;
+    if (use_persist && (tiles_for(krows) + resident - 1) / resident > kPersistTiles)
+      use_persist = false;  // too many tiles per CTA: multi-launch path
   }
   for (CgSys& s : systems) {
     s.nrows = s.w * s.h;
@@ -989,7 +1295,10 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   task_map.ensure(std::max<std::size_t>(tmap.size(), 1));
   if (!tmap.empty()) task_map.upload(tmap.data(), tmap.size(), c.stream);
   sys_h = std::move(systems);
-  const std::size_t nv = static_cast<std::size_t>(total_rows);
+  // padding: interior sweeps prefetch up to 4 rows past their window
+  int max_w = 1;
+  for (const CgSys& q : sys_h) max_w = std::max(max_w, q.w);
+  const std::size_t nv = static_cast<std::size_t>(total_rows) + kCgPadRows * max_w + 64;
   X.ensure(nv);
   R0.ensure(nv);
   R1.ensure(nv);
@@ -1012,24 +1321,33 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     sys_d.upload(sys_h.data(), sys_h.size(), c.stream);
   }
   std::vector<CgTile> tiles;
-  long long active_rows = 0;
   auto rebuild = [&](const std::vector<char>& active) {
     tiles.clear();
-    active_rows = 0;
     for (int s = 0; s < nsys; ++s)
-      if (active[s]) {
-        active_rows += sys_h[s].nrows;
+      if (active[s])
         for (int t = 0; t < sys_h[s].ntiles; ++t) tiles.push_back({s, t});
-      }
     tiles_d.upload(tiles.data(), tiles.size(), c.stream);
   };
   std::vector<char> active(nsys, 1);
   rebuild(active);
   cudaStream_t st = c.stream;
   const bool uni = L->uniform != 0;
+  // 5-point Laplacian stencil (P1 Laplace on the right-triangle lattice)
+  const bool lap = uni && L->ust.c == 4.0 && L->ust.e == -1.0 && L->ust.n == -1.0 &&
+                   L->ust.ne == 0.0 && L->udinv == 0.25 && std::getenv("MLG_CG_NOLAP") == nullptr;
   SweepArgs A = sweep_args(*L, mask);
   A.task_map = task_map.get();
-  const Finish F{part.get(), counters.get(), ctl_d.get(), tol};
+  const bool profiling = c.profile && mask == nullptr;
+  if (profiling) {
+    prof_rows.ensure(2);
+    prof_rows.zero(c.stream);
+  }
+  gsync.ensure(2);
+  gsync.zero(st);
+  active_d.ensure(1);
+  active_d.upload(&nsys, 1, st);
+  const Finish F{part.get(), counters.get(), ctl_d.get(), tol, nullptr, active_d.get()};
+  const Finish Fp{part.get(), counters.get(), ctl_d.get(), tol, prof_rows.get(), active_d.get()};
   double *rc = R0.get(), *rn = R1.get(), *pc = P0.get(), *pn = P1.get();
 
   if (uni)
@@ -1044,28 +1362,103 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
   int chunk = 16;
   long long iter_count = 0;
-  while (true) {
-    for (int it = 0; it < chunk && !tiles.empty(); ++it) {
-      const unsigned nt = static_cast<unsigned>(tiles.size());
-      // Kernel timing evidence: every 4th launch of the local solves is
-      // bracketed by pooled CUDA events (cheap enough not to starve the stream).
-      const bool prof = c.profile && mask == nullptr && (iter_count++ % 4 == 0);
+  if (use_persist) {
+    // All iterations in cooperative launches of at most kIters iterations (an
+    // even count, so the vector parity is unchanged between launches).
+    constexpr int kIters = 4096;
+    const int ntiles = static_cast<int>(tiles.size());
+    const int grid = std::min(ntiles, resident_persist());
+    const CgSys* sp = sys_d.get();
+    const CgTile* tp = tiles_d.get();
+    double* xp = X.get();
+    double *r0 = R0.get(), *r1 = R1.get(), *p0 = P0.get(), *p1 = P1.get();
+    const Finish& Fl = profiling ? Fp : F;
+    GridSync G{gsync.get(), gsync.get() + 1, active_d.get(), kIters};
+    void* args[] = {(void*)&sp, (void*)&tp, (void*)&ntiles, (void*)&A, (void*)&bsrc,
+                    (void*)&bstride, (void*)&xp, (void*)&r0, (void*)&r1, (void*)&p0,
+                    (void*)&p1, (void*)&Fl, (void*)&G};
+    for (int launch = 0;; ++launch) {
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-      if (prof) {
-        c.times.ka_rows += static_cast<double>(active_rows);
+      if (profiling) {
         ev0 = c.event(2 * evs.size());
         ev1 = c.event(2 * evs.size() + 1);
         MLG_CUDA(cudaEventRecord(ev0, st));
       }
-      if (uni && use_async)
-        k_cg_iter<true, true><<<nt, kBlock, kRingBytes, st>>>(
-            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, F);
+      const void* fn = lap ? reinterpret_cast<const void*>(&k_cg_persist<true, true>)
+                           : reinterpret_cast<const void*>(&k_cg_persist<true, false>);
+      MLG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args, 0, st));
+      ++launch_counter();
+      if (profiling) {
+        MLG_CUDA(cudaEventRecord(ev1, st));
+        evs.emplace_back(ev0, ev1);
+      }
+      int left = 0;
+      active_d.download(&left, 1, st);
+      c.sync();
+      if (left == 0) break;
+      if (launch > 1000) throw SolverError("cg_solve: persistent CG did not terminate");
+    }
+#ifdef MLG_CG_TRACE
+    {
+      static unsigned long long tr[4096][8];
+      MLG_CUDA(cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr)));
+      unsigned long long t0 = ~0ull, t7 = 0;
+      double s1 = 0, s6 = 0, s7 = 0, m6 = 0;
+      for (int b = 0; b < grid; ++b) {
+        t0 = std::min(t0, tr[b][0]);
+        t7 = std::max(t7, tr[b][7]);
+      }
+      for (int b = 0; b < grid; ++b) {
+        s1 += tr[b][1] - tr[b][0];
+        s6 += tr[b][6] - tr[b][1];
+        m6 = std::max(m6, double(tr[b][6] - t0));
+        s7 += tr[b][7] - tr[b][6];
+      }
+      fprintf(stderr, "trace: grid %d tiles %d span %.2f us | ctl %.2f work %.2f (last done %.2f) barrier %.2f us avg\n",
+              grid, ntiles, (t7 - t0) * 1e-3, s1 / grid * 1e-3, s6 / grid * 1e-3, m6 * 1e-3, s7 / grid * 1e-3);
+      for (int b = 0; b < grid; b += grid / 6)
+        fprintf(stderr, "  cta %d: start %+.2f ctl %.2f tiles %.2f %.2f %.2f done %.2f out %.2f\n", b,
+                (tr[b][0] - t0) * 1e-3, (tr[b][1] - tr[b][0]) * 1e-3, (tr[b][2] - tr[b][1]) * 1e-3,
+                tr[b][3] ? (tr[b][3] - tr[b][2]) * 1e-3 : 0.0, tr[b][4] ? (tr[b][4] - tr[b][3]) * 1e-3 : 0.0,
+                (tr[b][6] - t0) * 1e-3, (tr[b][7] - t0) * 1e-3);
+      memset(tr, 0, sizeof(tr));
+      MLG_CUDA(cudaMemcpyToSymbol(g_trace, tr, sizeof(tr)));
+    }
+#endif
+    ctl_d.download(ctl.data(), ctl.size(), st);
+    c.sync();
+    for (int s = 0; s < nsys; ++s)
+      if (ctl[static_cast<std::size_t>(s)].status == kIndefinite)
+        throw SolverError("cg_solve: matrix is not positive definite (p'Mp <= 0)");
+  }
+  while (!use_persist) {
+    for (int it = 0; it < chunk && !tiles.empty(); ++it) {
+      const unsigned nt = static_cast<unsigned>(tiles.size());
+      // Kernel timing evidence: every 4th launch of the local solves is
+      // bracketed by pooled CUDA events (cheap enough not to starve the stream).
+      const bool prof = profiling && (iter_count++ % 4 == 0);
+      cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+      if (prof) {
+        ev0 = c.event(2 * evs.size());
+        ev1 = c.event(2 * evs.size() + 1);
+        MLG_CUDA(cudaEventRecord(ev0, st));
+      }
+      const Finish& Fl = prof ? Fp : F;
+      if (uni && use_async && lap)
+        k_cg_iter<true, true, true><<<nt, kBlock, kRingBytes, st>>>(
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+      else if (uni && use_async)
+        k_cg_iter<true, true, false><<<nt, kBlock, kRingBytes, st>>>(
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+      else if (uni && lap)
+        k_cg_iter<true, false, true><<<nt, kBlock, 0, st>>>(
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else if (uni)
-        k_cg_iter<true, false><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc,
-                                                      bstride, X.get(), rc, rn, pc, pn, F);
+        k_cg_iter<true, false, false><<<nt, kBlock, 0, st>>>(
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else
-        k_cg_iter<false, false><<<nt, kBlock, 0, st>>>(sys_d.get(), tiles_d.get(), A, bsrc,
-                                                       bstride, X.get(), rc, rn, pc, pn, F);
+        k_cg_iter<false, false, false><<<nt, kBlock, 0, st>>>(
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       MLG_LAUNCH_CHECK();
       if (prof) {
         MLG_CUDA(cudaEventRecord(ev1, st));
@@ -1098,6 +1491,13 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     MLG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
     c.times.ka_ms_sum += ms;
     c.times.ka_launches += 1;
+  }
+  if (profiling) {
+    unsigned long long rows[2] = {0, 0};
+    prof_rows.download(rows, 2, c.stream);
+    c.sync();
+    c.times.ka_rows += static_cast<double>(rows[0]);
+    c.times.ka_check_rows += static_cast<double>(rows[1]);
   }
   c.times.ka_uniform = uni ? 1 : 0;
   CgResult res;

@@ -53,7 +53,9 @@ enum : int { kRunning = 0, kConverged = 1, kNotConverged = 2, kIndefinite = 3 };
 #endif
 constexpr int kCgWarps = MLG_CG_WARPS;  // warps (tasks) per CTA
 constexpr int kCgCols = 28;     // output columns per warp task (2 halo lanes each side)
-constexpr int kCgRows = 64;     // max window rows per warp task
+constexpr int kCgRows = 64;     // max window rows per warp task (register pipeline)
+constexpr int kCgRowsAsync = 64;  // ... (shared-memory pipeline: prologue amortised)
+constexpr int kCgPadRows = 6;  // padding rows after the pooled vectors (prefetch overrun)
 constexpr int kCgDots = 5;      // partial sums per tile
 
 struct CgResult {
@@ -82,6 +84,7 @@ class CgBatch {
   const double* bsrc = nullptr;
   int bstride = 1;
   bool use_async = false;  // HBM-streaming batches: shared-memory row pipeline
+  bool use_persist = false;  // L2-resident batches: one cooperative launch per solve
   std::vector<CgSys> sys_h;
   long long total_rows = 0;
   int total_tiles = 0;
@@ -90,6 +93,9 @@ class CgBatch {
   DevBuf<int> task_map;
   DevBuf<CgCtl> ctl_d;
   DevBuf<unsigned> counters;  // per-system tile arrival counters (last-tile reduction)
+  DevBuf<unsigned long long> prof_rows;
+  DevBuf<unsigned> gsync;  // grid barrier (count, generation) of the persistent kernel
+  DevBuf<int> active_d;    // systems still running  // rows swept by the sampled (profiled) launches
   DevBuf<double> X, R0, R1, P0, P1, part;
 };
 

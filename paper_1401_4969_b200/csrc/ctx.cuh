@@ -94,7 +94,8 @@ struct StepTimes {
   int local_iters_max = 0, strip_iters_max = 0;
   double ka_ms_sum = 0;  // summed device time of the local-solve SpMV kernel
   int ka_launches = 0;
-  double ka_rows = 0;    // summed active rows over those launches
+  double ka_rows = 0;    // rows swept in CG-update mode by those launches (device count)
+  double ka_check_rows = 0;  // ... in true-residual mode
   long long kernel_launches = 0;
   int ka_uniform = 0;  // the CG ran the constant-coefficient (no stencil stream) variant
   long long launch_base = 0;  // launch_counter() at the start of the step

@@ -52,9 +52,9 @@ def test_reference_arm_rank_gating(monkeypatch, capsys):
     assert capsys.readouterr().out == ""
 
 
-def test_ka_bytes_model():
+def test_cg_bytes_model():
     import bench
-    assert bench.ka_bytes_per_row(1) == 72
-    assert bench.ka_bytes_per_row(4) == 168
-    assert bench.ka_bytes_per_row(3) == 168
-    assert bench.ka_bytes_per_row(4, True) == 128
+    # update sweep: x, r, p read + written; check sweep: x, b read, r written
+    assert bench.cg_bytes_per_row(True) == (48, 24)
+    # non-uniform levels stream the {C,E,N,NE} stencil and D^-1 as well
+    assert bench.cg_bytes_per_row(False) == (88, 64)

@@ -30,10 +30,9 @@ for name in sys.argv[1:] or ["c2"]:
         bw = ""
         if t.spmv_launches:
             ms = t.spmv_kernel_ms / t.spmv_launches
-            rows = t.spmv_rows / t.spmv_launches
-            nr = 1 if c["nev"] == 1 else (2 if c["nev"] == 2 else (4 if c["nev"] <= 4 else 8))
-            by = rows * (40 + 32 * nr)
-            bw = f" ka {ms:.3f}ms {by / ms / 1e6:.0f}GB/s"
+            b_up, b_chk = (48, 24) if t.spmv_uniform_stencil else (88, 64)
+            by = (t.spmv_rows * b_up + t.spmv_check_rows * b_chk) / t.spmv_launches
+            bw = f" cg {ms:.3f}ms {by / ms / 1e6:.0f}GB/s"
         print(f"  L{k + 1}: n={n} local {t.local_seconds:.4f} iface {t.iface_seconds:.4f} "
               f"aug {t.aug_seconds:.4f} build {t.build_seconds:.4f} it {t.local_iterations_max}"
               f"/{t.strip_iterations_max} DOF/s {n / tot if tot else 0:.3e}{bw}")
