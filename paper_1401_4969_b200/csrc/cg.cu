@@ -45,6 +45,11 @@ namespace {
 constexpr int kBlock = CgBatch::kBlock;
 constexpr unsigned kFull = 0xffffffffu;
 
+#ifdef MLG_CG_TRACE
+__device__ unsigned long long g_trace[4096][8];  // per-CTA timestamps of one iteration
+__device__ unsigned g_kind[4096];                // per-CTA tile kinds (persistent kernel)
+#endif
+
 // Iterate loads.  The persistent kernel (CG) re-reads rows that other CTAs
 // rewrote in an earlier iteration of the same launch, so it must bypass the
 // (non-coherent) L1: ld.global.cg.
@@ -275,83 +280,6 @@ __device__ __forceinline__ Flags make_flags(const CgSys& S, const SweepArgs& A, 
   return f;
 }
 
-template <bool CG>
-__device__ __forceinline__ void fused_sweep_uni(const CgSys& S, const SweepArgs& A, const Task& k,
-                                                double al, double be, bool rst,
-                                                double* __restrict__ X,
-                                                const double* __restrict__ Rc,
-                                                double* __restrict__ Rn,
-                                                const double* __restrict__ Pc,
-                                                double* __restrict__ Pn,
-                                                double (&acc)[kCgDots]) {
-  const int lane = threadIdx.x & 31;
-  const Flags f = make_flags(S, A, k);
-  const bool out_col = lane >= 2 && lane < 2 + kCgCols && f.cin;
-  const int w = S.w;
-  const long long base = S.voff + k.col;
-  double* __restrict__ Xs = X + base;
-  const double* __restrict__ Rs = Rc + base;
-  double* __restrict__ Rns = Rn + base;
-  const double* __restrict__ Ps = Pc + base;
-  double* __restrict__ Pns = Pn + base;
-  const Stencil u = A.ust;
-  const double dv = A.udinv;
-  auto ld = [&](const double* __restrict__ p, int ly, int in) -> double {
-    return in ? ldv<CG>(p + ly * w) : 0.0;
-  };
-  // old p at rows n-1, n, n+1 (flags ia, ib, ic); r and x at rows n, n+1
-  int ia = f.row_in(k.ly0 - 2, A.sg), ib = f.row_in(k.ly0 - 1, A.sg), ic = f.row_in(k.ly0, A.sg);
-  double pa = ld(Ps, k.ly0 - 2, ia), pb = ld(Ps, k.ly0 - 1, ib), pc = ld(Ps, k.ly0, ic);
-  double rb = ld(Rs, k.ly0 - 1, ib), xb = ld(Xs, k.ly0 - 1, ib);
-  double rc = ld(Rs, k.ly0, ic), xc = ld(Xs, k.ly0, ic);
-  double sp = 0.0, mp = 0.0, mz = 0.0;
-  int sin_ = 0, min_ = 0;
-  for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
-    const int id = n + 2 <= k.ly1 + 1 ? f.row_in(n + 2, A.sg) : 0;
-    const double pd = ld(Ps, n + 2, id);
-    const double rd = ld(Rs, n + 2, id);
-    const double xd = ld(Xs, n + 2, id);
-    double rn = rb, xn = xb;
-    if (!rst) {
-      const double qo = product_flags(pa, ia, pb, ib, pc, ic, u);
-      rn = fma(-al, qo, rb);
-      xn = fma(al, pb, xb);
-    }
-    const double tz = xmul(dv, rn);
-    const double tp = rst ? tz : fma(be, pb, tz);
-    if (out_col && ib && n >= k.ly0 && n < k.ly1) {
-      Xs[n * w] = xn;
-      Rns[n * w] = rn;
-      Pns[n * w] = tp;
-      acc[0] += rn * rn;
-      acc[1] += rn * tz;
-    }
-    if (n - 1 >= k.ly0) {
-      const double q = product_flags(sp, sin_, mp, min_, tp, ib, u);
-      if (out_col && min_) {
-        acc[2] += mp * q;
-        acc[3] += q * mz;
-        acc[4] += q * xmul(dv, q);
-      }
-    }
-    sp = mp;
-    sin_ = min_;
-    mp = tp;
-    min_ = ib;
-    mz = tz;
-    pa = pb;
-    ia = ib;
-    pb = pc;
-    ib = ic;
-    pc = pd;
-    ic = id;
-    rb = rc;
-    xb = xc;
-    rc = rd;
-    xc = xd;
-  }
-}
-
 // True residual r = b - A x of a constant-coefficient system (x current).
 template <bool CG>
 __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs& A,
@@ -384,119 +312,6 @@ __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs&
     ia = ib;
     xb = xc;
     ib = ic;
-  }
-}
-
-// Register-prefetch sweep (rows n+2 .. n+4 in flight in registers): the path
-// for L2-resident batches (short latency, few rows needed in flight).
-//   EDGE = false: the task's stencil rectangle lies inside its system; no
-//     tests at all.  Every lane accumulates its dot-product terms and the
-//     halo lanes' sums are dropped at the end, so the only per-row predicate
-//     guards the three stores (predicated, not branched).
-//   EDGE = true: window-edge / strip-boundary task.  Points outside the system
-//     read as zero and get new p = 0, which reproduces the flagged product
-//     bit for bit (an absent neighbour contributes a literal 0 to the same
-//     paired-FMA chain); row loads are clamped into the window.
-// The first (stage 1 only) and last (stage 2 only) steps are peeled, so the
-// steady-state loop carries no row tests either.
-template <bool RST, bool EDGE, bool CG>
-__device__ __forceinline__ void sweep_regs(const CgSys& S, const SweepArgs& A, const Task& k,
-                                           double al, double be, double* __restrict__ X,
-                                           const double* __restrict__ Rc,
-                                           double* __restrict__ Rn,
-                                           const double* __restrict__ Pc,
-                                           double* __restrict__ Pn, double (&acc)[kCgDots]) {
-  const int lane = threadIdx.x & 31;
-  const Flags f = make_flags(S, A, k);  // EDGE only
-  const bool own = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
-  const int w = S.w;
-  const int col = EDGE ? min(max(k.col, 0), w - 1) : k.col;  // address-safe column
-  const long long base = S.voff + col;
-  double* __restrict__ Xs = X + base;
-  const double* __restrict__ Rs = Rc + base;
-  double* __restrict__ Rns = Rn + base;
-  const double* __restrict__ Ps = Pc + base;
-  double* __restrict__ Pns = Pn + base;
-  const Stencil u = A.ust;
-  const double dv = A.udinv;
-  const int rlo = EDGE ? 0 : k.ly0 - 2;                   // first row that exists
-  const int rhi = EDGE ? min(k.ly1 + 1, S.h - 1) : k.ly1 + 1;  // last row needed & existing
-  struct V {
-    double p, r, x;
-    bool in;
-  };
-  auto load = [&](int row) {
-    V v;
-    const long long o = static_cast<long long>(min(max(row, rlo), rhi)) * w;
-    v.p = ldv<CG>(Ps + o);
-    v.r = ldv<CG>(Rs + o);
-    v.x = ldv<CG>(Xs + o);
-    v.in = true;
-    if constexpr (EDGE) {
-      v.in = f.row_in(row, A.sg) != 0;
-      if (!v.in) v.p = v.r = v.x = 0.0;
-    }
-    return v;
-  };
-  V a = load(k.ly0 - 2), b = load(k.ly0 - 1), c = load(k.ly0);
-  V d1 = load(k.ly0 + 1), d2 = load(k.ly0 + 2);
-  double sp = 0.0, mp = 0.0, mz = 0.0;
-  bool m_in = false;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
-  auto step = [&](int n, auto store, auto stage2) {
-    const V nx = load(n + 4);  // window: a..d2 = rows n-1 .. n+3
-    double rn = b.r, xn = b.x;
-    if constexpr (!RST) {
-      const double qo = product_full(a.p, b.p, c.p, u);
-      rn = fma(-al, qo, b.r);
-      xn = fma(al, b.p, b.x);
-    }
-    const double tz = xmul(dv, rn);
-    double tp = RST ? tz : fma(be, b.p, tz);
-    if constexpr (EDGE)
-      if (!b.in) tp = 0.0;
-    if constexpr (decltype(store)::value) {
-      if (own && b.in) {
-        const long long o = static_cast<long long>(n) * w;
-        Xs[o] = xn;
-        Rns[o] = rn;
-        Pns[o] = tp;
-      }
-      if (!EDGE || (own && b.in)) {
-        a0 += rn * rn;
-        a1 += rn * tz;
-      }
-    }
-    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
-      const double q = product_full(sp, mp, tp, u);
-      if (!EDGE || (own && m_in)) {
-        a2 += mp * q;
-        a3 += q * mz;
-        a4 += q * xmul(dv, q);
-      }
-    }
-    sp = mp;
-    mp = tp;
-    mz = tz;
-    m_in = b.in;
-    a = b;
-    b = c;
-    c = d1;
-    d1 = d2;
-    d2 = nx;
-  };
-  using T = std::true_type;
-  using F = std::false_type;
-  step(k.ly0 - 1, F{}, F{});
-  step(k.ly0, T{}, F{});
-  for (int n = k.ly0 + 1; n < k.ly1; ++n) step(n, T{}, T{});
-  step(k.ly1, F{}, T{});
-  if (EDGE || own) {  // halo lanes' terms are dropped (EDGE: never accumulated)
-    acc[0] += a0;
-    acc[1] += a1;
-    acc[2] += a2;
-    acc[3] += a3;
-    acc[4] += a4;
   }
 }
 
@@ -589,6 +404,134 @@ __device__ __forceinline__ void sweep_int(const CgSys& S, const SweepArgs& A, co
 #pragma unroll
     for (int q = 0; q < kCgDots; ++q) acc[q] = 0.0;
   }
+}
+
+// In-system test of the window rows one task touches, without per-row
+// division: the G row intervals of the (at most three) lattice blocks the
+// task's rows fall in are precomputed; tasks spanning more blocks (tiny
+// levels) fall back to Flags::row_in.
+struct RowMask {
+  int h, cin, gx, slow;
+  int ya0, yb0, ya1, yb1, ya2, yb2;  // window-row intervals of G (closed; empty = (1, 0))
+  __device__ __forceinline__ bool in(int r, const Flags& f, const StripGeom& g) const {
+    if (!cin || r < 0 || r >= h) return false;
+    if (!gx) return true;
+    if (slow) return f.row_in(r, g) != 0;
+    return !((r >= ya0 && r <= yb0) || (r >= ya1 && r <= yb1) || (r >= ya2 && r <= yb2));
+  }
+};
+
+__device__ __forceinline__ RowMask make_rowmask(const CgSys& S, const SweepArgs& A, const Task& k,
+                                                const Flags& f) {
+  RowMask m;
+  m.h = S.h;
+  m.cin = f.cin;
+  m.gx = f.masked && f.gx;
+  m.slow = 0;
+  m.ya0 = m.ya1 = m.ya2 = 1;
+  m.yb0 = m.yb1 = m.yb2 = 0;
+  if (f.masked) {
+    const StripGeom& g = A.sg;
+    const int bhs = g.bh * g.scale;
+    const int r0 = max(k.ly0 - 2, 0), r1 = min(k.ly1 + 4, S.h - 1);
+    const int by0 = min((S.y0 + r0) / bhs, g.side - 1);
+    const int by1 = min((S.y0 + r1) / bhs, g.side - 1);
+    m.slow = by1 - by0 > 2;
+    auto lo = [&](int by) { return (by == 0 ? 0 : by * g.bh + g.dc) * g.scale - S.y0; };
+    auto hi = [&](int by) { return (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale - S.y0; };
+    m.ya0 = lo(by0);
+    m.yb0 = hi(by0);
+    if (by0 + 1 <= by1) {
+      m.ya1 = lo(by0 + 1);
+      m.yb1 = hi(by0 + 1);
+    }
+    if (by0 + 2 <= by1) {
+      m.ya2 = lo(by0 + 2);
+      m.yb2 = hi(by0 + 2);
+    }
+  }
+  return m;
+}
+
+// Register sweep of a window-edge / strip-boundary task.  Points outside the
+// system read as zero and get new p = 0, which reproduces the flagged product
+// bit for bit (an absent neighbour contributes a literal 0 to the same
+// paired-FMA chain); row loads are clamped into the window.
+template <bool RST, bool CG, bool LAP>
+__device__ __forceinline__ void sweep_edge(const CgSys& S, const SweepArgs& A, const Task& k,
+                                           double al, double be, double* __restrict__ X,
+                                           const double* __restrict__ Rc,
+                                           double* __restrict__ Rn,
+                                           const double* __restrict__ Pc,
+                                           double* __restrict__ Pn, double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  const Flags f = make_flags(S, A, k);
+  const RowMask rm = make_rowmask(S, A, k, f);
+  const bool own = lane >= 2 && lane < 2 + kCgCols && f.cin;
+  const long long w = S.w;
+  const long long base = S.voff + min(max(k.col, 0), S.w - 1);  // address-safe column
+  const Stencil u = A.ust;
+  const double dv = LAP ? 0.25 : A.udinv;
+  const int rhi = min(k.ly1 + 1, S.h - 1);  // last row needed & existing
+  struct V {
+    double p, r, x;
+    bool in;
+  };
+  auto load = [&](int row) {
+    const long long o = base + static_cast<long long>(min(max(row, 0), rhi)) * w;
+    V v{ldv<CG>(Pc + o), ldv<CG>(Rc + o), ldv<CG>(X + o), rm.in(row, f, A.sg)};
+    if (!v.in) v.p = v.r = v.x = 0.0;
+    return v;
+  };
+  V a = load(k.ly0 - 2), b = load(k.ly0 - 1), c = load(k.ly0);
+  V d1 = load(k.ly0 + 1), d2 = load(k.ly0 + 2);
+  double sp = 0.0, mp = 0.0, mz = 0.0;
+  bool m_in = false;
+  auto step = [&](int n, auto store, auto stage2) {
+    const V nx = load(n + 4);  // window: a..d2 = rows n-1 .. n+3
+    double rn = b.r, xn = b.x;
+    if constexpr (!RST) {
+      const double qo = product_int<LAP>(a.p, b.p, c.p, u);
+      rn = fma(-al, qo, b.r);
+      xn = fma(al, b.p, b.x);
+    }
+    const double tz = xmul(dv, rn);
+    double tp = RST ? tz : fma(be, b.p, tz);
+    if (!b.in) tp = 0.0;
+    if constexpr (decltype(store)::value) {
+      if (own && b.in) {
+        const long long o = base + static_cast<long long>(n) * w;
+        X[o] = xn;
+        Rn[o] = rn;
+        Pn[o] = tp;
+        acc[0] += rn * rn;
+        acc[1] += rn * tz;
+      }
+    }
+    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
+      const double q = product_int<LAP>(sp, mp, tp, u);
+      if (own && m_in) {
+        acc[2] += mp * q;
+        acc[3] += q * mz;
+        acc[4] += q * xmul(dv, q);
+      }
+    }
+    sp = mp;
+    mp = tp;
+    mz = tz;
+    m_in = b.in;
+    a = b;
+    b = c;
+    c = d1;
+    d1 = d2;
+    d2 = nx;
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  step(k.ly0 - 1, F{}, F{});
+  step(k.ly0, T{}, F{});
+  for (int n = k.ly0 + 1; n < k.ly1; ++n) step(n, T{}, T{});
+  step(k.ly1, F{}, T{});
 }
 
 // ---- asynchronous row pipeline for interior tasks ---------------------------
@@ -910,6 +853,10 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
     edge = ASYNC && k.valid && mode == kModeNormal && !fast;
     flagged = k.valid && mode == kModeNormal && !fast && !edge;
   }
+#ifdef MLG_CG_TRACE
+  if (PERSIST && (threadIdx.x & 31) == 0 && blockIdx.x < 4096)
+    atomicOr(&g_kind[blockIdx.x], fast ? 1u : edge ? 2u : flagged ? 4u : 8u);
+#endif
   if (fast) {
     if constexpr (ASYNC) {
       RowRing& ring = s_ring[threadIdx.x >> 5];
@@ -931,9 +878,9 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
       sweep_async<false, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
   } else if (flagged) {
     if (rst)
-      sweep_regs<true, true, PERSIST>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+      sweep_edge<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
     else
-      sweep_regs<false, true, PERSIST>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+      sweep_edge<false, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
   } else if (!UNI && k.valid && mode == kModeNormal) {
     ORow a, b, c, d;  // old iterate at rows n-1, n, n+1 (and n+2 in flight)
     NRow s, m;        // new p at rows n-2, n-1
@@ -1066,7 +1013,6 @@ __device__ __forceinline__ void grid_sync(const GridSync& G) {
 }
 
 #ifdef MLG_CG_TRACE
-__device__ unsigned long long g_trace[4096][8];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1416,6 +1362,22 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       }
       fprintf(stderr, "trace: grid %d tiles %d span %.2f us | ctl %.2f work %.2f (last done %.2f) barrier %.2f us avg\n",
               grid, ntiles, (t7 - t0) * 1e-3, s1 / grid * 1e-3, s6 / grid * 1e-3, m6 * 1e-3, s7 / grid * 1e-3);
+      static unsigned kind[4096];
+      MLG_CUDA(cudaMemcpyFromSymbol(kind, g_kind, sizeof(kind)));
+      for (unsigned kk = 0; kk < 16; ++kk) {
+        int n = 0;
+        double sum = 0, mx = 0;
+        for (int b = 0; b < grid; ++b)
+          if (kind[b] == kk) {
+            ++n;
+            const double d = (tr[b][6] - tr[b][1]) * 1e-3;
+            sum += d;
+            mx = std::max(mx, d);
+          }
+        if (n) fprintf(stderr, "  kind %u: %d CTAs, tile work avg %.2f max %.2f us\n", kk, n, sum / n, mx);
+      }
+      memset(kind, 0, sizeof(kind));
+      MLG_CUDA(cudaMemcpyToSymbol(g_kind, kind, sizeof(kind)));
       for (int b = 0; b < grid; b += grid / 6)
         fprintf(stderr, "  cta %d: start %+.2f ctl %.2f tiles %.2f %.2f %.2f done %.2f out %.2f\n", b,
                 (tr[b][0] - t0) * 1e-3, (tr[b][1] - tr[b][0]) * 1e-3, (tr[b][2] - tr[b][1]) * 1e-3,
