@@ -1168,9 +1168,9 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   const int max_rows = use_async ? max_rows_async : kCgRows;
   int krows = static_cast<int>(std::min<long long>(
       max_rows, std::max<long long>(min_rows, all_rows / (kCgCols * target_tasks))));
-  // Wave quantisation: every tile costs ~(krows + 3) row steps and the grid
+  // Wave quantisation: every tile costs ~(krows + c0) row steps and the grid
   // runs in waves of `resident` tiles, so pick the row count that minimises
-  // waves x (krows + 3) among the candidates at or below the first choice.
+  // waves x (krows + c0) from half the first choice up to the cap.
   {
     const int resident = use_persist ? resident_persist() : resident_tiles(use_async);
     auto tiles_for = [&](int kr) {
@@ -1182,11 +1182,16 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
       }
       return t;
     };
+    // (c0: a task's prologue/epilogue in row steps)
+    static const int c0 = [] {
+      const char* e = std::getenv("MLG_CG_C0");  // tuning hook
+      return e ? std::atoi(e) : 6;
+    }();
     double best = 1e300;
     int best_k = krows;
-    for (int kr = std::max(8, krows / 2); kr <= krows; ++kr) {
+    for (int kr = std::max(4, krows / 2); kr <= max_rows; ++kr) {
       const long long waves = (tiles_for(kr) + resident - 1) / resident;
-      const double cost = static_cast<double>(waves) * (kr + 3);
+      const double cost = static_cast<double>(waves) * (kr + c0);
       if (cost < best - 1e-9) {
         best = cost;
         best_k = kr;
