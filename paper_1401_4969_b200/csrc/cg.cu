@@ -34,6 +34,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <queue>
 #include <type_traits>
 
 #include "cg.cuh"
@@ -140,7 +141,7 @@ __device__ __forceinline__ void load_old(const CgSys& S, const SweepArgs& A, int
     o.st = A.st[g];
     o.dv = A.dinv[g];
   }
-  const long long v = S.voff + static_cast<long long>(ly) * S.w + col;
+  const long long v = cg_index(S, ly, col);
   o.p = Pc[v];
   o.r = Rc[v];
   o.x = X[v];
@@ -294,7 +295,7 @@ __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs&
   const double* __restrict__ Xs = X + base;
   double* __restrict__ Rns = Rn + base;
   auto ld = [&](int ly, int in) -> double {
-    return in ? ldv<CG>(Xs + static_cast<long long>(ly) * S.w) : 0.0;
+    return in ? ldv<CG>(Xs + static_cast<long long>(ly) * S.pitch) : 0.0;
   };
   int ia = f.row_in(k.ly0 - 1, A.sg), ib = f.row_in(k.ly0, A.sg);
   double xa = ld(k.ly0 - 1, ia), xb = ld(k.ly0, ib);
@@ -305,7 +306,7 @@ __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs&
     if (out_col && ib) {
       const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
       const double rt = bsrc[g * bstride + S.rhs] - ax;
-      Rns[static_cast<long long>(ly) * S.w] = rt;
+      Rns[static_cast<long long>(ly) * S.pitch] = rt;
       acc[0] += rt * rt;
     }
     xa = xb;
@@ -315,9 +316,7 @@ __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs&
   }
 }
 
-// Interior register sweep with running row pointers (no per-row index math:
-// the pooled vectors carry kCgPadRows rows of padding, so prefetches past a
-// window read padding or the next system and are never used).  LAP: the
+// Row product inside the CG sweeps.  LAP: the
 // level's interior stencil is the 5-point Laplacian {4, -1, -1, 0} with
 // D^-1 = 1/4 (P1 on the right-triangle lattice): constants are immediates and
 // the zero SW/NE pair is skipped -- fma(0, s, y) == y for finite s, so the
@@ -335,77 +334,6 @@ __device__ __forceinline__ double product_int(double sv, double cv, double nv, c
   }
 }
 
-template <bool RST, bool CG, bool LAP>
-__device__ __forceinline__ void sweep_int(const CgSys& S, const SweepArgs& A, const Task& k,
-                                          double al, double be, double* __restrict__ X,
-                                          const double* __restrict__ Rc,
-                                          double* __restrict__ Rn,
-                                          const double* __restrict__ Pc,
-                                          double* __restrict__ Pn, double (&acc)[kCgDots]) {
-  const int lane = threadIdx.x & 31;
-  const bool own = lane >= 2 && lane < 2 + kCgCols;
-  const long long w = S.w;
-  long long lo = S.voff + k.col + (k.ly0 - 2) * w;  // next row to load (starts at ly0-2)
-  long long so = lo + 2 * w;                         // next row to store (starts at ly0)
-  const Stencil u = A.ust;
-  const double dv = LAP ? 0.25 : A.udinv;
-  struct V {
-    double p, r, x;
-  };
-  auto load = [&]() {
-    V v{ldv<CG>(Pc + lo), ldv<CG>(Rc + lo), ldv<CG>(X + lo)};
-    lo += w;
-    return v;
-  };
-  V a = load(), b = load(), c = load(), d1 = load(), d2 = load();  // rows ly0-2 .. ly0+2
-  double sp = 0.0, mp = 0.0, mz = 0.0;
-  auto step = [&](auto store, auto stage2) {
-    const V nx = load();  // row n+4
-    double rn = b.r, xn = b.x;
-    if constexpr (!RST) {
-      const double qo = product_int<LAP>(a.p, b.p, c.p, u);
-      rn = fma(-al, qo, b.r);
-      xn = fma(al, b.p, b.x);
-    }
-    const double tz = xmul(dv, rn);
-    const double tp = RST ? tz : fma(be, b.p, tz);
-    if constexpr (decltype(store)::value) {
-      if (own) {
-        X[so] = xn;
-        Rn[so] = rn;
-        Pn[so] = tp;
-      }
-      so += w;
-      acc[0] += rn * rn;
-      acc[1] += rn * tz;
-    }
-    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
-      const double q = product_int<LAP>(sp, mp, tp, u);
-      acc[2] += mp * q;
-      acc[3] += q * mz;
-      acc[4] += q * xmul(dv, q);
-    }
-    sp = mp;
-    mp = tp;
-    mz = tz;
-    a = b;
-    b = c;
-    c = d1;
-    d1 = d2;
-    d2 = nx;
-  };
-  using T = std::true_type;
-  using F = std::false_type;
-  step(F{}, F{});  // row ly0-1: stage 1 only
-  step(T{}, F{});  // row ly0
-  for (int n = k.ly0 + 1; n < k.ly1; ++n) step(T{}, T{});
-  step(F{}, T{});  // row ly1: stage 2 for ly1-1
-  if (!own) {      // the halo lanes' terms are dropped (acc is fresh per tile)
-#pragma unroll
-    for (int q = 0; q < kCgDots; ++q) acc[q] = 0.0;
-  }
-}
-
 // In-system test of the window rows one task touches, without per-row
 // division: the G row intervals of the (at most three) lattice blocks the
 // task's rows fall in are precomputed; tasks spanning more blocks (tiny
@@ -413,11 +341,12 @@ __device__ __forceinline__ void sweep_int(const CgSys& S, const SweepArgs& A, co
 struct RowMask {
   int h, cin, gx, slow;
   int ya0, yb0, ya1, yb1, ya2, yb2;  // window-row intervals of G (closed; empty = (1, 0))
+  template <bool SLOW>
   __device__ __forceinline__ bool in(int r, const Flags& f, const StripGeom& g) const {
-    if (!cin || r < 0 || r >= h) return false;
-    if (!gx) return true;
-    if (slow) return f.row_in(r, g) != 0;
-    return !((r >= ya0 && r <= yb0) || (r >= ya1 && r <= yb1) || (r >= ya2 && r <= yb2));
+    if (SLOW) return f.row_in(r, g) != 0;  // tasks spanning > 3 blocks (tiny levels only)
+    const bool rowok = static_cast<unsigned>(r) < static_cast<unsigned>(h);
+    const bool ing = (r >= ya0 & r <= yb0) | (r >= ya1 & r <= yb1) | (r >= ya2 & r <= yb2);
+    return cin & rowok & !(gx & ing);
   }
 };
 
@@ -453,10 +382,123 @@ __device__ __forceinline__ RowMask make_rowmask(const CgSys& S, const SweepArgs&
   return m;
 }
 
-// Register sweep of a window-edge / strip-boundary task.  Points outside the
-// system read as zero and get new p = 0, which reproduces the flagged product
-// bit for bit (an absent neighbour contributes a literal 0 to the same
-// paired-FMA chain); row loads are clamped into the window.
+// Register sweep, modulo-scheduled by hand.  The 5-row window of old p, r, x
+// (rows n-1 .. n+3) lives in slot (row - ly0 + 2) mod 5 of register arrays;
+// the step for row n (J = slot of row n-1) consumes slots J, J+1, J+2 and
+// refills slot J with row n+4.  Nothing is ever copied, so no instruction
+// waits on a row before it is consumed (three steps after it was requested);
+// a rotating window compiled as register moves stalls on every new load.
+//   EDGE = false: the task's stencil rectangle lies inside its system, no tests.
+//   EDGE = true: window-edge / strip-boundary task.  The zero frame of the
+//     pooled vectors makes reads outside the window zeros and points of G hold
+//     zeros, so loads need no tests; r, z, p and q of points outside the
+//     system are forced to zero -- an absent neighbour then contributes a
+//     literal 0 to the same paired-FMA chain (bitwise the flagged product) and
+//     every dot term of such a point is an exact zero.
+// Every lane accumulates; the halo lanes' sums are dropped at the end, so the
+// only per-row predicate guards the three stores.
+template <bool RST, bool CG, bool LAP, bool EDGE, bool SLOW>
+__device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, const Task& k,
+                                          double al, double be, double* __restrict__ X,
+                                          const double* __restrict__ Rc,
+                                          double* __restrict__ Rn,
+                                          const double* __restrict__ Pc,
+                                          double* __restrict__ Pn, double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  const Flags f = make_flags(S, A, k);          // EDGE only
+  const RowMask rm = make_rowmask(S, A, k, f);  // EDGE only
+  const bool own = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
+  const long long w = S.pitch;
+  long long lo = cg_index(S, k.ly0 - 2, k.col);  // next row to request
+  long long so = lo + 2 * w;                      // next row to store (ly0)
+  const Stencil u = A.ust;
+  const double dv = LAP ? 0.25 : A.udinv;
+  double P[5], Rr[5], Xr[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {  // rows ly0-2 .. ly0+2
+    P[j] = ldv<CG>(Pc + lo);
+    Rr[j] = ldv<CG>(Rc + lo);
+    Xr[j] = ldv<CG>(X + lo);
+    lo += w;
+  }
+  double sp = 0.0, mp = 0.0, mz = 0.0;  // new p at rows n-2, n-1; z at n-1
+  bool m_in = false;
+  auto step = [&](auto J, auto store, auto stage2, int n) {
+    constexpr int j0 = decltype(J)::value, j1 = (j0 + 1) % 5, j2 = (j0 + 2) % 5;
+    bool b_in = true;
+    if constexpr (EDGE) b_in = rm.template in<SLOW>(n, f, A.sg);
+    double rn = Rr[j1], xn = Xr[j1];
+    if constexpr (!RST) {
+      const double qo = product_int<LAP>(P[j0], P[j1], P[j2], u);
+      rn = fma(-al, qo, Rr[j1]);
+      xn = fma(al, P[j1], Xr[j1]);
+    }
+    if constexpr (EDGE) rn = b_in ? rn : 0.0;
+    const double tz = xmul(dv, rn);
+    double tp = RST ? tz : fma(be, P[j1], tz);
+    if constexpr (EDGE) tp = b_in ? tp : 0.0;
+    P[j0] = ldv<CG>(Pc + lo);  // slot of row n-1 is free: request row n+4
+    Rr[j0] = ldv<CG>(Rc + lo);
+    Xr[j0] = ldv<CG>(X + lo);
+    lo += w;
+    if constexpr (decltype(store)::value) {
+      if (own && b_in) {
+        X[so] = xn;
+        Rn[so] = rn;
+        Pn[so] = tp;
+      }
+      so += w;
+      acc[0] += rn * rn;
+      acc[1] += rn * tz;
+    }
+    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
+      double q = product_int<LAP>(sp, mp, tp, u);
+      if constexpr (EDGE) q = m_in ? q : 0.0;
+      acc[2] += mp * q;
+      acc[3] += q * mz;
+      acc[4] += q * xmul(dv, q);
+    }
+    sp = mp;
+    mp = tp;
+    mz = tz;
+    m_in = b_in;
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  using J0 = std::integral_constant<int, 0>;
+  using J1 = std::integral_constant<int, 1>;
+  using J2 = std::integral_constant<int, 2>;
+  using J3 = std::integral_constant<int, 3>;
+  using J4 = std::integral_constant<int, 4>;
+  step(J0{}, F{}, F{}, k.ly0 - 1);  // stage 1 only
+  step(J1{}, T{}, F{}, k.ly0);
+  int n = k.ly0 + 1;  // slot phase 2
+#pragma unroll 1
+  for (; n + 4 < k.ly1; n += 5) {
+    step(J2{}, T{}, T{}, n);
+    step(J3{}, T{}, T{}, n + 1);
+    step(J4{}, T{}, T{}, n + 2);
+    step(J0{}, T{}, T{}, n + 3);
+    step(J1{}, T{}, T{}, n + 4);
+  }
+  const int rem = k.ly1 - n;  // 0..4 rows left, then row ly1 (stage 2 only)
+  if (rem > 0) step(J2{}, T{}, T{}, n);
+  if (rem > 1) step(J3{}, T{}, T{}, n + 1);
+  if (rem > 2) step(J4{}, T{}, T{}, n + 2);
+  if (rem > 3) step(J0{}, T{}, T{}, n + 3);
+  switch (rem) {
+    case 0: step(J2{}, F{}, T{}, k.ly1); break;
+    case 1: step(J3{}, F{}, T{}, k.ly1); break;
+    case 2: step(J4{}, F{}, T{}, k.ly1); break;
+    case 3: step(J0{}, F{}, T{}, k.ly1); break;
+    default: step(J1{}, F{}, T{}, k.ly1); break;
+  }
+  if (!own) {  // halo lanes (and columns outside the window) contribute nothing
+#pragma unroll
+    for (int q = 0; q < kCgDots; ++q) acc[q] = 0.0;
+  }
+}
+
 template <bool RST, bool CG, bool LAP>
 __device__ __forceinline__ void sweep_edge(const CgSys& S, const SweepArgs& A, const Task& k,
                                            double al, double be, double* __restrict__ X,
@@ -464,74 +506,14 @@ __device__ __forceinline__ void sweep_edge(const CgSys& S, const SweepArgs& A, c
                                            double* __restrict__ Rn,
                                            const double* __restrict__ Pc,
                                            double* __restrict__ Pn, double (&acc)[kCgDots]) {
-  const int lane = threadIdx.x & 31;
-  const Flags f = make_flags(S, A, k);
-  const RowMask rm = make_rowmask(S, A, k, f);
-  const bool own = lane >= 2 && lane < 2 + kCgCols && f.cin;
-  const long long w = S.w;
-  const long long base = S.voff + min(max(k.col, 0), S.w - 1);  // address-safe column
-  const Stencil u = A.ust;
-  const double dv = LAP ? 0.25 : A.udinv;
-  const int rhi = min(k.ly1 + 1, S.h - 1);  // last row needed & existing
-  struct V {
-    double p, r, x;
-    bool in;
-  };
-  auto load = [&](int row) {
-    const long long o = base + static_cast<long long>(min(max(row, 0), rhi)) * w;
-    V v{ldv<CG>(Pc + o), ldv<CG>(Rc + o), ldv<CG>(X + o), rm.in(row, f, A.sg)};
-    if (!v.in) v.p = v.r = v.x = 0.0;
-    return v;
-  };
-  V a = load(k.ly0 - 2), b = load(k.ly0 - 1), c = load(k.ly0);
-  V d1 = load(k.ly0 + 1), d2 = load(k.ly0 + 2);
-  double sp = 0.0, mp = 0.0, mz = 0.0;
-  bool m_in = false;
-  auto step = [&](int n, auto store, auto stage2) {
-    const V nx = load(n + 4);  // window: a..d2 = rows n-1 .. n+3
-    double rn = b.r, xn = b.x;
-    if constexpr (!RST) {
-      const double qo = product_int<LAP>(a.p, b.p, c.p, u);
-      rn = fma(-al, qo, b.r);
-      xn = fma(al, b.p, b.x);
-    }
-    const double tz = xmul(dv, rn);
-    double tp = RST ? tz : fma(be, b.p, tz);
-    if (!b.in) tp = 0.0;
-    if constexpr (decltype(store)::value) {
-      if (own && b.in) {
-        const long long o = base + static_cast<long long>(n) * w;
-        X[o] = xn;
-        Rn[o] = rn;
-        Pn[o] = tp;
-        acc[0] += rn * rn;
-        acc[1] += rn * tz;
-      }
-    }
-    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
-      const double q = product_int<LAP>(sp, mp, tp, u);
-      if (own && m_in) {
-        acc[2] += mp * q;
-        acc[3] += q * mz;
-        acc[4] += q * xmul(dv, q);
-      }
-    }
-    sp = mp;
-    mp = tp;
-    mz = tz;
-    m_in = b.in;
-    a = b;
-    b = c;
-    c = d1;
-    d1 = d2;
-    d2 = nx;
-  };
-  using T = std::true_type;
-  using F = std::false_type;
-  step(k.ly0 - 1, F{}, F{});
-  step(k.ly0, T{}, F{});
-  for (int n = k.ly0 + 1; n < k.ly1; ++n) step(n, T{}, T{});
-  step(k.ly1, F{}, T{});
+  // warp-uniform: only tiny levels have tasks spanning more than three blocks
+  const int bhs = A.sg.bh * A.sg.scale;
+  const bool slow = A.mask && (S.y0 + min(k.ly1 + 4, S.h - 1)) / bhs -
+                                      (S.y0 + max(k.ly0 - 2, 0)) / bhs > 2;
+  if (slow)
+    sweep_reg<RST, CG, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+  else
+    sweep_reg<RST, CG, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
 }
 
 // ---- asynchronous row pipeline for interior tasks ---------------------------
@@ -585,7 +567,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
   const int lane = threadIdx.x & 31;
   const Flags f = make_flags(S, A, k);  // EDGE only
   const bool out = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
-  const int w = S.w;
+  const int w = S.pitch;
   const long long base = S.voff + k.col;
   double* __restrict__ Xs = X + base;
   const double* __restrict__ Rs = Rc + base;
@@ -815,7 +797,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
   if (out_lane(S, k)) {
     for (int ly = k.ly0; ly < k.ly1; ++ly) {
       const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
-      const long long v = S.voff + static_cast<long long>(ly) * S.w + k.col;
+      const long long v = cg_index(S, ly, k.col);
       X[v] = 0.0;
       if (A.mask && !in_strip(A.sg, S.x0 + k.col, S.y0 + ly)) {
         R[v] = 0.0;
@@ -850,6 +832,9 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
   bool fast = false, edge = false, flagged = false;
   if constexpr (UNI) {
     fast = k.valid && mode == kModeNormal && task_interior(S, A, k);
+#ifdef MLG_CG_FORCE_EDGE
+    fast = false;
+#endif
     edge = ASYNC && k.valid && mode == kModeNormal && !fast;
     flagged = k.valid && mode == kModeNormal && !fast && !edge;
   }
@@ -866,9 +851,9 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
         sweep_async<false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
     } else {
       if (rst)
-        sweep_int<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+        sweep_reg<true, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
       else
-        sweep_int<false, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+        sweep_reg<false, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
     }
   } else if (ASYNC && edge) {
     RowRing& ring = s_ring[threadIdx.x >> 5];
@@ -908,7 +893,7 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
       t.st = b.st;
       t.in = b.in;
       if (out && b.in && n >= k.ly0 && n < k.ly1) {
-        const long long v = S.voff + static_cast<long long>(n) * S.w + k.col;
+        const long long v = cg_index(S, n, k.col);
         X[v] = xn;
         Rn[v] = rn;
         Pn[v] = t.p;
@@ -941,7 +926,7 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
       const double ax = product<UNI>(a.x, a.st, a.in, b.x, b.st, b.in, c.x, c.in, A);
       if (out && b.in) {
         const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
-        const long long v = S.voff + static_cast<long long>(ly) * S.w + k.col;
+        const long long v = cg_index(S, ly, k.col);
         const double rt = xsub(bsrc[g * bstride + S.rhs], ax);
         Rn[v] = rt;
         acc[0] += rt * rt;
@@ -1024,8 +1009,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TRACE(slot)
 #endif
 
+#ifndef MLG_CG_PERSIST_MINBLOCKS
+#define MLG_CG_PERSIST_MINBLOCKS 4  // 128 registers: the modulo-scheduled sweep without spills
+#endif
+// tiles: ntiles = per-CTA count x gridDim.x entries, entry i * gridDim.x + b is
+// the i-th tile of CTA b (host-balanced); sys < 0 marks an empty slot.
 template <bool UNI, bool LAP>
-__global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS * 4 / kCgWarps)
+__global__ void __launch_bounds__(kBlock, MLG_CG_PERSIST_MINBLOCKS * 4 / kCgWarps)
     k_cg_persist(const CgSys* sys, const CgTile* tiles, int ntiles, SweepArgs A,
                  const double* bsrc, int bstride, double* __restrict__ X, double* R0,
                  double* R1, double* P0, double* P1, Finish F, GridSync G) {
@@ -1038,13 +1028,13 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS * 4 / kCgWarps)
   if (threadIdx.x < mine) {
     const CgTile t = tiles[blockIdx.x + threadIdx.x * gridDim.x];
     s_tl[threadIdx.x] = t;
-    s_sys[threadIdx.x] = sys[t.sys];
+    if (t.sys >= 0) s_sys[threadIdx.x] = sys[t.sys];
   }
   unsigned long long rows_acc = 0;
   for (int it = 0; it < G.max_iters; ++it) {
     const bool odd = it & 1;
     TRACE(0);
-    if (threadIdx.x < mine) {  // scalars written by other CTAs: read through L2
+    if (threadIdx.x < mine && s_tl[threadIdx.x].sys >= 0) {  // written by other CTAs: via L2
       const CgCtl* c = F.ctl + s_tl[threadIdx.x].sys;
       s_mode[threadIdx.x] = __ldcg(&c->mode);
       s_rst[threadIdx.x] = __ldcg(&c->restart);
@@ -1054,6 +1044,7 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_MINBLOCKS * 4 / kCgWarps)
     __syncthreads();
     TRACE(1);
     for (int i = 0; i < mine; ++i) {
+      if (s_tl[i].sys < 0) continue;  // empty slot (CTA-uniform)
       cg_tile<UNI, false, true, LAP>(s_sys[i], s_tl[i], s_mode[i], s_al[i], s_be[i], s_rst[i] != 0, A,
                                 bsrc, bstride, X, odd ? R1 : R0, odd ? R0 : R1, odd ? P1 : P0,
                                 odd ? P0 : P1, F, nullptr, rows_acc);
@@ -1235,26 +1226,32 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
       q.ntasks = static_cast<int>(tmap.size());
     }
   }
+  // Pooled layout: window rows at pitch w + 1 (the extra column is zero and
+  // doubles as the left neighbour of the next row), a zero row above and
+  // below each window, two spare rows in front and kCgPadRows behind the last
+  // window (prefetch overrun).  Everything outside the windows stays zero.
+  int max_pitch = 1;
+  for (const CgSys& s : systems) max_pitch = std::max(max_pitch, s.w + 1);
+  long long cursor = 2LL * max_pitch + 2;
   for (CgSys& s : systems) {
+    s.pitch = s.w + 1;
     s.ntiles = std::max(1, (s.ntasks + kCgWarps - 1) / kCgWarps);
-    s.voff = total_rows;
+    s.voff = cursor + s.pitch;  // row 0 (row -1 is the zero row)
     s.toff = total_tiles;
     s.maxit = 10 * std::max(s.nrows, 1);
-    total_rows += s.nrows;
+    cursor += static_cast<long long>(s.h + 2) * s.pitch;
     total_tiles += s.ntiles;
   }
+  total_rows = cursor + static_cast<long long>(kCgPadRows) * max_pitch + 64;
+  tmap_h = tmap;
   task_map.ensure(std::max<std::size_t>(tmap.size(), 1));
   if (!tmap.empty()) task_map.upload(tmap.data(), tmap.size(), c.stream);
   sys_h = std::move(systems);
-  // padding: interior sweeps prefetch up to 4 rows past their window
-  int max_w = 1;
-  for (const CgSys& q : sys_h) max_w = std::max(max_w, q.w);
-  const std::size_t nv = static_cast<std::size_t>(total_rows) + kCgPadRows * max_w + 64;
-  X.ensure(nv);
-  R0.ensure(nv);
-  R1.ensure(nv);
-  P0.ensure(nv);
-  P1.ensure(nv);
+  const std::size_t nv = static_cast<std::size_t>(total_rows);
+  for (DevBuf<double>* v : {&X, &R0, &R1, &P0, &P1}) {
+    v->ensure(nv);
+    MLG_CUDA(cudaMemsetAsync(v->get(), 0, nv * sizeof(double), c.stream));  // zero frames
+  }
   part.ensure(static_cast<std::size_t>(total_tiles) * kCgDots);
   sys_d.ensure(sys_h.size());
   sys_d.upload(sys_h.data(), sys_h.size(), c.stream);
@@ -1262,7 +1259,76 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   ctl_d.zero(c.stream);
   counters.ensure(sys_h.size());
   counters.zero(c.stream);
-  tiles_d.ensure(total_tiles);
+  // persistent layouts hold up to kPersistTiles slots per resident CTA
+  tiles_d.ensure(use_persist ? std::max<std::size_t>(total_tiles, static_cast<std::size_t>(kPersistTiles) * resident_persist())
+                             : static_cast<std::size_t>(total_tiles));
+}
+
+namespace {
+bool host_rect_in_strip(const StripGeom& g, int xa, int xb, int ya, int yb) {
+  const int bxa = std::min(xa / (g.bw * g.scale), g.side - 1);
+  const int bxb = std::min(xb / (g.bw * g.scale), g.side - 1);
+  const int bya = std::min(ya / (g.bh * g.scale), g.side - 1);
+  const int byb = std::min(yb / (g.bh * g.scale), g.side - 1);
+  for (int bx = bxa; bx <= bxb; ++bx)
+    for (int by = bya; by <= byb; ++by) {
+      const int x0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+      const int x1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+      const int y0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+      const int y1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+      if (xa <= x1 && xb >= x0 && ya <= y1 && yb >= y0) return false;
+    }
+  return true;
+}
+}  // namespace
+
+// Estimated cost of a tile: its slowest warp task, (rows + 6) row steps, x1.6
+// for tasks on the window edge or touching G (the flagged sweep).
+double CgBatch::tile_cost(const CgTile& t, const std::vector<int>& tmap) const {
+  const CgSys& S = sys_h[static_cast<std::size_t>(t.sys)];
+  double worst = 0.0;
+  for (int wi = 0; wi < kCgWarps; ++wi) {
+    int task = t.t * kCgWarps + wi;
+    if (task >= S.ntasks) break;
+    if (S.tmap_off >= 0) task = tmap[static_cast<std::size_t>(S.tmap_off + task)];
+    const int rb = task / S.nstrips, strip = task % S.nstrips;
+    const int c0 = strip * kCgCols - 2, ly0 = rb * S.krows, ly1 = std::min(ly0 + S.krows, S.h);
+    bool interior = c0 >= 0 && c0 + 31 < S.w && ly0 - 2 >= 0 && ly1 + 1 < S.h;
+    if (interior && mask)
+      interior = host_rect_in_strip(L->strip_geom, S.x0 + c0, S.x0 + c0 + 31, S.y0 + ly0 - 2,
+                                    S.y0 + ly1 + 1);
+    worst = std::max(worst, (ly1 - ly0 + 6) * (interior ? 1.0 : 1.6));
+  }
+  return worst;
+}
+
+std::vector<CgTile> CgBatch::balance_tiles(const std::vector<CgTile>& tiles, int grid) const {
+  std::vector<std::pair<double, int>> order;
+  order.reserve(tiles.size());
+  for (std::size_t i = 0; i < tiles.size(); ++i)
+    order.emplace_back(tile_cost(tiles[i], tmap_h), static_cast<int>(i));
+  std::stable_sort(order.begin(), order.end(),
+                   [](const auto& a, const auto& b) { return a.first > b.first; });
+  // min-heap of (load, cta); CTAs at kPersistTiles are retired from the heap
+  using Slot = std::pair<double, int>;
+  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+  for (int b = 0; b < grid; ++b) heap.emplace(0.0, b);
+  std::vector<std::vector<int>> per(static_cast<std::size_t>(grid));
+  for (const auto& o : order) {
+    Slot sl = heap.top();
+    heap.pop();
+    per[static_cast<std::size_t>(sl.second)].push_back(o.second);
+    if (static_cast<int>(per[static_cast<std::size_t>(sl.second)].size()) < kPersistTiles)
+      heap.emplace(sl.first + o.first, sl.second);
+  }
+  std::size_t m = 0;
+  for (const auto& p : per) m = std::max(m, p.size());
+  std::vector<CgTile> lay(m * static_cast<std::size_t>(grid), CgTile{-1, 0});
+  for (int b = 0; b < grid; ++b)
+    for (std::size_t i = 0; i < per[static_cast<std::size_t>(b)].size(); ++i)
+      lay[i * static_cast<std::size_t>(grid) + static_cast<std::size_t>(b)] =
+          tiles[static_cast<std::size_t>(per[static_cast<std::size_t>(b)][i])];
+  return lay;
 }
 
 CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
@@ -1317,8 +1383,30 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     // All iterations in cooperative launches of at most kIters iterations (an
     // even count, so the vector parity is unchanged between launches).
     constexpr int kIters = 4096;
-    const int ntiles = static_cast<int>(tiles.size());
-    const int grid = std::min(ntiles, resident_persist());
+    const int grid = std::min(static_cast<int>(tiles.size()), resident_persist());
+    // Longest-processing-time assignment of tiles to the resident CTAs (a
+    // window-edge / strip-boundary tile costs ~1.6 interior tiles): the
+    // iteration ends with the slowest CTA, so balance the per-CTA sums.
+    const std::vector<CgTile> lay = balance_tiles(tiles, grid);
+#ifdef MLG_CG_TRACE
+    for (int b : {0, 1, 2, 3, grid / 2, grid - 1}) {
+      const CgTile& t = lay[static_cast<std::size_t>(b)];
+      if (t.sys < 0) continue;
+      const CgSys& S = sys_h[static_cast<std::size_t>(t.sys)];
+      fprintf(stderr, "  layout cta %d: sys %d tile %d (w %d h %d krows %d nstrips %d nrb %d) cost %.1f tasks:", b,
+              t.sys, t.t, S.w, S.h, S.krows, S.nstrips, S.nrb, tile_cost(t, tmap_h));
+      for (int wi = 0; wi < kCgWarps; ++wi) {
+        int task = t.t * kCgWarps + wi;
+        if (task >= S.ntasks) break;
+        if (S.tmap_off >= 0) task = tmap_h[static_cast<std::size_t>(S.tmap_off + task)];
+        fprintf(stderr, " (strip %d rb %d)", task % S.nstrips, task / S.nstrips);
+      }
+      fprintf(stderr, "\n");
+    }
+#endif
+    tiles_d.ensure(lay.size());
+    tiles_d.upload(lay.data(), lay.size(), st);
+    const int ntiles = static_cast<int>(lay.size());
     const CgSys* sp = sys_d.get();
     const CgTile* tp = tiles_d.get();
     double* xp = X.get();

@@ -25,6 +25,7 @@ namespace mlg {
 // one system and owns one partial-sum slot.
 struct CgSys {
   int x0, y0, w, h;
+  int pitch;       // row pitch in the pooled vectors (w + 1: one shared zero column)
   int rhs;         // lane of the rhs-interleaved source (b) vector
   long long voff;  // first row in the pooled vectors
   int toff;        // first tile id (partials index)
@@ -34,6 +35,14 @@ struct CgSys {
   int nstrips, nrb, ntasks, krows;
   int tmap_off;  // >= 0: tasks are task_map[tmap_off + i] (strip tasks with strip rows)
 };
+
+// Pooled-vector index of window point (lx, ly).  Every window is stored with a
+// zero frame -- one zero column shared between consecutive rows (pitch w + 1)
+// and a zero row above and below -- so stencil reads that leave the window
+// read zeros.
+__host__ __device__ __forceinline__ long long cg_index(const CgSys& s, int ly, int lx) {
+  return s.voff + static_cast<long long>(ly) * s.pitch + lx;
+}
 
 struct CgTile {
   int sys;
@@ -79,6 +88,8 @@ class CgBatch {
   const CgSys* sys_dev() const { return sys_d.get(); }
 
  private:
+  double tile_cost(const CgTile& t, const std::vector<int>& tmap) const;
+  std::vector<CgTile> balance_tiles(const std::vector<CgTile>& tiles, int grid) const;
   const Level* L = nullptr;
   const unsigned char* mask = nullptr;
   const double* bsrc = nullptr;
@@ -86,6 +97,7 @@ class CgBatch {
   bool use_async = false;  // HBM-streaming batches: shared-memory row pipeline
   bool use_persist = false;  // L2-resident batches: one cooperative launch per solve
   std::vector<CgSys> sys_h;
+  std::vector<int> tmap_h;  // host copy of task_map
   long long total_rows = 0;
   int total_tiles = 0;
   DevBuf<CgSys> sys_d;

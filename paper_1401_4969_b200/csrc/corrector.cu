@@ -246,8 +246,7 @@ __global__ void k_glue_cg(int nx, int ny, PartDev P, int nev, const CgSys* sys, 
       for (int r = 0; r < NR; ++r) {
         if (r >= nev) break;
         const CgSys S = sys[j * nev + r];
-        const long long i = static_cast<long long>(iy - S.y0) * S.w + (ix - S.x0);
-        y[r] = xadd(uu[r], X[S.voff + i]);
+        y[r] = xadd(uu[r], X[cg_index(S, iy - S.y0, ix - S.x0)]);
       }
     }
   }
@@ -275,13 +274,14 @@ __global__ void k_strip_scatter(int nx, int nev, const CgSys* sys, const unsigne
   const CgSys S0 = sys[0];
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= S0.nrows) return;
-  const long long d = static_cast<long long>(S0.y0 + i / S0.w) * (nx + 1) + (S0.x0 + i % S0.w);
+  const int ly = static_cast<int>(i / S0.w), lx = static_cast<int>(i % S0.w);
+  const long long d = static_cast<long long>(S0.y0 + ly) * (nx + 1) + (S0.x0 + lx);
   if (!mask[d]) return;
   double x[NR];
   ldv<NR>(glued + d * NR, x);
 #pragma unroll
   for (int r = 0; r < NR; ++r)
-    if (r < nev) x[r] = X[sys[r].voff + i];
+    if (r < nev) x[r] = X[cg_index(sys[r], ly, lx)];
   stv<NR>(glued + d * NR, x);
 }
 
