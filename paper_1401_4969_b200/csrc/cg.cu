@@ -556,7 +556,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // instead of copied) and their new p is forced to zero, which reproduces the
 // flagged product exactly (an absent neighbour contributes a literal 0 to the
 // same paired-FMA chain).
-template <bool RST, bool EDGE>
+template <bool RST, bool LAP, bool EDGE, bool SLOW>
 __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, const Task& k,
                                             double al, double be, double* __restrict__ X,
                                             const double* __restrict__ Rc,
@@ -565,31 +565,21 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
                                             double* __restrict__ Pn, double (&acc)[kCgDots],
                                             RowRing& ring) {
   const int lane = threadIdx.x & 31;
-  const Flags f = make_flags(S, A, k);  // EDGE only
-  const bool out = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
-  const int w = S.pitch;
-  const long long base = S.voff + k.col;
-  double* __restrict__ Xs = X + base;
-  const double* __restrict__ Rs = Rc + base;
-  double* __restrict__ Rns = Rn + base;
-  const double* __restrict__ Ps = Pc + base;
-  double* __restrict__ Pns = Pn + base;
+  const Flags f = make_flags(S, A, k);          // EDGE only
+  const RowMask rm = make_rowmask(S, A, k, f);  // EDGE only
+  const bool own = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
+  const long long w = S.pitch;
+  const long long base = cg_index(S, 0, k.col);
   const Stencil u = A.ust;
-  const double dv = A.udinv;
-  const int last = k.ly1 + 1;  // last old row needed
+  const double dv = LAP ? 0.25 : A.udinv;
+  const int last = k.ly1 + 1;  // last old row needed (the zero frame makes it readable)
   auto issue = [&](int row) {  // one commit group per row, empty past the end
     if (row <= last) {
       const int s = row & (kD - 1);
-      if (!EDGE || f.row_in(row, A.sg)) {
-        const long long o = static_cast<long long>(row) * w;
-        cp_async8(&ring.v[s][0][lane], Ps + o);
-        cp_async8(&ring.v[s][1][lane], Rs + o);
-        cp_async8(&ring.v[s][2][lane], Xs + o);
-      } else {
-        ring.v[s][0][lane] = 0.0;
-        ring.v[s][1][lane] = 0.0;
-        ring.v[s][2][lane] = 0.0;
-      }
+      const long long o = base + row * w;
+      cp_async8(&ring.v[s][0][lane], Pc + o);
+      cp_async8(&ring.v[s][1][lane], Rc + o);
+      cp_async8(&ring.v[s][2][lane], X + o);
     }
     cp_async_commit();
   };
@@ -600,35 +590,39 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
   double pb = ring.v[(k.ly0 - 1) & (kD - 1)][0][lane];
   issue(k.ly0 - 2 + kD);  // slot of row ly0-2 consumed
   double sp = 0.0, mp = 0.0, mz = 0.0;
-  bool min_ = false;  // row n-1 in the system
-  for (int n = k.ly0 - 1; n <= k.ly1; ++n) {
+  bool m_in = false;  // row n-1 in the system
+  auto step = [&](int n, auto store, auto stage2) {
     // issued up to row n+kD-1; row n+1 must have landed
     cp_async_wait<kD - 2>();
     const int sc = n & (kD - 1);
     const double pc = ring.v[(n + 1) & (kD - 1)][0][lane];
     const double rb = ring.v[sc][1][lane];
     const double xb = ring.v[sc][2][lane];
+    bool b_in = true;
+    if constexpr (EDGE) b_in = rm.template in<SLOW>(n, f, A.sg);
     double rn = rb, xn = xb;
-    if (!RST) {
-      const double qo = product_full(pa, pb, pc, u);
+    if constexpr (!RST) {
+      const double qo = product_int<LAP>(pa, pb, pc, u);
       rn = fma(-al, qo, rb);
       xn = fma(al, pb, xb);
     }
+    if constexpr (EDGE) rn = b_in ? rn : 0.0;
     const double tz = xmul(dv, rn);
     double tp = RST ? tz : fma(be, pb, tz);
-    const bool nin = !EDGE || f.row_in(n, A.sg);
-    if (!nin) tp = 0.0;
-    if (out && nin && n >= k.ly0 && n < k.ly1) {
-      const long long o = static_cast<long long>(n) * w;
-      Xs[o] = xn;
-      Rns[o] = rn;
-      Pns[o] = tp;
+    if constexpr (EDGE) tp = b_in ? tp : 0.0;
+    if constexpr (decltype(store)::value) {
+      if (own && b_in) {
+        const long long o = base + n * w;
+        X[o] = xn;
+        Rn[o] = rn;
+        Pn[o] = tp;
+      }
       acc[0] += rn * rn;
       acc[1] += rn * tz;
     }
-    // stage 2 at row n-1 (computed unconditionally: no branch around shuffles)
-    const double q = product_full(sp, mp, tp, u);
-    if (out && min_ && n - 1 >= k.ly0) {
+    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
+      double q = product_int<LAP>(sp, mp, tp, u);
+      if constexpr (EDGE) q = m_in ? q : 0.0;
       acc[2] += mp * q;
       acc[3] += q * mz;
       acc[4] += q * xmul(dv, q);
@@ -636,12 +630,22 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     sp = mp;
     mp = tp;
     mz = tz;
-    min_ = nin;
+    m_in = b_in;
     pa = pb;
     pb = pc;
     issue(n + kD);  // refill slot n (its p, r, x are consumed)
-  }
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  step(k.ly0 - 1, F{}, F{});
+  step(k.ly0, T{}, F{});
+  for (int n = k.ly0 + 1; n < k.ly1; ++n) step(n, T{}, T{});
+  step(k.ly1, F{}, T{});
   cp_async_wait<0>();
+  if (!own) {  // halo lanes (and columns outside the window) contribute nothing
+#pragma unroll
+    for (int q = 0; q < kCgDots; ++q) acc[q] = 0.0;
+  }
 }
 
 
@@ -846,9 +850,9 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
     if constexpr (ASYNC) {
       RowRing& ring = s_ring[threadIdx.x >> 5];
       if (rst)
-        sweep_async<true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<true, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
       else
-        sweep_async<false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<false, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
     } else {
       if (rst)
         sweep_reg<true, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
@@ -857,10 +861,20 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
     }
   } else if (ASYNC && edge) {
     RowRing& ring = s_ring[threadIdx.x >> 5];
-    if (rst)
-      sweep_async<true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
-    else
-      sweep_async<false, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+    const int bhs = A.sg.bh * A.sg.scale;  // see sweep_edge
+    const bool slow = A.mask && (S.y0 + min(k.ly1 + 4, S.h - 1)) / bhs -
+                                        (S.y0 + max(k.ly0 - 2, 0)) / bhs > 2;
+    if (slow) {
+      if (rst)
+        sweep_async<true, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+      else
+        sweep_async<false, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+    } else {
+      if (rst)
+        sweep_async<true, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+      else
+        sweep_async<false, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+    }
   } else if (flagged) {
     if (rst)
       sweep_edge<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
