@@ -341,10 +341,12 @@ __device__ __forceinline__ double product_int(double sv, double cv, double nv, c
 struct RowMask {
   int h, cin, gx, slow;
   int ya0, yb0, ya1, yb1, ya2, yb2;  // window-row intervals of G (closed; empty = (1, 0))
-  template <bool SLOW>
+  // SLOW: tasks spanning > 3 blocks (tiny levels only); MASKED: strip systems
+  template <bool SLOW, bool MASKED = true>
   __device__ __forceinline__ bool in(int r, const Flags& f, const StripGeom& g) const {
-    if (SLOW) return f.row_in(r, g) != 0;  // tasks spanning > 3 blocks (tiny levels only)
+    if (SLOW) return f.row_in(r, g) != 0;
     const bool rowok = static_cast<unsigned>(r) < static_cast<unsigned>(h);
+    if (!MASKED) return cin & rowok;
     const bool ing = (r >= ya0 & r <= yb0) | (r >= ya1 & r <= yb1) | (r >= ya2 & r <= yb2);
     return cin & rowok & !(gx & ing);
   }
@@ -397,7 +399,7 @@ __device__ __forceinline__ RowMask make_rowmask(const CgSys& S, const SweepArgs&
 //     every dot term of such a point is an exact zero.
 // Every lane accumulates; the halo lanes' sums are dropped at the end, so the
 // only per-row predicate guards the three stores.
-template <bool RST, bool CG, bool LAP, bool EDGE, bool SLOW>
+template <bool RST, bool CG, bool LAP, bool EDGE, bool SLOW, bool MASKED = true>
 __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, const Task& k,
                                           double al, double be, double* __restrict__ X,
                                           const double* __restrict__ Rc,
@@ -426,7 +428,7 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
   auto step = [&](auto J, auto store, auto stage2, int n) {
     constexpr int j0 = decltype(J)::value, j1 = (j0 + 1) % 5, j2 = (j0 + 2) % 5;
     bool b_in = true;
-    if constexpr (EDGE) b_in = rm.template in<SLOW>(n, f, A.sg);
+    if constexpr (EDGE) b_in = rm.template in<SLOW, MASKED>(n, f, A.sg);
     double rn = Rr[j1], xn = Xr[j1];
     if constexpr (!RST) {
       const double qo = product_int<LAP>(P[j0], P[j1], P[j2], u);
@@ -512,8 +514,10 @@ __device__ __forceinline__ void sweep_edge(const CgSys& S, const SweepArgs& A, c
                                       (S.y0 + max(k.ly0 - 2, 0)) / bhs > 2;
   if (slow)
     sweep_reg<RST, CG, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
-  else
-    sweep_reg<RST, CG, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+  else if (A.mask)
+    sweep_reg<RST, CG, LAP, true, false, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+  else  // local systems: only the window edges (no G)
+    sweep_reg<RST, CG, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
 }
 
 // ---- asynchronous row pipeline for interior tasks ---------------------------
@@ -556,7 +560,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // instead of copied) and their new p is forced to zero, which reproduces the
 // flagged product exactly (an absent neighbour contributes a literal 0 to the
 // same paired-FMA chain).
-template <bool RST, bool LAP, bool EDGE, bool SLOW>
+template <bool RST, bool LAP, bool EDGE, bool SLOW, bool MASKED = true>
 __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, const Task& k,
                                             double al, double be, double* __restrict__ X,
                                             const double* __restrict__ Rc,
@@ -599,7 +603,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     const double rb = ring.v[sc][1][lane];
     const double xb = ring.v[sc][2][lane];
     bool b_in = true;
-    if constexpr (EDGE) b_in = rm.template in<SLOW>(n, f, A.sg);
+    if constexpr (EDGE) b_in = rm.template in<SLOW, MASKED>(n, f, A.sg);
     double rn = rb, xn = xb;
     if constexpr (!RST) {
       const double qo = product_int<LAP>(pa, pb, pc, u);
@@ -869,11 +873,16 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
         sweep_async<true, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
       else
         sweep_async<false, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
-    } else {
+    } else if (A.mask) {
       if (rst)
         sweep_async<true, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
       else
         sweep_async<false, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+    } else {
+      if (rst)
+        sweep_async<true, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+      else
+        sweep_async<false, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
     }
   } else if (flagged) {
     if (rst)
@@ -1203,6 +1212,18 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
       }
     }
     krows = best_k;
+    // Persistent batches: one tile per CTA leaves the slow (edge) tiles on the
+    // critical path; aim for ~`tpc` tiles per CTA so the LPT assignment can
+    // pair them with cheap ones.
+    static const int tpc = [] {
+      const char* e = std::getenv("MLG_CG_PTPC");  // tuning hook
+      return e ? std::atoi(e) : 1;
+    }();
+    if (use_persist && tpc > 1) {
+      int kr = krows;
+      while (kr > 4 && tiles_for(kr) < static_cast<long long>(tpc) * resident) --kr;
+      krows = kr;
+    }
     if (use_persist && (tiles_for(krows) + resident - 1) / resident > kPersistTiles)
       use_persist = false;  // too many tiles per CTA: multi-launch path
   }
