@@ -321,6 +321,55 @@ __device__ __forceinline__ void check_sweep_uni(const CgSys& S, const SweepArgs&
 // D^-1 = 1/4 (P1 on the right-triangle lattice): constants are immediates and
 // the zero SW/NE pair is skipped -- fma(0, s, y) == y for finite s, so the
 // row product is bitwise the generic paired-FMA product.
+// Lateral neighbours through a per-warp shared-memory exchange instead of
+// warp shuffles: one 64-bit store, __syncwarp, two 64-bit loads (4 instructions
+// per value instead of 4 SHFL + 3 LOP3), and no divergence check (BRA.DIV) in
+// front of each shuffle group -- ptxas attaches the waits for outstanding
+// global loads to it, which defeated the row prefetch.  Slot 0 serves the
+// stage-1 product, slot 1 the stage-2 product; a slot is rewritten only after
+// the other slot's __syncwarp, so every lane has read it.
+// (Measured: +4 % at config 2 in the register pipeline; -2 % at config 5 in
+// the cp.async pipeline, whose shared-memory traffic it competes with, so the
+// latter keeps the shuffles.)
+struct Xchg {
+  double v[2][32];
+};
+
+struct Lat {  // a lane's view of its warp's exchange buffer
+  double* self;
+  const double* west;
+  const double* east;
+  __device__ __forceinline__ Lat(Xchg& x, int slot) {
+    const int lane = threadIdx.x & 31;
+    self = &x.v[slot][lane];
+    west = &x.v[slot][(lane - 1) & 31];
+    east = &x.v[slot][(lane + 1) & 31];
+  }
+  __device__ __forceinline__ void get(double c, double& w, double& e) const {
+    *self = c;
+    __syncwarp();
+    w = *west;
+    e = *east;
+  }
+};
+
+template <bool LAP, bool SMX>
+__device__ __forceinline__ double product_lat(double sv, double cv, double nv, const Stencil& u,
+                                              const Lat& lat) {
+  if constexpr (LAP && SMX) {
+    double wv, ev;
+    lat.get(cv, wv, ev);
+    return fma(-1.0, wv + ev, fma(-1.0, sv + nv, 4.0 * cv));
+  } else {
+    const double wv = __shfl_up_sync(kFull, cv, 1);
+    const double ev = __shfl_down_sync(kFull, cv, 1);
+    if constexpr (LAP) return fma(-1.0, wv + ev, fma(-1.0, sv + nv, 4.0 * cv));
+    const double swv = __shfl_up_sync(kFull, sv, 1);
+    const double nev = __shfl_down_sync(kFull, nv, 1);
+    return fma(u.e, wv + ev, fma(u.n, sv + nv, fma(u.ne, swv + nev, u.c * cv)));
+  }
+}
+
 template <bool LAP>
 __device__ __forceinline__ double product_int(double sv, double cv, double nv, const Stencil& u) {
   const double wv = __shfl_up_sync(kFull, cv, 1);
@@ -405,7 +454,9 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
                                           const double* __restrict__ Rc,
                                           double* __restrict__ Rn,
                                           const double* __restrict__ Pc,
-                                          double* __restrict__ Pn, double (&acc)[kCgDots]) {
+                                          double* __restrict__ Pn, double (&acc)[kCgDots],
+                                          Xchg& xch) {
+  const Lat lat1(xch, 0), lat2(xch, 1);
   const int lane = threadIdx.x & 31;
   const Flags f = make_flags(S, A, k);          // EDGE only
   const RowMask rm = make_rowmask(S, A, k, f);  // EDGE only
@@ -431,7 +482,7 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
     if constexpr (EDGE) b_in = rm.template in<SLOW, MASKED>(n, f, A.sg);
     double rn = Rr[j1], xn = Xr[j1];
     if constexpr (!RST) {
-      const double qo = product_int<LAP>(P[j0], P[j1], P[j2], u);
+      const double qo = product_lat<LAP, true>(P[j0], P[j1], P[j2], u, lat1);
       rn = fma(-al, qo, Rr[j1]);
       xn = fma(al, P[j1], Xr[j1]);
     }
@@ -454,7 +505,7 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
       acc[1] += rn * tz;
     }
     if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
-      double q = product_int<LAP>(sp, mp, tp, u);
+      double q = product_lat<LAP, true>(sp, mp, tp, u, lat2);
       if constexpr (EDGE) q = m_in ? q : 0.0;
       acc[2] += mp * q;
       acc[3] += q * mz;
@@ -507,17 +558,18 @@ __device__ __forceinline__ void sweep_edge(const CgSys& S, const SweepArgs& A, c
                                            const double* __restrict__ Rc,
                                            double* __restrict__ Rn,
                                            const double* __restrict__ Pc,
-                                           double* __restrict__ Pn, double (&acc)[kCgDots]) {
+                                           double* __restrict__ Pn, double (&acc)[kCgDots],
+                                           Xchg& xch) {
   // warp-uniform: only tiny levels have tasks spanning more than three blocks
   const int bhs = A.sg.bh * A.sg.scale;
   const bool slow = A.mask && (S.y0 + min(k.ly1 + 4, S.h - 1)) / bhs -
                                       (S.y0 + max(k.ly0 - 2, 0)) / bhs > 2;
   if (slow)
-    sweep_reg<RST, CG, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+    sweep_reg<RST, CG, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
   else if (A.mask)
-    sweep_reg<RST, CG, LAP, true, false, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+    sweep_reg<RST, CG, LAP, true, false, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
   else  // local systems: only the window edges (no G)
-    sweep_reg<RST, CG, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+    sweep_reg<RST, CG, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
 }
 
 // ---- asynchronous row pipeline for interior tasks ---------------------------
@@ -567,7 +619,8 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
                                             double* __restrict__ Rn,
                                             const double* __restrict__ Pc,
                                             double* __restrict__ Pn, double (&acc)[kCgDots],
-                                            RowRing& ring) {
+                                            RowRing& ring, Xchg& xch) {
+  const Lat lat1(xch, 0), lat2(xch, 1);
   const int lane = threadIdx.x & 31;
   const Flags f = make_flags(S, A, k);          // EDGE only
   const RowMask rm = make_rowmask(S, A, k, f);  // EDGE only
@@ -606,7 +659,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     if constexpr (EDGE) b_in = rm.template in<SLOW, MASKED>(n, f, A.sg);
     double rn = rb, xn = xb;
     if constexpr (!RST) {
-      const double qo = product_int<LAP>(pa, pb, pc, u);
+      const double qo = product_lat<LAP, false>(pa, pb, pc, u, lat1);
       rn = fma(-al, qo, rb);
       xn = fma(al, pb, xb);
     }
@@ -625,7 +678,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
       acc[1] += rn * tz;
     }
     if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
-      double q = product_int<LAP>(sp, mp, tp, u);
+      double q = product_lat<LAP, false>(sp, mp, tp, u, lat2);
       if constexpr (EDGE) q = m_in ? q : 0.0;
       acc[2] += mp * q;
       acc[3] += q * mz;
@@ -834,6 +887,8 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
                                         const Finish& F, RowRing* s_ring,
                                         unsigned long long& rows_acc) {
   if (mode == kModeSkip) return;  // uniform across the system's tiles
+  __shared__ Xchg s_xch[kCgWarps];
+  Xchg& xch = s_xch[threadIdx.x >> 5];
   const Task k = task_of(S, tl.t, A.task_map);
   const bool out = out_lane(S, k);
   double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -854,14 +909,14 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
     if constexpr (ASYNC) {
       RowRing& ring = s_ring[threadIdx.x >> 5];
       if (rst)
-        sweep_async<true, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<true, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
       else
-        sweep_async<false, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<false, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
     } else {
       if (rst)
-        sweep_reg<true, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+        sweep_reg<true, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
       else
-        sweep_reg<false, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+        sweep_reg<false, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
     }
   } else if (ASYNC && edge) {
     RowRing& ring = s_ring[threadIdx.x >> 5];
@@ -870,25 +925,25 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
                                         (S.y0 + max(k.ly0 - 2, 0)) / bhs > 2;
     if (slow) {
       if (rst)
-        sweep_async<true, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<true, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
       else
-        sweep_async<false, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<false, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
     } else if (A.mask) {
       if (rst)
-        sweep_async<true, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<true, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
       else
-        sweep_async<false, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<false, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
     } else {
       if (rst)
-        sweep_async<true, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<true, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
       else
-        sweep_async<false, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring);
+        sweep_async<false, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
     }
   } else if (flagged) {
     if (rst)
-      sweep_edge<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+      sweep_edge<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
     else
-      sweep_edge<false, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+      sweep_edge<false, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
   } else if (!UNI && k.valid && mode == kModeNormal) {
     ORow a, b, c, d;  // old iterate at rows n-1, n, n+1 (and n+2 in flight)
     NRow s, m;        // new p at rows n-2, n-1
