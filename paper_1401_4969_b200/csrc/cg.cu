@@ -335,19 +335,24 @@ struct Xchg {
   double v[2][32];
 };
 
+// The warp barrier is a named CTA barrier with a count of 32 (`bar.sync
+// 1+warp, 32` -> BAR.SYNC): __syncwarp compiles to a divergence check
+// (BRA.DIV) at which ptxas waits for every outstanding global load.
 struct Lat {  // a lane's view of its warp's exchange buffer
   double* self;
   const double* west;
   const double* east;
+  int bar;
   __device__ __forceinline__ Lat(Xchg& x, int slot) {
     const int lane = threadIdx.x & 31;
     self = &x.v[slot][lane];
     west = &x.v[slot][(lane - 1) & 31];
     east = &x.v[slot][(lane + 1) & 31];
+    bar = 1 + (threadIdx.x >> 5);
   }
   __device__ __forceinline__ void get(double c, double& w, double& e) const {
     *self = c;
-    __syncwarp();
+    asm volatile("bar.sync %0, 32;" ::"r"(bar) : "memory");
     w = *west;
     e = *east;
   }
@@ -433,12 +438,13 @@ __device__ __forceinline__ RowMask make_rowmask(const CgSys& S, const SweepArgs&
   return m;
 }
 
-// Register sweep, modulo-scheduled by hand.  The 5-row window of old p, r, x
-// (rows n-1 .. n+3) lives in slot (row - ly0 + 2) mod 5 of register arrays;
-// the step for row n (J = slot of row n-1) consumes slots J, J+1, J+2 and
-// refills slot J with row n+4.  Nothing is ever copied, so no instruction
-// waits on a row before it is consumed (three steps after it was requested);
-// a rotating window compiled as register moves stalls on every new load.
+// Register sweep, modulo-scheduled by hand.  The kW-row window of old p, r, x
+// (rows n-1 .. n+kW-2) lives in slot (row - ly0 + 2) mod kW of register
+// arrays; the step for row n (J = slot of row n-1) consumes slots J, J+1, J+2
+// and refills slot J with row n+kW-1.  Nothing is ever copied, so no
+// instruction waits on a row before it is consumed (kW-2 steps after it was
+// requested); a rotating window compiled as register moves stalls on every
+// new load.
 //   EDGE = false: the task's stencil rectangle lies inside its system, no tests.
 //   EDGE = true: window-edge / strip-boundary task.  The zero frame of the
 //     pooled vectors makes reads outside the window zeros and points of G hold
@@ -448,6 +454,16 @@ __device__ __forceinline__ RowMask make_rowmask(const CgSys& S, const SweepArgs&
 //     every dot term of such a point is an exact zero.
 // Every lane accumulates; the halo lanes' sums are dropped at the end, so the
 // only per-row predicate guards the three stores.
+template <int... Is, typename Fn>
+__device__ __forceinline__ void static_for(std::integer_sequence<int, Is...>, Fn&& fn) {
+  (fn(std::integral_constant<int, Is>{}), ...);
+}
+
+#ifndef MLG_CG_W
+#define MLG_CG_W 5
+#endif
+constexpr int kW = MLG_CG_W;  // register window rows (prefetch distance kW - 2 steps)
+
 template <bool RST, bool CG, bool LAP, bool EDGE, bool SLOW, bool MASKED = true>
 __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, const Task& k,
                                           double al, double be, double* __restrict__ X,
@@ -466,9 +482,9 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
   long long so = lo + 2 * w;                      // next row to store (ly0)
   const Stencil u = A.ust;
   const double dv = LAP ? 0.25 : A.udinv;
-  double P[5], Rr[5], Xr[5];
+  double P[kW], Rr[kW], Xr[kW];
 #pragma unroll
-  for (int j = 0; j < 5; ++j) {  // rows ly0-2 .. ly0+2
+  for (int j = 0; j < kW; ++j) {  // rows ly0-2 .. ly0+kW-3
     P[j] = ldv<CG>(Pc + lo);
     Rr[j] = ldv<CG>(Rc + lo);
     Xr[j] = ldv<CG>(X + lo);
@@ -477,7 +493,7 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
   double sp = 0.0, mp = 0.0, mz = 0.0;  // new p at rows n-2, n-1; z at n-1
   bool m_in = false;
   auto step = [&](auto J, auto store, auto stage2, int n) {
-    constexpr int j0 = decltype(J)::value, j1 = (j0 + 1) % 5, j2 = (j0 + 2) % 5;
+    constexpr int j0 = decltype(J)::value % kW, j1 = (j0 + 1) % kW, j2 = (j0 + 2) % kW;
     bool b_in = true;
     if constexpr (EDGE) b_in = rm.template in<SLOW, MASKED>(n, f, A.sg);
     double rn = Rr[j1], xn = Xr[j1];
@@ -490,7 +506,7 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
     const double tz = xmul(dv, rn);
     double tp = RST ? tz : fma(be, P[j1], tz);
     if constexpr (EDGE) tp = b_in ? tp : 0.0;
-    P[j0] = ldv<CG>(Pc + lo);  // slot of row n-1 is free: request row n+4
+    P[j0] = ldv<CG>(Pc + lo);  // slot of row n-1 is free: request row n+kW-1
     Rr[j0] = ldv<CG>(Rc + lo);
     Xr[j0] = ldv<CG>(X + lo);
     lo += w;
@@ -518,34 +534,25 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
   };
   using T = std::true_type;
   using F = std::false_type;
-  using J0 = std::integral_constant<int, 0>;
-  using J1 = std::integral_constant<int, 1>;
-  using J2 = std::integral_constant<int, 2>;
-  using J3 = std::integral_constant<int, 3>;
-  using J4 = std::integral_constant<int, 4>;
-  step(J0{}, F{}, F{}, k.ly0 - 1);  // stage 1 only
-  step(J1{}, T{}, F{}, k.ly0);
+  step(std::integral_constant<int, 0>{}, F{}, F{}, k.ly0 - 1);  // stage 1 only
+  step(std::integral_constant<int, 1>{}, T{}, F{}, k.ly0);
   int n = k.ly0 + 1;  // slot phase 2
+  using Seq = std::make_integer_sequence<int, kW>;
 #pragma unroll 1
-  for (; n + 4 < k.ly1; n += 5) {
-    step(J2{}, T{}, T{}, n);
-    step(J3{}, T{}, T{}, n + 1);
-    step(J4{}, T{}, T{}, n + 2);
-    step(J0{}, T{}, T{}, n + 3);
-    step(J1{}, T{}, T{}, n + 4);
-  }
-  const int rem = k.ly1 - n;  // 0..4 rows left, then row ly1 (stage 2 only)
-  if (rem > 0) step(J2{}, T{}, T{}, n);
-  if (rem > 1) step(J3{}, T{}, T{}, n + 1);
-  if (rem > 2) step(J4{}, T{}, T{}, n + 2);
-  if (rem > 3) step(J0{}, T{}, T{}, n + 3);
-  switch (rem) {
-    case 0: step(J2{}, F{}, T{}, k.ly1); break;
-    case 1: step(J3{}, F{}, T{}, k.ly1); break;
-    case 2: step(J4{}, F{}, T{}, k.ly1); break;
-    case 3: step(J0{}, F{}, T{}, k.ly1); break;
-    default: step(J1{}, F{}, T{}, k.ly1); break;
-  }
+  for (; n + kW - 1 < k.ly1; n += kW)
+    static_for(Seq{}, [&](auto i) {
+      constexpr int ii = decltype(i)::value;
+      step(std::integral_constant<int, (2 + ii) % kW>{}, T{}, T{}, n + ii);
+    });
+  const int rem = k.ly1 - n;  // 0..kW-1 rows left, then row ly1 (stage 2 only)
+  static_for(std::make_integer_sequence<int, kW - 1>{}, [&](auto i) {
+    constexpr int ii = decltype(i)::value;
+    if (ii < rem) step(std::integral_constant<int, (2 + ii) % kW>{}, T{}, T{}, n + ii);
+  });
+  static_for(Seq{}, [&](auto r) {
+    constexpr int rr = decltype(r)::value;
+    if (rr == rem) step(std::integral_constant<int, (2 + rr) % kW>{}, F{}, T{}, k.ly1);
+  });
   if (!own) {  // halo lanes (and columns outside the window) contribute nothing
 #pragma unroll
     for (int q = 0; q < kCgDots; ++q) acc[q] = 0.0;
@@ -1051,26 +1058,25 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
 constexpr int kPersistTiles = 8;
 
 struct GridSync {
-  unsigned* count;  // arrivals at the current barrier
-  unsigned* gen;    // barrier generation
+  unsigned* count;  // arrivals since the launch began (zeroed before each launch)
+  unsigned* gen;    // unused (kept for the layout of the sync buffer)
   int* active;      // systems still running
   int max_iters;    // safety bound (every system stops by maxit)
 };
 
-__device__ __forceinline__ void grid_sync(const GridSync& G) {
+// Barrier number k (k = 1, 2, ... within the launch): arrive on a monotonic
+// counter and wait until it reaches k * gridDim.x -- one atomic round trip per
+// CTA, no reset/generation step on the critical path.
+__device__ __forceinline__ void grid_sync(const GridSync& G, unsigned k) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = G.gen;
-    const unsigned g = *gen;
     __threadfence();
-    if (atomicAdd(G.count, 1u) == gridDim.x - 1) {
-      atomicExch(G.count, 0u);
-      __threadfence();
-      atomicAdd(G.gen, 1u);
-    } else {
-      while (*gen == g) __nanosleep(32);
-    }
-    __threadfence();
+    atomicAdd(G.count, 1u);
+    const unsigned target = k * gridDim.x;
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(G.count) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }
@@ -1130,7 +1136,7 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_PERSIST_MINBLOCKS * 4 / kCgWarp
       if (i < 4) TRACE(2 + i);
     }
     TRACE(6);
-    grid_sync(G);
+    grid_sync(G, static_cast<unsigned>(it) + 1u);
     TRACE(7);
     if (threadIdx.x == 0) s_active = __ldcg(G.active);
     __syncthreads();
@@ -1513,6 +1519,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
         ev1 = c.event(2 * evs.size() + 1);
         MLG_CUDA(cudaEventRecord(ev0, st));
       }
+      gsync.zero(st);  // barrier counter restarts with every launch
       const void* fn = lap ? reinterpret_cast<const void*>(&k_cg_persist<true, true>)
                            : reinterpret_cast<const void*>(&k_cg_persist<true, false>);
       MLG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args, 0, st));
