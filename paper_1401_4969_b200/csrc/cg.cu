@@ -44,6 +44,11 @@ namespace mlg {
 namespace {
 
 constexpr int kBlock = CgBatch::kBlock;
+// Persistent kernel: systems with at most this many tiles are reduced
+// redundantly by every CTA holding one of their tiles after the grid barrier;
+// larger systems keep the last-tile reduction before it (reading hundreds of
+// partials per CTA costs more than the atomic round trip).
+constexpr int kReplTiles = 96;
 constexpr unsigned kFull = 0xffffffffu;
 
 #ifdef MLG_CG_TRACE
@@ -1028,7 +1033,11 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
       atomicAdd(F.rows + (mode == kModeCheck ? 1 : 0), 1ull * n);
     }
   }
-  finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
+  if (PERSIST && S.ntiles <= kReplTiles)  // reduced after the grid barrier (k_cg_persist)
+    block_reduce_store<kCgDots, kBlock>(acc,
+                                        F.part + static_cast<long long>(S.toff + tl.t) * kCgDots);
+  else
+    finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
 }
 
 template <bool UNI, bool ASYNC, bool LAP>
@@ -1058,10 +1067,9 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
 constexpr int kPersistTiles = 8;
 
 struct GridSync {
-  unsigned* count;  // arrivals since the launch began (zeroed before each launch)
-  unsigned* gen;    // unused (kept for the layout of the sync buffer)
-  int* active;      // systems still running
-  int max_iters;    // safety bound (every system stops by maxit)
+  unsigned* count;    // arrivals since the launch began (zeroed before each launch)
+  unsigned* running;  // [3] running-system counts of the last iterations (zeroed per launch)
+  int max_iters;      // iterations of this launch (even: vector parity is preserved)
 };
 
 // Barrier number k (k = 1, 2, ... within the launch): arrive on a monotonic
@@ -1105,43 +1113,96 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_PERSIST_MINBLOCKS * 4 / kCgWarp
                  double* R1, double* P0, double* P1, Finish F, GridSync G) {
   __shared__ CgSys s_sys[kPersistTiles];
   __shared__ CgTile s_tl[kPersistTiles];
-  __shared__ int s_mode[kPersistTiles], s_rst[kPersistTiles];
-  __shared__ double s_al[kPersistTiles], s_be[kPersistTiles];
-  __shared__ int s_active;
+  __shared__ CgCtl s_ctl[kPersistTiles];  // private copy of the tile's system scalars
+  __shared__ double s_red[kCgWarps][kCgDots];
+  __shared__ unsigned s_running;
   const int mine = (ntiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1;
   if (threadIdx.x < mine) {
     const CgTile t = tiles[blockIdx.x + threadIdx.x * gridDim.x];
     s_tl[threadIdx.x] = t;
-    if (t.sys >= 0) s_sys[threadIdx.x] = sys[t.sys];
+    if (t.sys >= 0) {
+      s_sys[threadIdx.x] = sys[t.sys];
+      s_ctl[threadIdx.x] = load_ctl(F.ctl + t.sys);
+    }
   }
+  __syncthreads();
   unsigned long long rows_acc = 0;
   for (int it = 0; it < G.max_iters; ++it) {
     const bool odd = it & 1;
     TRACE(0);
-    if (threadIdx.x < mine && s_tl[threadIdx.x].sys >= 0) {  // written by other CTAs: via L2
-      const CgCtl* c = F.ctl + s_tl[threadIdx.x].sys;
-      s_mode[threadIdx.x] = __ldcg(&c->mode);
-      s_rst[threadIdx.x] = __ldcg(&c->restart);
-      s_al[threadIdx.x] = __ldcg(&c->alpha);
-      s_be[threadIdx.x] = __ldcg(&c->beta);
-    }
-    __syncthreads();
     TRACE(1);
     for (int i = 0; i < mine; ++i) {
       if (s_tl[i].sys < 0) continue;  // empty slot (CTA-uniform)
-      cg_tile<UNI, false, true, LAP>(s_sys[i], s_tl[i], s_mode[i], s_al[i], s_be[i], s_rst[i] != 0, A,
-                                bsrc, bstride, X, odd ? R1 : R0, odd ? R0 : R1, odd ? P1 : P0,
-                                odd ? P0 : P1, F, nullptr, rows_acc);
+      const CgCtl& c = s_ctl[i];
+      cg_tile<UNI, false, true, LAP>(s_sys[i], s_tl[i], c.mode, c.alpha, c.beta, c.restart != 0, A,
+                                     bsrc, bstride, X, odd ? R1 : R0, odd ? R0 : R1,
+                                     odd ? P1 : P0, odd ? P0 : P1, F, nullptr, rows_acc);
       __syncthreads();  // shared scratch of the tile body is reused
       if (i < 4) TRACE(2 + i);
     }
     TRACE(6);
     grid_sync(G, static_cast<unsigned>(it) + 1u);
     TRACE(7);
-    if (threadIdx.x == 0) s_active = __ldcg(G.active);
+    // Every CTA reduces the tile partials of its own systems in the same fixed
+    // order (thread t takes tiles t, t + kBlock, ...; then a fixed tree), so all
+    // copies of a system's scalars stay bitwise identical -- no "last tile"
+    // atomics or fences on the critical path.  Termination: the holder of a
+    // system's tile 0 counts it in running[it % 3] while it runs; that slot is
+    // complete at the next barrier and is cleared two iterations later.
+    unsigned running_prev = 1;
+    if (threadIdx.x == 0) {
+      if (it > 0) running_prev = __ldcg(G.running + (it - 1) % 3);
+      if (blockIdx.x == 0) G.running[(it + 1) % 3] = 0u;
+    }
+    for (int i = 0; i < mine; ++i) {
+      const int sy = s_tl[i].sys;
+      if (sy < 0) continue;
+      const CgSys& S = s_sys[i];
+      if (S.ntiles > kReplTiles) {  // reduced by its last tile before the barrier
+        if (threadIdx.x == 0) {
+          s_ctl[i] = load_ctl(F.ctl + sy);
+          if (s_tl[i].t == 0 && s_ctl[i].status == kRunning) atomicAdd(G.running + it % 3, 1u);
+        }
+        __syncthreads();
+        continue;
+      }
+      double a[kCgDots];
+#pragma unroll
+      for (int q = 0; q < kCgDots; ++q) a[q] = 0.0;
+      for (int tt = threadIdx.x; tt < S.ntiles; tt += kBlock) {
+        const double* p = F.part + static_cast<long long>(S.toff + tt) * kCgDots;
+#pragma unroll
+        for (int q = 0; q < kCgDots; ++q) a[q] += __ldcg(p + q);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < kCgDots; ++q) a[q] += __shfl_xor_sync(kFull, a[q], o);
+      if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int q = 0; q < kCgDots; ++q) s_red[threadIdx.x >> 5][q] = a[q];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < kCgDots; ++q) {
+          double v = 0.0;
+          for (int w = 0; w < kCgWarps; ++w) v += s_red[w][q];
+          a[q] = v;
+        }
+        CgCtl c = s_ctl[i];
+        if (c.mode != kModeSkip) update_ctl<kPhaseIter>(c, a, F.tol, S.maxit);
+        s_ctl[i] = c;
+        if (s_tl[i].t == 0 && c.status == kRunning) atomicAdd(G.running + it % 3, 1u);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) s_running = running_prev;
     __syncthreads();
-    if (s_active == 0) break;
+    if (s_running == 0) break;  // every system had stopped one iteration ago
   }
+  // write the scalars back (one copy per system: the holder of its tile 0)
+  if (threadIdx.x < mine && s_tl[threadIdx.x].sys >= 0 && s_tl[threadIdx.x].t == 0)
+    F.ctl[s_tl[threadIdx.x].sys] = s_ctl[threadIdx.x];
   if (F.rows && (threadIdx.x & 31) == 0 && rows_acc) {
     atomicAdd(F.rows, rows_acc & ((1ull << 40) - 1));
     atomicAdd(F.rows + 1, rows_acc >> 40);
@@ -1455,7 +1516,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     prof_rows.ensure(2);
     prof_rows.zero(c.stream);
   }
-  gsync.ensure(2);
+  gsync.ensure(4);  // persistent kernel: barrier counter + running[3]
   gsync.zero(st);
   active_d.ensure(1);
   active_d.upload(&nsys, 1, st);
@@ -1508,7 +1569,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     double* xp = X.get();
     double *r0 = R0.get(), *r1 = R1.get(), *p0 = P0.get(), *p1 = P1.get();
     const Finish& Fl = profiling ? Fp : F;
-    GridSync G{gsync.get(), gsync.get() + 1, active_d.get(), kIters};
+    GridSync G{gsync.get(), gsync.get() + 1, kIters};
     void* args[] = {(void*)&sp, (void*)&tp, (void*)&ntiles, (void*)&A, (void*)&bsrc,
                     (void*)&bstride, (void*)&xp, (void*)&r0, (void*)&r1, (void*)&p0,
                     (void*)&p1, (void*)&Fl, (void*)&G};
@@ -1528,10 +1589,11 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
         MLG_CUDA(cudaEventRecord(ev1, st));
         evs.emplace_back(ev0, ev1);
       }
-      int left = 0;
-      active_d.download(&left, 1, st);
+      ctl_d.download(ctl.data(), ctl.size(), st);
       c.sync();
-      if (left == 0) break;
+      bool any = false;
+      for (const CgCtl& q : ctl) any |= q.status == kRunning;
+      if (!any) break;
       if (launch > 1000) throw SolverError("cg_solve: persistent CG did not terminate");
     }
 #ifdef MLG_CG_TRACE
