@@ -1309,12 +1309,43 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   // waves x (krows + c0) from half the first choice up to the cap.
   {
     const int resident = use_persist ? resident_persist() : resident_tiles(use_async);
+    // Strip systems drop the tasks whose output cells lie inside one G_j
+    // (setup below); count them per block in closed form.
+    auto inside_tasks = [&](const CgSys& s, int kr) {
+      if (!mask_) return 0LL;
+      const StripGeom& g = lev.strip_geom;
+      long long n = 0;
+      for (int bx = 0; bx < g.side; ++bx)
+        for (int by = 0; by < g.side; ++by) {
+          const int gx0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+          const int gx1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+          const int gy0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+          const int gy1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+          long long cs = 0, cr = 0;
+          for (int c = 0; c * kCgCols < s.w; ++c) {
+            const int ca = s.x0 + c * kCgCols, cb = s.x0 + std::min(c * kCgCols + kCgCols, s.w) - 1;
+            cs += ca >= gx0 && cb <= gx1;
+          }
+          for (int r = 0; r * kr < s.h; ++r) {
+            const int ra = s.y0 + r * kr, rb = s.y0 + std::min(r * kr + kr, s.h) - 1;
+            cr += ra >= gy0 && rb <= gy1;
+          }
+          n += cs * cr;
+        }
+      return n;
+    };
     auto tiles_for = [&](int kr) {
+      // strip systems (mask) all share one window: count its dropped tasks once.
+      // (Persistent batches keep the uncompacted count: there the per-tile
+      // fixed cost favours fewer, taller tiles -- measured at config 2.)
+      const long long drop =
+          mask_ && !use_persist && !systems.empty() ? inside_tasks(systems[0], kr) : 0;
       long long t = 0;
       for (const CgSys& s : systems) {
         const long long ns = std::max(1, (s.w + kCgCols - 1) / kCgCols);
         const long long nb = std::max(1, (s.h + kr - 1) / kr);
-        t += (ns * nb + kCgWarps - 1) / kCgWarps;
+        const long long nt = std::max(1LL, ns * nb - drop);
+        t += (nt + kCgWarps - 1) / kCgWarps;
       }
       return t;
     };
