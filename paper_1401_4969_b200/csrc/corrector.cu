@@ -804,13 +804,40 @@ std::vector<DensePair> dense_gen_eigensolve_dev(Ctx& c, int n, double* a, double
   w.eigw.ensure(n);
   w.info.ensure(1);
   int lwork = 0;
-  cusolverDnDsygvd_bufferSize(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                              CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, w.eigw.get(), &lwork);
-  w.work.ensure(std::max(lwork, 1));
-  const cusolverStatus_t st =
-      cusolverDnDsygvd(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                       CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, w.eigw.get(), w.work.get(), lwork,
-                       w.info.get());
+  static const int variant = [] {  // A/B hook: 0 sygvd, 1 sygvdx (lowest nev), 2 sygvj
+    const char* e = std::getenv("MLG_AUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  cusolverStatus_t st;
+  if (variant == 1) {
+    int h_meig = 0;
+    cusolverDnDsygvdx_bufferSize(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                 CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, 0.0,
+                                 0.0, 1, nev, &h_meig, w.eigw.get(), &lwork);
+    w.work.ensure(std::max(lwork, 1));
+    st = cusolverDnDsygvdx(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                           CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, 0.0, 0.0,
+                           1, nev, &h_meig, w.eigw.get(), w.work.get(), lwork, w.info.get());
+  } else if (variant == 2) {
+    syevjInfo_t params = nullptr;
+    cusolverDnCreateSyevjInfo(&params);
+    cusolverDnDsygvj_bufferSize(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, w.eigw.get(), &lwork,
+                                params);
+    w.work.ensure(std::max(lwork, 1));
+    st = cusolverDnDsygvj(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                          CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, w.eigw.get(), w.work.get(),
+                          lwork, w.info.get(), params);
+    c.sync();
+    cusolverDnDestroySyevjInfo(params);
+  } else {
+    cusolverDnDsygvd_bufferSize(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, w.eigw.get(), &lwork);
+    w.work.ensure(std::max(lwork, 1));
+    st = cusolverDnDsygvd(c.solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                          CUBLAS_FILL_MODE_LOWER, n, a, n, b, n, w.eigw.get(), w.work.get(),
+                          lwork, w.info.get());
+  }
   if (st != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnDsygvd failed to launch");
   int info = 0;
   std::vector<double> lam(nev);

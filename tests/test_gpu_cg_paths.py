@@ -1,0 +1,65 @@
+"""Every CG code path reproduces the reference's multilevel eigenvalues (golden
+vectors from the compiled reference, tests/golden/golden.json).
+
+The path is chosen per batch at run time (persistent cooperative kernel for
+L2-resident batches, multi-launch register pipeline, cp.async row pipeline for
+HBM-streaming batches, general per-row stencil, generic uniform stencil); the
+selection hooks are read once per process, so each variant runs in its own
+subprocess."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLDEN = json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())
+CASES = ["small_L3_nev3", "unit8_L3_m4_nev4", "square_L4_nev5", "unit8_L4_m4_nev1"]
+VARIANTS = {
+    "default": {},
+    "multi_launch_registers": {"MLG_CG_PERSIST": "0"},
+    "cp_async_pipeline": {"MLG_CG_ASYNC": "1"},
+    "general_stencil": {"MLG_GENERAL_STENCIL": "1"},
+    "generic_uniform_stencil": {"MLG_CG_NOLAP": "1"},
+    "short_tasks": {"MLG_CG_MINROWS": "4", "MLG_CG_MAXROWS": "8"},
+}
+
+SCRIPT = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import paper_1401_4969_b200 as mlg
+out = {}
+for name, c in json.loads(sys.argv[2]).items():
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*c["domain"]), H=c["H"], delta=c["delta"], m=c["m"],
+                        n_levels=c["n_levels"], nev=c["nev"])
+    with mlg.Hierarchy(cfg) as hy:
+        lam, pairs, matched, times = mlg.multilevel_correction(hy)
+    out[name] = [list(map(float, l)) for l in lam]
+print(json.dumps(out))
+"""
+
+
+def _run(env_extra):
+    cfgs = {n: GOLDEN["multilevel"][n]["config"] for n in CASES if n in GOLDEN["multilevel"]}
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), json.dumps(cfgs)],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_cg_path_matches_golden_eigenvalues(variant):
+    got = _run(VARIANTS[variant])
+    for name, lams in got.items():
+        ref = GOLDEN["multilevel"][name]["lambdas"]
+        assert len(lams) == len(ref), name
+        for k, (a, b) in enumerate(zip(lams, ref)):
+            a, b = np.asarray(a), np.asarray(b)
+            rel = np.max(np.abs(a - b) / np.abs(b))
+            assert rel <= 1e-10, (variant, name, k, rel)
