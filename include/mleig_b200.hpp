@@ -13,6 +13,11 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
+#include <cmath>
+#include <map>
+#include <optional>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -90,11 +95,13 @@ struct CorrectionState {  // corrector.hpp:103-107
   bool matched_previous = true;
 };
 
-struct LevelTrace {  // corrector.hpp:151-159 (errors are the caller's business)
+struct LevelTrace {  // corrector.hpp:151-159
   int level = 0;
   double h = 0.0;
   int interior_dofs = 0;
   std::vector<double> lambdas;
+  std::vector<double> eig_errors;  // NaN without a ReferenceSet
+  std::vector<double> h1_errors;   // NaN without a closed-form eigenfunction
   StepTimings timings;
   bool matched_previous = true;
   std::vector<EigenPair> pairs;
@@ -104,28 +111,50 @@ struct MultilevelResult {
   std::vector<LevelTrace> levels;
 };
 
+inline mlg_config to_c(const RunConfig& config) {
+  mlg_config c{};
+  c.x_min = config.domain.x_min;
+  c.x_max = config.domain.x_max;
+  c.y_min = config.domain.y_min;
+  c.y_max = config.domain.y_max;
+  c.H = config.H;
+  c.delta = config.delta;
+  c.m = config.m;
+  c.n_levels = config.n_levels;
+  c.degree = config.degree;
+  c.nev = config.nev;
+  c.example = config.example == "laplace" ? 0 : (config.example == "variable" ? 1 : -1);
+  if (c.example < 0)
+    throw ConfigError("unknown example id \"" + config.example +
+                      "\" (expected laplace or variable)");
+  c.workers = config.workers;
+  c.cg_tol = config.cg_tol;
+  c.deterministic = config.deterministic ? 1 : 0;
+  c.device = config.device;
+  return c;
+}
+
+inline RunConfig from_c(const mlg_config& c) {
+  RunConfig r;
+  r.domain = {c.x_min, c.x_max, c.y_min, c.y_max};
+  r.H = c.H;
+  r.delta = c.delta;
+  r.m = c.m;
+  r.n_levels = c.n_levels;
+  r.degree = c.degree;
+  r.nev = c.nev;
+  r.example = c.example == 1 ? "variable" : "laplace";
+  r.cg_tol = c.cg_tol;
+  r.workers = c.workers;
+  r.deterministic = c.deterministic != 0;
+  r.device = c.device;
+  return r;
+}
+
 class Hierarchy {
  public:
   explicit Hierarchy(const RunConfig& config) : config_(config) {
-    mlg_config c{};
-    c.x_min = config.domain.x_min;
-    c.x_max = config.domain.x_max;
-    c.y_min = config.domain.y_min;
-    c.y_max = config.domain.y_max;
-    c.H = config.H;
-    c.delta = config.delta;
-    c.m = config.m;
-    c.n_levels = config.n_levels;
-    c.degree = config.degree;
-    c.nev = config.nev;
-    c.example = config.example == "laplace" ? 0 : (config.example == "variable" ? 1 : -1);
-    if (c.example < 0)
-      throw ConfigError("unknown example id \"" + config.example +
-                        "\" (expected laplace or variable)");
-    c.workers = config.workers;
-    c.cg_tol = config.cg_tol;
-    c.deterministic = config.deterministic ? 1 : 0;
-    c.device = config.device;
+    const mlg_config c = to_c(config);
     check(mlg_create(&c, &ctx_));
   }
   ~Hierarchy() { mlg_destroy(ctx_); }
@@ -249,18 +278,89 @@ inline CorrectionState one_correction_step(Hierarchy& hy, const CorrectionState&
   return out;
 }
 
+// ---- reference sets and error reporting (fespace.hpp:103-120, harness.cpp:126-169) ----
+struct ExactFunction {  // a separable sine mode (make_reference's closed forms)
+  mlg_exact_mode mode{};
+  double value(double x, double y) const {
+    constexpr double kPi = 3.14159265358979323846;
+    return mode.amp * (std::sin(mode.mx * kPi * (x - mode.x0) / mode.lx) *
+                       std::sin(mode.my * kPi * (y - mode.y0) / mode.ly));
+  }
+  std::array<double, 2> gradient(double x, double y) const {
+    constexpr double kPi = 3.14159265358979323846;
+    const double ax = mode.mx * kPi / mode.lx, ay = mode.my * kPi / mode.ly;
+    return {mode.amp * (ax * std::cos(ax * (x - mode.x0)) * std::sin(ay * (y - mode.y0))),
+            mode.amp * (ay * std::sin(ax * (x - mode.x0)) * std::cos(ay * (y - mode.y0)))};
+  }
+};
+
+struct ReferenceSet {  // corrector.hpp
+  std::vector<double> lambdas;
+  std::map<int, ExactFunction> eigenfunctions;
+};
+
+inline int example_id(const std::string& example) {
+  if (example == "laplace") return 0;
+  if (example == "variable") return 1;
+  throw ConfigError("no reference data for example \"" + example + "\"");
+}
+
+// make_reference(example, nev): the reference's table ((-1,1)^2 for laplace).
+inline ReferenceSet make_reference(const std::string& example, int nev,
+                                   const DomainRect* domain = nullptr) {
+  const int ex = example_id(example);
+  std::vector<double> lam(static_cast<std::size_t>(std::max(nev, 0)));
+  std::vector<mlg_exact_mode> modes(lam.size());
+  const double dom[4] = {domain ? domain->x_min : -1.0, domain ? domain->x_max : 1.0,
+                         domain ? domain->y_min : -1.0, domain ? domain->y_max : 1.0};
+  check(mlg_make_reference(ex, nev, domain ? dom : nullptr, lam.data(), modes.data()));
+  ReferenceSet r;
+  r.lambdas = lam;
+  for (int i = 0; i < nev; ++i)
+    if (modes[i].mx > 0) r.eigenfunctions[i] = ExactFunction{modes[i]};
+  return r;
+}
+
+struct ErrorReport {  // fespace.hpp:108-112
+  double eig_err = 0.0, l2_err = 0.0, h1_err = 0.0;
+};
+
+// compute_errors (fespace.cpp:434-488); the sweep runs on the device.
+inline ErrorReport compute_errors(Hierarchy& hy, int level, const std::vector<double>& coeffs_full,
+                                  double lambda_h, double lambda_ref,
+                                  const ExactFunction* reference) {
+  mlg_error_report r{};
+  check(mlg_compute_errors(hy.handle(), level, coeffs_full.data(), lambda_h, lambda_ref,
+                           reference ? &reference->mode : nullptr, &r));
+  return {r.eig_err, r.l2_err, r.h1_err};
+}
+
 // multilevel_correction (corrector.cpp:414-462): level-1 direct solve, then
-// one correction step per level; the whole loop stays on the device.
-inline MultilevelResult multilevel_correction(Hierarchy& hy) {
+// one correction step per level; the whole loop stays on the device, and with
+// a ReferenceSet the per-level errors are computed there too.
+inline MultilevelResult multilevel_correction(Hierarchy& hy, const ReferenceSet* refs = nullptr) {
   const int nlev = hy.config().n_levels, nev = hy.config().nev;
   hy.extend_to(nlev);
-  std::vector<double> lam(static_cast<std::size_t>(nlev) * nev);
+  const std::size_t nn = static_cast<std::size_t>(nlev) * nev;
+  std::vector<double> lam(nn), ee(nn, std::nan("")), h1(nn, std::nan(""));
   std::vector<int> matched(static_cast<std::size_t>(nlev));
   std::vector<mlg_step_timings> t(static_cast<std::size_t>(nlev));
   const std::size_t n = static_cast<std::size_t>(hy.info(nlev).n_interior);
   std::vector<double> co(n * nev);
-  check(mlg_multilevel_correction(hy.handle(), nlev, lam.data(), co.data(), nullptr,
-                                  matched.data(), t.data()));
+  if (refs) {
+    const int nref = std::min(static_cast<int>(refs->lambdas.size()), nev);
+    std::vector<mlg_exact_mode> modes(static_cast<std::size_t>(std::max(nref, 1)));
+    for (int i = 0; i < nref; ++i) {
+      auto it = refs->eigenfunctions.find(i);
+      if (it != refs->eigenfunctions.end()) modes[i] = it->second.mode;
+    }
+    check(mlg_multilevel_correction_refs(hy.handle(), nlev, nref, refs->lambdas.data(),
+                                         modes.data(), lam.data(), ee.data(), nullptr, h1.data(),
+                                         co.data(), matched.data(), t.data()));
+  } else {
+    check(mlg_multilevel_correction(hy.handle(), nlev, lam.data(), co.data(), nullptr,
+                                    matched.data(), t.data()));
+  }
   MultilevelResult r;
   for (int k = 1; k <= nlev; ++k) {
     LevelTrace tr;
@@ -269,6 +369,8 @@ inline MultilevelResult multilevel_correction(Hierarchy& hy) {
     tr.h = i.h_max;
     tr.interior_dofs = static_cast<int>(i.n_interior);
     tr.lambdas.assign(lam.begin() + (k - 1) * nev, lam.begin() + k * nev);
+    tr.eig_errors.assign(ee.begin() + (k - 1) * nev, ee.begin() + k * nev);
+    tr.h1_errors.assign(h1.begin() + (k - 1) * nev, h1.begin() + k * nev);
     tr.timings = {t[k - 1].local_seconds, t[k - 1].iface_seconds, t[k - 1].aug_seconds};
     tr.matched_previous = matched[k - 1] != 0;
     if (k == nlev)
@@ -278,6 +380,92 @@ inline MultilevelResult multilevel_correction(Hierarchy& hy) {
     r.levels.push_back(std::move(tr));
   }
   return r;
+}
+
+// ---- experiment harness (harness.hpp; native code in libmlg_b200.so) ----
+inline RunConfig parse_config_json(const std::string& json_text) {
+  mlg_config c{};
+  check(mlg_parse_config_json(json_text.c_str(), &c));
+  return from_c(c);
+}
+
+inline RunConfig parse_config_file(const std::string& path) {
+  mlg_config c{};
+  check(mlg_parse_config_file(path.c_str(), &c));
+  return from_c(c);
+}
+
+inline std::vector<double> estimate_orders(const std::vector<double>& errors, double beta) {
+  std::vector<double> out(errors.empty() ? 0 : errors.size() - 1);
+  std::vector<double> tmp(std::max<std::size_t>(out.size(), 1));
+  check(mlg_estimate_orders(errors.data(), static_cast<int>(errors.size()), beta, tmp.data()));
+  std::copy(tmp.begin(), tmp.begin() + out.size(), out.begin());
+  return out;
+}
+
+struct ReportRow {  // harness.hpp:23-35
+  int level = 0;
+  double h = 0.0;
+  int dofs = 0;
+  int eig_index = 0;
+  double lambda = 0.0;
+  double eig_err = 0.0;
+  std::optional<double> h1_err;
+  std::optional<double> order;
+  double local_s = 0.0, iface_s = 0.0, aug_s = 0.0;
+};
+
+struct ExperimentReport {  // harness.hpp:37-41
+  RunConfig config;
+  std::vector<ReportRow> rows;
+};
+
+inline ExperimentReport run_experiment(const RunConfig& config, const std::string& csv_path) {
+  const mlg_config c = to_c(config);
+  std::vector<mlg_report_row> rows(static_cast<std::size_t>(std::max(config.n_levels * config.nev, 1)));
+  int n = 0;
+  check(mlg_run_experiment(&c, csv_path.c_str(), rows.data(), static_cast<int>(rows.size()), &n));
+  ExperimentReport rep;
+  rep.config = config;
+  for (int k = 0; k < n; ++k) {
+    const mlg_report_row& r = rows[k];
+    ReportRow o;
+    o.level = r.level;
+    o.h = r.h;
+    o.dofs = r.dofs;
+    o.eig_index = r.eig_index;
+    o.lambda = r.lambda;
+    o.eig_err = r.eig_err;
+    if (r.has_h1) o.h1_err = r.h1_err;
+    if (r.has_order) o.order = r.order;
+    o.local_s = r.local_s;
+    o.iface_s = r.iface_s;
+    o.aug_s = r.aug_s;
+    rep.rows.push_back(o);
+  }
+  return rep;
+}
+
+inline void write_csv(const ExperimentReport& report, const std::string& path) {
+  std::vector<mlg_report_row> rows;
+  for (const ReportRow& r : report.rows)
+    rows.push_back({r.level, r.h, r.dofs, r.eig_index, r.lambda, r.eig_err, r.h1_err ? 1 : 0,
+                    r.h1_err.value_or(0.0), r.order ? 1 : 0, r.order.value_or(0.0), r.local_s,
+                    r.iface_s, r.aug_s});
+  check(mlg_write_csv(rows.data(), static_cast<int>(rows.size()), path.c_str()));
+}
+
+inline void print_table(const std::string& csv_path, std::ostream& os) {
+  size_t len = 0;
+  check(mlg_print_table(csv_path.c_str(), nullptr, 0, &len));
+  std::string buf(len + 1, '\0');
+  check(mlg_print_table(csv_path.c_str(), buf.data(), buf.size(), &len));
+  os << buf.c_str();
+}
+
+inline void export_vtk(const RunConfig& config, const std::string& out_dir) {
+  const mlg_config c = to_c(config);
+  check(mlg_export_vtk(&c, out_dir.c_str()));
 }
 
 }  // namespace mleig_b200

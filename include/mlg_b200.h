@@ -186,6 +186,87 @@ int mlg_set_profiling(mlg_ctx* ctx, int on);
 int mlg_bench_spmv(mlg_ctx* ctx, int level, int reps, double* ms_per_launch,
                    double* bytes_per_launch);
 
+/* ---- error reporting and the experiment harness ------------------------
+ * (fespace.cpp:434-488 compute_errors, harness.cpp of the reference).  The
+ * closed-form reference eigenfunctions of make_reference are separable sine
+ * modes, so they cross the ABI as parameters instead of std::function. */
+
+/* amp * sin(mx pi (x-x0)/lx) * sin(my pi (y-y0)/ly); mx == 0: no closed form
+ * (the eigenvalue is multiple, harness.cpp:146-152). */
+typedef struct mlg_exact_mode {
+  int mx, my;
+  double x0, lx, y0, ly, amp;
+} mlg_exact_mode;
+
+/* ErrorReport (fespace.hpp:108-112); l2/h1 are NaN without a closed form. */
+typedef struct mlg_error_report {
+  double eig_err, l2_err, h1_err;
+} mlg_error_report;
+
+/* make_reference (harness.cpp:126-169): example 0 laplace, 1 variable.
+ * domain = {x_min, x_max, y_min, y_max} generalises the reference's (-1,1)^2
+ * Laplace table to the configured rectangle (bitwise the reference's table on
+ * (-1,1)^2); NULL = the reference's table.  lambdas[nev], modes[nev] (either
+ * may be NULL). */
+int mlg_make_reference(int example, int nev, const double* domain, double* lambdas,
+                       mlg_exact_mode* modes);
+
+/* compute_errors (fespace.cpp:434-488) of a full coefficient vector at
+ * `level` against lambda_ref and (if non-NULL with mx > 0) the closed form:
+ * 49-point Gauss-Duffy sweep over every element, on device. */
+int mlg_compute_errors(mlg_ctx* ctx, int level, const double* coeffs_full, double lambda_h,
+                       double lambda_ref, const mlg_exact_mode* reference,
+                       mlg_error_report* out);
+
+/* multilevel_correction with a ReferenceSet (corrector.cpp:414-462): as
+ * mlg_multilevel_correction plus per-level errors of the first n_refs pairs
+ * (LevelTrace::eig_errors / h1_errors, computed on the resident vectors);
+ * eig_err / l2_err / h1_err are [last_level][nev] (NaN where undefined), any
+ * may be NULL. */
+int mlg_multilevel_correction_refs(mlg_ctx* ctx, int last_level, int n_refs,
+                                   const double* ref_lambdas, const mlg_exact_mode* ref_modes,
+                                   double* lambdas, double* eig_err, double* l2_err,
+                                   double* h1_err, double* final_coeffs, int* matched,
+                                   mlg_step_timings* timings);
+
+/* parse_config_json / parse_config_file (harness.cpp:58-111): strict JSON
+ * (every field required, unknown keys rejected, ints must be integers), then
+ * validate_config.  device is set to 0. */
+int mlg_parse_config_json(const char* json_text, mlg_config* out);
+int mlg_parse_config_file(const char* path, mlg_config* out);
+
+/* estimate_orders (harness.cpp:113-122): orders[n-1]. */
+int mlg_estimate_orders(const double* errors, int n, double beta, double* orders);
+
+/* ReportRow (harness.hpp:23-35); optional columns carry a has_* flag. */
+typedef struct mlg_report_row {
+  int level;
+  double h;
+  int dofs, eig_index;
+  double lambda, eig_err;
+  int has_h1;
+  double h1_err;
+  int has_order;
+  double order;
+  double local_s, iface_s, aug_s;
+} mlg_report_row;
+
+/* run_experiment (harness.cpp:171-206): multilevel correction with the
+ * reference set of the example, rows written to csv_path (write_csv,
+ * harness.cpp:208-222, %.17g, byte-identical across runs when deterministic).
+ * rows may be NULL; n_rows receives n_levels*nev. */
+int mlg_run_experiment(const mlg_config* cfg, const char* csv_path, mlg_report_row* rows,
+                       int rows_cap, int* n_rows);
+int mlg_write_csv(const mlg_report_row* rows, int n, const char* path);
+
+/* print_table (harness.cpp:240-290) into buf (NUL-terminated, truncated to
+ * cap); *len = full length. */
+int mlg_print_table(const char* csv_path, char* buf, size_t cap, size_t* len);
+
+/* export_vtk (harness.cpp:292-351): final-level eigenfunctions as VTK legacy
+ * ASCII point data in out_dir/eigenfunctions.vtk. */
+int mlg_export_vtk(const mlg_config* cfg, const char* out_dir);
+
 #ifdef __cplusplus
 }
 #endif

@@ -261,3 +261,79 @@ def fnv1a64(*arrays) -> str:
             h ^= byte
             h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
     return f"{h:016x}"
+
+
+# ---- harness and error reporting (harness.hpp, fespace.hpp:103-120) ----
+def _cfg(domain=(-1.0, 1.0, -1.0, 1.0), H=0.5, delta=0.5, m=1, n_levels=2, nev=2, cg_tol=1e-10,
+         workers=1, degree=1, example=0, deterministic=True):
+    return RefConfig(*domain, H, delta, m, n_levels, degree, nev, example, workers, cg_tol,
+                     int(deterministic))
+
+
+def _cfg_dict(c: RefConfig) -> dict:
+    return {k: getattr(c, k) for k, _ in RefConfig._fields_}
+
+
+def parse_config_json(text: str):
+    """(status, message, config dict) of the reference's parse_config_json."""
+    out = RefConfig()
+    st = lib().ref_parse_config_json(text.encode(), C.byref(out))
+    return st, (lib().ref_last_error().decode() if st else ""), (_cfg_dict(out) if st == 0
+                                                                 else None)
+
+
+def parse_config_file(path: str):
+    out = RefConfig()
+    st = lib().ref_parse_config_file(str(path).encode(), C.byref(out))
+    return st, (lib().ref_last_error().decode() if st else ""), (_cfg_dict(out) if st == 0
+                                                                 else None)
+
+
+def estimate_orders(errors, beta):
+    e = np.ascontiguousarray(errors, np.float64)
+    out = np.empty(max(len(e) - 1, 1))
+    lib().ref_estimate_orders.argtypes = [dp, C.c_int, C.c_double, dp]
+    st = lib().ref_estimate_orders(_d(e), len(e), beta, _d(out))
+    if st:
+        raise RefError(st, lib().ref_last_error().decode())
+    return out[:max(len(e) - 1, 0)]
+
+
+def make_reference(example: str, nev: int, pts=None):
+    """lambdas, has_fn, and (value, dx, dy) of each closed form at pts (k x 2)."""
+    lam = np.empty(nev)
+    has = np.zeros(nev, np.int32)
+    pts = np.zeros((0, 2)) if pts is None else np.ascontiguousarray(pts, np.float64)
+    vals = np.zeros((nev, len(pts), 3))
+    _chk(lib().ref_make_reference(example.encode(), nev, _d(lam), _i(has), len(pts), _d(pts),
+                                  _d(vals)))
+    return lam, has.astype(bool), vals
+
+
+def run_experiment(csv_path, **kw):
+    c = _cfg(**kw)
+    _chk(lib().ref_run_experiment(C.byref(c), str(csv_path).encode()))
+
+
+def print_table(csv_path) -> str:
+    n = C.c_ulong()
+    lib().ref_print_table.argtypes = [C.c_char_p, C.c_char_p, C.c_ulong, C.POINTER(C.c_ulong)]
+    _chk(lib().ref_print_table(str(csv_path).encode(), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _chk(lib().ref_print_table(str(csv_path).encode(), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def export_vtk(out_dir, **kw):
+    c = _cfg(**kw)
+    _chk(lib().ref_export_vtk(C.byref(c), str(out_dir).encode()))
+
+
+def compute_errors(h: "RefHierarchy", level, coeffs_full, lambda_h, lambda_ref, ref_index=-1):
+    """compute_errors with make_reference("laplace")'s eigenfunction ref_index."""
+    u = np.ascontiguousarray(coeffs_full, np.float64)
+    out = np.empty(3)
+    lib().ref_compute_errors.argtypes = [C.c_void_p, C.c_int, dp, C.c_double, C.c_double,
+                                         C.c_int, dp]
+    _chk(lib().ref_compute_errors(h.h, level, _d(u), lambda_h, lambda_ref, ref_index, _d(out)))
+    return out

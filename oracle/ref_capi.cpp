@@ -9,6 +9,9 @@
 //   local_bvp_solve / interface_solve /
 //   augmented_eigensolve / one_correction_step   corrector.hpp:112-136
 //   cg_solve / dense_gen_eigensolve        sparse.hpp:118-131
+//   compute_errors                         fespace.hpp:118-120
+//   parse_config_json / run_experiment /
+//   print_table / export_vtk / make_reference   harness.hpp:16-67
 // Status codes follow the reference's exit-code taxonomy (mleig_main.cpp:57-66):
 // 0 ok, 2 ConfigError, 3 SolverError, 4 IoError, 1 anything else.
 #include <chrono>
@@ -18,7 +21,10 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
 #include "mleig/corrector.hpp"
+#include "mleig/harness.hpp"
 #include "mleig/decomp.hpp"
 #include "mleig/fespace.hpp"
 #include "mleig/mesh.hpp"
@@ -451,6 +457,117 @@ int ref_dense_gen_eigensolve(int n, const double* a, const double* b, int nev, d
       from_vec(pairs[i].vec, vecs + static_cast<long>(i) * n);
     }
   });
+}
+
+// ---- harness and error reporting (harness.hpp, fespace.hpp:103-120) ----
+static void to_ref(const RunConfig& cfg, RefConfig* c) {
+  c->x_min = cfg.domain.x_min;
+  c->x_max = cfg.domain.x_max;
+  c->y_min = cfg.domain.y_min;
+  c->y_max = cfg.domain.y_max;
+  c->H = cfg.H;
+  c->delta = cfg.delta;
+  c->m = cfg.m;
+  c->n_levels = cfg.n_levels;
+  c->degree = cfg.degree;
+  c->nev = cfg.nev;
+  c->example = cfg.example == "variable" ? 1 : (cfg.example == "laplace" ? 0 : -1);
+  c->workers = cfg.workers;
+  c->cg_tol = cfg.cg_tol;
+  c->deterministic = cfg.deterministic ? 1 : 0;
+}
+
+static RunConfig from_ref(const RefConfig* c) {
+  RunConfig cfg;
+  cfg.domain = {c->x_min, c->x_max, c->y_min, c->y_max};
+  cfg.H = c->H;
+  cfg.delta = c->delta;
+  cfg.m = c->m;
+  cfg.n_levels = c->n_levels;
+  cfg.degree = c->degree;
+  cfg.nev = c->nev;
+  cfg.example = c->example == 1 ? "variable" : "laplace";
+  cfg.workers = c->workers;
+  cfg.cg_tol = c->cg_tol;
+  cfg.deterministic = c->deterministic != 0;
+  return cfg;
+}
+
+int ref_parse_config_json(const char* text, RefConfig* out) {
+  return guarded([&] { to_ref(parse_config_json(text), out); });
+}
+
+int ref_parse_config_file(const char* path, RefConfig* out) {
+  return guarded([&] { to_ref(parse_config_file(path), out); });
+}
+
+int ref_estimate_orders(const double* e, int n, double beta, double* out) {
+  return guarded([&] {
+    const auto o = estimate_orders(std::vector<double>(e, e + n), beta);
+    for (std::size_t k = 0; k < o.size(); ++k) out[k] = o[k];
+  });
+}
+
+// lambdas[nev]; has_fn[nev]; fn values at the probe points (x,y)[np] -> vals[nev][np][3]
+// (value, du/dx, du/dy) for the indices with a closed form.
+int ref_make_reference(const char* example, int nev, double* lambdas, int* has_fn, int np,
+                       const double* pts, double* vals) {
+  return guarded([&] {
+    const ReferenceSet r = make_reference(example, nev);
+    for (int i = 0; i < nev; ++i) {
+      lambdas[i] = r.lambdas[i];
+      auto it = r.eigenfunctions.find(i);
+      has_fn[i] = it != r.eigenfunctions.end();
+      if (has_fn[i] && vals)
+        for (int k = 0; k < np; ++k) {
+          const double x = pts[2 * k], y = pts[2 * k + 1];
+          const auto g = it->second.gradient(x, y);
+          double* o = vals + (static_cast<long>(i) * np + k) * 3;
+          o[0] = it->second.value(x, y);
+          o[1] = g[0];
+          o[2] = g[1];
+        }
+    }
+  });
+}
+
+// compute_errors with the make_reference("laplace") eigenfunction of index
+// ref_index (< 0: none), on a full coefficient vector of `level`.
+int ref_compute_errors(void* h, int level, const double* coeffs_full, double lambda_h,
+                       double lambda_ref, int ref_index, double* out3) {
+  return guarded([&] {
+    const LevelSystem& L = H(h).level(level);
+    const ReferenceSet r = make_reference("laplace", std::max(ref_index + 1, 1));
+    const ExactFunction* fn = nullptr;
+    if (ref_index >= 0) fn = &r.eigenfunctions.at(ref_index);
+    const ErrorReport e = compute_errors(L.space, H(h).field(), to_vec(coeffs_full, L.space.ndofs),
+                                         lambda_h, lambda_ref, fn);
+    out3[0] = e.eig_err;
+    out3[1] = e.l2_err;
+    out3[2] = e.h1_err;
+  });
+}
+
+int ref_run_experiment(const RefConfig* c, const char* csv_path) {
+  return guarded([&] { run_experiment(from_ref(c), csv_path); });
+}
+
+int ref_print_table(const char* csv_path, char* buf, unsigned long cap, unsigned long* len) {
+  return guarded([&] {
+    std::ostringstream os;
+    print_table(csv_path, os);
+    const std::string s = os.str();
+    *len = s.size();
+    if (buf && cap > 0) {
+      const std::size_t n = std::min<std::size_t>(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+
+int ref_export_vtk(const RefConfig* c, const char* out_dir) {
+  return guarded([&] { export_vtk(from_ref(c), out_dir); });
 }
 
 }  // extern "C"

@@ -168,9 +168,52 @@ def build_space(mesh):  # fespace.cpp:230-312 (degree 1)
 QUAD2 = (np.array([[0.5, 0.5, 0.0], [0.0, 0.5, 0.5], [0.5, 0.0, 0.5]]), 1.0 / 3.0)  # :41-47
 
 
-def local_matrices(mesh):
+# quad_degree6 (make_degree6, fespace.cpp:49-75): barycentrics and weights, same order
+_A1, _B1, _W1 = 0.501426509658179, 0.249286745170910, 0.116786275726379
+_A2, _B2, _W2 = 0.873821971016996, 0.063089014491502, 0.050844906370207
+_A3, _B3, _C3, _W3 = 0.053145049844816, 0.310352451033785, 0.636502499121399, 0.082851075618374
+QUAD6 = [((_A1, _B1, _B1), _W1), ((_B1, _A1, _B1), _W1), ((_B1, _B1, _A1), _W1),
+         ((_A2, _B2, _B2), _W2), ((_B2, _A2, _B2), _W2), ((_B2, _B2, _A2), _W2),
+         ((_A3, _B3, _C3), _W3), ((_A3, _C3, _B3), _W3), ((_B3, _A3, _C3), _W3),
+         ((_B3, _C3, _A3), _W3), ((_C3, _A3, _B3), _W3), ((_C3, _B3, _A3), _W3)]
+
+
+def local_matrices_variable(mesh):
+    """CoefficientField::variable (fespace.cpp:114-123) with the degree-6 rule
+    (default_rule, fespace.cpp:219-222), operation order of local_matrix
+    (fespace.cpp:185-217).  np.exp is not glibc's exp: entries agree with the
+    reference to a few ulp."""
+    v = mesh.vertices[mesh.triangles]
+    x0, y0, x1, y1, x2, y2 = (v[:, 0, 0], v[:, 0, 1], v[:, 1, 0], v[:, 1, 1], v[:, 2, 0],
+                              v[:, 2, 1])
+    area2 = (x1 - x0) * (y2 - y0) - (x2 - x0) * (y1 - y0)
+    area = 0.5 * area2
+    g = np.stack([np.stack([(y1 - y2) / area2, (x2 - x1) / area2], 1),
+                  np.stack([(y2 - y0) / area2, (x0 - x2) / area2], 1),
+                  np.stack([(y0 - y1) / area2, (x1 - x0) / area2], 1)], axis=1)
+    T = len(v)
+    KA = np.zeros((T, 3, 3))
+    KM = np.zeros((T, 3, 3))
+    for (l, wq) in QUAD6:
+        w = wq * area
+        x = l[0] * x0 + l[1] * x1 + l[2] * x2
+        y = l[0] * y0 + l[1] * y1 + l[2] * y2
+        d0, d1, d2 = np.exp(1.0 + x * x), np.exp(x * y), np.exp(1.0 + y * y)
+        phi = (1.0 + x * x) * (1.0 + y * y)
+        for i in range(3):
+            agx = d0 * g[:, i, 0] + d1 * g[:, i, 1]
+            agy = d1 * g[:, i, 0] + d2 * g[:, i, 1]
+            for j in range(i, 3):
+                KA[:, i, j] = KA[:, i, j] + w * (agx * g[:, j, 0] + agy * g[:, j, 1])
+                KM[:, i, j] = KM[:, i, j] + w * phi * l[i] * l[j]
+    return KA, KM
+
+
+def local_matrices(mesh, example="laplace"):
     """Element stiffness and mass, P1, Laplace field, 3-point rule, in the exact
     operation order of local_matrix/element_geometry (fespace.cpp:169-217)."""
+    if example == "variable":
+        return local_matrices_variable(mesh)
     v = mesh.vertices[mesh.triangles]                            # [T,3,2]
     x0, y0, x1, y1, x2, y2 = (v[:, 0, 0], v[:, 0, 1], v[:, 1, 0], v[:, 1, 1], v[:, 2, 0],
                               v[:, 2, 1])
@@ -220,8 +263,8 @@ def from_upper_triplets(n, rows, cols, vals):  # sparse.cpp:24-61
     return np.cumsum(row_ptr).astype(np.int32), fc.astype(np.int32), fv
 
 
-def assemble(space):  # assemble_form fespace.cpp:314-341, both forms
-    KA, KM = local_matrices(space.mesh)
+def assemble(space, example="laplace"):  # assemble_form fespace.cpp:314-341, both forms
+    KA, KM = local_matrices(space.mesh, example)
     iu, ju = np.triu_indices(3)                                  # i<=j, row-major order
     gi, gj = space.connectivity[:, iu], space.connectivity[:, ju]
     rows = np.minimum(gi, gj).reshape(-1).astype(np.int64)
@@ -459,14 +502,15 @@ class Level:
 
 class Hierarchy:  # corrector.cpp:111-181
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), H=0.25, delta=0.1, m=4, n_levels=5,
-                 nev=5, cg_tol=1e-10):
+                 nev=5, cg_tol=1e-10, example="laplace"):
         self.n_levels, self.nev, self.cg_tol = n_levels, nev, cg_tol
+        self.example = example
         mesh = build_structured_mesh(domain, H)
         cell = mesh.dx
         dc = max(1, int(np.ceil(delta / cell - 1e-9)))         # corrector.cpp:117-121
         self.part = build_partition(mesh, m, dc * cell)
         sp0 = build_space(mesh)
-        self.levels = [Level(mesh, sp0, *assemble(sp0))]
+        self.levels = [Level(mesh, sp0, *assemble(sp0, example))]
         self._dense = None
 
     def extend_to(self, level):  # corrector.cpp:131-146
@@ -474,7 +518,8 @@ class Hierarchy:  # corrector.cpp:111-181
             prev = self.levels[-1]
             mesh = refine_regular(prev.mesh)
             s = build_space(mesh)
-            self.levels.append(Level(mesh, s, *assemble(s), prolongation(prev.space, s)))
+            self.levels.append(Level(mesh, s, *assemble(s, self.example),
+                                     prolongation(prev.space, s)))
 
     def prolong(self, full, a, b):  # corrector.cpp:158-163
         for k in range(a + 1, b + 1):

@@ -7,10 +7,11 @@ from .corrector import (CorrectionState, DomainRect, EigenPair, Hierarchy, RunCo
                         SolveReport, StepTimings, augmented_eigensolve, coarse_eigensolve,
                         interface_solve, local_bvp_solve, multilevel_correction,
                         one_correction_step)
+from . import harness
 
 __all__ = [
     "ConfigError", "CudaError", "IoError", "MlgError", "SolverError", "lib",
     "CorrectionState", "DomainRect", "EigenPair", "Hierarchy", "RunConfig", "SolveReport",
     "StepTimings", "augmented_eigensolve", "coarse_eigensolve", "interface_solve",
-    "local_bvp_solve", "multilevel_correction", "one_correction_step",
+    "local_bvp_solve", "multilevel_correction", "one_correction_step", "harness",
 ]

@@ -16,7 +16,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libmlg_b200.so"
-SOURCES = ["mesh.cu", "assemble.cu", "cg.cu", "corrector.cu", "capi.cu"]
+SOURCES = ["mesh.cu", "assemble.cu", "cg.cu", "corrector.cu", "errors.cu", "capi.cu",
+           "harness.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3",

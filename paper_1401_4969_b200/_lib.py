@@ -77,6 +77,24 @@ class MlgStepTimings(C.Structure):
     ]
 
 
+class MlgExactMode(C.Structure):
+    _fields_ = [("mx", C.c_int), ("my", C.c_int), ("x0", C.c_double), ("lx", C.c_double),
+                ("y0", C.c_double), ("ly", C.c_double), ("amp", C.c_double)]
+
+
+class MlgErrorReport(C.Structure):
+    _fields_ = [("eig_err", C.c_double), ("l2_err", C.c_double), ("h1_err", C.c_double)]
+
+
+class MlgReportRow(C.Structure):
+    _fields_ = [
+        ("level", C.c_int), ("h", C.c_double), ("dofs", C.c_int), ("eig_index", C.c_int),
+        ("lambda_", C.c_double), ("eig_err", C.c_double), ("has_h1", C.c_int),
+        ("h1_err", C.c_double), ("has_order", C.c_int), ("order", C.c_double),
+        ("local_s", C.c_double), ("iface_s", C.c_double), ("aug_s", C.c_double),
+    ]
+
+
 # name -> argtypes (every symbol declared in include/mlg_b200.h)
 SIGNATURES = {
     "mlg_last_error": [],
@@ -108,6 +126,21 @@ SIGNATURES = {
                                    C.POINTER(MlgStepTimings)],
     "mlg_multilevel_correction": [C.c_void_p, C.c_int, c_double_p, c_double_p, C.c_void_p,
                                   c_int_p, C.POINTER(MlgStepTimings)],
+    "mlg_multilevel_correction_refs": [C.c_void_p, C.c_int, C.c_int, c_double_p,
+                                       C.POINTER(MlgExactMode), c_double_p, c_double_p,
+                                       c_double_p, c_double_p, c_double_p, c_int_p,
+                                       C.POINTER(MlgStepTimings)],
+    "mlg_make_reference": [C.c_int, C.c_int, c_double_p, c_double_p, C.POINTER(MlgExactMode)],
+    "mlg_compute_errors": [C.c_void_p, C.c_int, c_double_p, C.c_double, C.c_double,
+                           C.POINTER(MlgExactMode), C.POINTER(MlgErrorReport)],
+    "mlg_parse_config_json": [C.c_char_p, C.POINTER(MlgConfig)],
+    "mlg_parse_config_file": [C.c_char_p, C.POINTER(MlgConfig)],
+    "mlg_estimate_orders": [c_double_p, C.c_int, C.c_double, c_double_p],
+    "mlg_run_experiment": [C.POINTER(MlgConfig), C.c_char_p, C.POINTER(MlgReportRow), C.c_int,
+                           c_int_p],
+    "mlg_write_csv": [C.POINTER(MlgReportRow), C.c_int, C.c_char_p],
+    "mlg_print_table": [C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+    "mlg_export_vtk": [C.POINTER(MlgConfig), C.c_char_p],
     "mlg_set_profiling": [C.c_void_p, C.c_int],
     "mlg_bench_spmv": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
 }

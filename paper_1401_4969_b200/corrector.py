@@ -116,6 +116,9 @@ class LevelTrace:  # corrector.hpp:151-159 (reporting fields filled by the calle
     timings: StepTimings
     matched_previous: bool
     pairs: list
+    eig_errors: list = field(default_factory=list)  # filled when a ReferenceSet is given
+    l2_errors: list = field(default_factory=list)
+    h1_errors: list = field(default_factory=list)
 
 
 @dataclass

@@ -2,7 +2,9 @@
 // with the reference's element-order triplet accumulation.
 //
 //   local_matrix / element_geometry  fespace.cpp:169-217 (3-point edge-midpoint
-//                                    rule, quad_degree2 fespace.cpp:41-47)
+//                                    rule, quad_degree2 fespace.cpp:41-47, for the
+//                                    Laplace field; 12-point quad_degree6
+//                                    fespace.cpp:49-75 for the variable field)
 //   assemble_form                    fespace.cpp:314-341
 //   SparseSymMatrix::from_upper_triplets  sparse.cpp:24-61 (stable (row,col)
 //                                    sort => duplicates summed from 0.0 in
@@ -127,6 +129,136 @@ __device__ __forceinline__ void ordered_sum(Contrib* c, int n, double* a, double
   }
   *a = sa;
   *m = sm;
+}
+
+// ---- CoefficientField::variable (fespace.cpp:114-123) with quad_degree6 ----
+// Upper entries of the element matrices of one triangle in element-local
+// vertex order, packed (0,0),(0,1),(0,2),(1,1),(1,2),(2,2); the reference's
+// operation sequence of local_matrix (fespace.cpp:185-217) for degree 1:
+// per quadrature point w = weight*area, x = l0*v0x + l1*v1x + l2*v2x,
+// stiffness += w*(agx*g_j0 + agy*g_j1) with a = diffusion(x,y), mass +=
+// ((w*phi)*l_i)*l_j -- every operation rounded separately (the reference is
+// built for baseline x86-64: no FMA contraction).  exp() is CUDA's (<= 1 ulp),
+// so entries agree with the reference to a few ulp, not bitwise.
+__device__ __forceinline__ int upk(int i, int j) { return i * 3 - (i * (i - 1)) / 2 + (j - i); }
+
+__constant__ double kQ6[12][4];  // l0, l1, l2, weight (make_degree6, fespace.cpp:49-75)
+
+__device__ void elem_variable(double v0x, double v0y, double v1x, double v1y, double v2x,
+                              double v2y, double a[6], double m[6]) {
+  const double area2 = xsub(xmul(xsub(v1x, v0x), xsub(v2y, v0y)),
+                            xmul(xsub(v2x, v0x), xsub(v1y, v0y)));
+  const double area = xmul(0.5, area2);
+  double g[3][2];
+  g[0][0] = xdiv(xsub(v1y, v2y), area2);
+  g[0][1] = xdiv(xsub(v2x, v1x), area2);
+  g[1][0] = xdiv(xsub(v2y, v0y), area2);
+  g[1][1] = xdiv(xsub(v0x, v2x), area2);
+  g[2][0] = xdiv(xsub(v0y, v1y), area2);
+  g[2][1] = xdiv(xsub(v1x, v0x), area2);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) a[k] = m[k] = 0.0;
+  for (int q = 0; q < 12; ++q) {
+    const double l0 = kQ6[q][0], l1 = kQ6[q][1], l2 = kQ6[q][2];
+    const double w = xmul(kQ6[q][3], area);
+    const double x = xadd(xadd(xmul(l0, v0x), xmul(l1, v1x)), xmul(l2, v2x));
+    const double y = xadd(xadd(xmul(l0, v0y), xmul(l1, v1y)), xmul(l2, v2y));
+    const double d0 = exp(xadd(1.0, xmul(x, x)));
+    const double d1 = exp(xmul(x, y));
+    const double d2 = exp(xadd(1.0, xmul(y, y)));
+    const double phi = xmul(xadd(1.0, xmul(x, x)), xadd(1.0, xmul(y, y)));
+    const double l[3] = {l0, l1, l2};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double agx = xadd(xmul(d0, g[i][0]), xmul(d1, g[i][1]));
+      const double agy = xadd(xmul(d1, g[i][0]), xmul(d2, g[i][1]));
+#pragma unroll
+      for (int j = i; j < 3; ++j) {
+        a[upk(i, j)] = xadd(a[upk(i, j)], xmul(w, xadd(xmul(agx, g[j][0]), xmul(agy, g[j][1]))));
+        m[upk(i, j)] = xadd(m[upk(i, j)], xmul(xmul(xmul(w, phi), l[i]), l[j]));
+      }
+    }
+  }
+}
+
+// Element matrix of triangle (cell, upper) in its mesh vertex order; returns
+// false outside the lattice.
+__device__ __forceinline__ bool elem_matrix_var(const LevelGeom& G, int cx, int cy, int upper,
+                                                double a[6], double m[6], unsigned* e,
+                                                int* rot) {
+  if (cx < 0 || cy < 0 || cx >= G.nx || cy >= G.ny) return false;
+  const unsigned code = G.geo[2 * (static_cast<std::int64_t>(cy) * G.nx + cx) + upper];
+  *rot = static_cast<int>(code & 3u);
+  *e = code >> 2;
+  double vx[3], vy[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    int lx, ly;
+    canon_vertex(cx, cy, upper, (*rot + j) % 3, &lx, &ly);
+    vx[j] = lattice_coord(G.x0, lx, G.dx);
+    vy[j] = lattice_coord(G.y0, ly, G.dy);
+  }
+  elem_variable(vx[0], vy[0], vx[1], vy[1], vx[2], vy[2], a, m);
+  return true;
+}
+
+__device__ __forceinline__ void push_entry(const double a[6], const double m[6], unsigned e,
+                                           int rot, int kd, int kn, Contrib* list, int* n) {
+  const int ld = (kd - rot + 3) % 3, ln = (kn - rot + 3) % 3;
+  const int k = upk(min(ld, ln), max(ld, ln));
+  list[*n] = Contrib{e, a[k], m[k]};
+  ++*n;
+}
+
+// Variable-coefficient assembly: one thread per dof computes each of its <= 6
+// triangles' element matrices once (12 quadrature points, 3 exp each) and
+// scatters the entries it owns into the C/E/N/NE lists, summed in ascending
+// element id as in k_assemble.
+__global__ void __launch_bounds__(kBlock) k_assemble_var(LevelGeom G, Stencil* stA,
+                                                         Stencil* stM, double* dinv) {
+  const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t nd = static_cast<std::int64_t>(G.nx + 1) * (G.ny + 1);
+  if (d >= nd) return;
+  const int ix = static_cast<int>(d % (G.nx + 1)), iy = static_cast<int>(d / (G.nx + 1));
+  Contrib cd[6], ce[2], cn[2], cne[2];
+  int nd_ = 0, ne_ = 0, nn_ = 0, nne_ = 0;
+  double a[6], m[6];
+  unsigned e;
+  int rot;
+  // T0 = L(ix,iy): diag k0; E (0,1); NE (0,2)
+  if (elem_matrix_var(G, ix, iy, 0, a, m, &e, &rot)) {
+    push_entry(a, m, e, rot, 0, 0, cd, &nd_);
+    push_entry(a, m, e, rot, 0, 1, ce, &ne_);
+    push_entry(a, m, e, rot, 0, 2, cne, &nne_);
+  }
+  // T1 = U(ix,iy): diag k0; N (0,2); NE (0,1)
+  if (elem_matrix_var(G, ix, iy, 1, a, m, &e, &rot)) {
+    push_entry(a, m, e, rot, 0, 0, cd, &nd_);
+    push_entry(a, m, e, rot, 0, 2, cn, &nn_);
+    push_entry(a, m, e, rot, 0, 1, cne, &nne_);
+  }
+  // T2 = L(ix-1,iy): diag k1; N (1,2)
+  if (elem_matrix_var(G, ix - 1, iy, 0, a, m, &e, &rot)) {
+    push_entry(a, m, e, rot, 1, 1, cd, &nd_);
+    push_entry(a, m, e, rot, 1, 2, cn, &nn_);
+  }
+  // T3 = U(ix,iy-1): diag k2; E (2,1)
+  if (elem_matrix_var(G, ix, iy - 1, 1, a, m, &e, &rot)) {
+    push_entry(a, m, e, rot, 2, 2, cd, &nd_);
+    push_entry(a, m, e, rot, 2, 1, ce, &ne_);
+  }
+  if (elem_matrix_var(G, ix - 1, iy - 1, 0, a, m, &e, &rot))  // T4 = L(ix-1,iy-1): k2
+    push_entry(a, m, e, rot, 2, 2, cd, &nd_);
+  if (elem_matrix_var(G, ix - 1, iy - 1, 1, a, m, &e, &rot))  // T5 = U(ix-1,iy-1): k1
+    push_entry(a, m, e, rot, 1, 1, cd, &nd_);
+  Stencil A{0.0, 0.0, 0.0, 0.0}, M{0.0, 0.0, 0.0, 0.0};
+  ordered_sum<6>(cd, nd_, &A.c, &M.c);
+  ordered_sum<2>(ce, ne_, &A.e, &M.e);
+  ordered_sum<2>(cn, nn_, &A.n, &M.n);
+  ordered_sum<2>(cne, nne_, &A.ne, &M.ne);
+  stA[d] = A;
+  stM[d] = M;
+  dinv[d] = 1.0 / A.c;
 }
 
 __global__ void __launch_bounds__(kBlock) k_assemble(LevelGeom G, Stencil* stA, Stencil* stM,
@@ -257,8 +389,26 @@ void assemble_level(Ctx& c, Level& L) {
   L.stM.alloc(nd);
   L.dinv.alloc(nd);
   LevelGeom G{L.nx, L.ny, c.cfg.x_min, c.cfg.y_min, L.dx, L.dy, L.geo.get()};
-  k_assemble<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
-                                                            L.dinv.get());
+  if (c.cfg.example == 1) {
+    {  // make_degree6 (fespace.cpp:49-75), same point order
+      const double a1 = 0.501426509658179, b1 = 0.249286745170910, w1 = 0.116786275726379;
+      const double a2 = 0.873821971016996, b2 = 0.063089014491502, w2 = 0.050844906370207;
+      const double a3 = 0.053145049844816, b3 = 0.310352451033785, c3 = 0.636502499121399,
+                   w3 = 0.082851075618374;
+      const double q[12][4] = {{a1, b1, b1, w1}, {b1, a1, b1, w1}, {b1, b1, a1, w1},
+                               {a2, b2, b2, w2}, {b2, a2, b2, w2}, {b2, b2, a2, w2},
+                               {a3, b3, c3, w3}, {a3, c3, b3, w3}, {b3, a3, c3, w3},
+                               {b3, c3, a3, w3}, {c3, a3, b3, w3}, {c3, b3, a3, w3}};
+      MLG_CUDA(cudaMemcpyToSymbolAsync(kQ6, q, sizeof(q), 0, cudaMemcpyHostToDevice,
+                                       c.stream));
+      c.sync();  // q is a host temporary
+    }
+    k_assemble_var<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
+                                                                  L.dinv.get());
+  } else {
+    k_assemble<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
+                                                              L.dinv.get());
+  }
   MLG_LAUNCH_CHECK();
   // Constant-coefficient detection for the CG fast path (MLG_GENERAL_STENCIL=1
   // forces the general per-row path, used by the tests to cover both).

@@ -2,6 +2,7 @@
 // exception taxonomy to status codes, and calls the device implementation.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -9,15 +10,23 @@
 
 #include "../../include/mlg_b200.h"
 #include "corrector.cuh"
+#include "errors.cuh"
 #include "vec_kernels.cuh"
 
 struct mlg_ctx {
   std::unique_ptr<mlg::Ctx> c;
 };
 
+namespace mlg {
+std::string& last_error_slot() {
+  static thread_local std::string s;
+  return s;
+}
+}  // namespace mlg
+
 namespace {
 
-thread_local std::string g_err;
+std::string& g_err = mlg::last_error_slot();
 
 template <class F>
 int guarded(F&& f) {
@@ -95,6 +104,79 @@ bool keep_dof(const mlg::Partition& p, int kind, int j, bool zero_trace, int S, 
       return true;
   }
   throw mlg::ConfigError("unknown region id");
+}
+
+mlg::ExactMode from_c(const mlg_exact_mode& m) {
+  mlg::ExactMode r;
+  r.mx = m.mx;
+  r.my = m.my;
+  r.x0 = m.x0;
+  r.lx = m.lx;
+  r.y0 = m.y0;
+  r.ly = m.ly;
+  r.amp = m.amp;
+  return r;
+}
+
+mlg_exact_mode to_c(const mlg::ExactMode& m) {
+  return mlg_exact_mode{m.mx, m.my, m.x0, m.lx, m.y0, m.ly, m.amp};
+}
+
+// multilevel_correction (corrector.cpp:414-462) with the optional ReferenceSet
+// of its `record` lambda: errors of the resident (interleaved) coefficients at
+// every level, outside the step timers like the reference.
+void multilevel_impl(mlg_ctx* ctx, int last_level, int n_refs, const double* ref_lambdas,
+                     const mlg_exact_mode* ref_modes, double* lambdas, double* eig_err,
+                     double* l2_err, double* h1_err, double* final_coeffs,
+                     double* d_final_coeffs, int* matched, mlg_step_timings* timings) {
+  mlg::Ctx& c = C(ctx);
+  const int nlev = last_level > 0 ? last_level : c.cfg.n_levels;
+  const int nev = c.cfg.nev;
+  const int nr = mlg::nr_for(nev);
+  mlg::DevBuf<double> u, u2;
+  auto record = [&](int k, const std::vector<double>& lam) {
+    std::copy(lam.begin(), lam.end(), lambdas + static_cast<std::size_t>(k - 1) * nev);
+    for (int i = 0; i < nev; ++i) {
+      const std::size_t o = static_cast<std::size_t>(k - 1) * nev + i;
+      double ee = std::nan(""), l2 = std::nan(""), h1 = std::nan("");
+      if (ref_lambdas && i < n_refs) {
+        mlg::ExactMode md;
+        const bool fn = ref_modes && ref_modes[i].mx > 0;
+        if (fn) md = from_c(ref_modes[i]);
+        const mlg::ErrorReport r = mlg::compute_errors(c, c.level(k), u.get(), nr, i, lam[i],
+                                                       ref_lambdas[i], fn ? &md : nullptr);
+        ee = r.eig_err;
+        if (fn) {
+          l2 = r.l2_err;
+          h1 = r.h1_err;
+        }
+      }
+      if (eig_err) eig_err[o] = ee;
+      if (l2_err) l2_err[o] = l2;
+      if (h1_err) h1_err[o] = h1;
+    }
+  };
+  std::vector<double> lam = mlg::coarse_eigensolve(c, 1, nev, u);
+  record(1, lam);
+  if (matched) matched[0] = 1;
+  if (timings) std::memset(&timings[0], 0, sizeof(mlg_step_timings));
+  for (int k = 1; k < nlev; ++k) {
+    reset_kernel_stats(c);
+    const mlg::StepResult r = mlg::correction_step(c, k, k + 1, nev, lam.data(), u.get(), u2);
+    std::swap(u, u2);
+    lam = r.lambdas;
+    if (matched) matched[k] = r.matched ? 1 : 0;
+    if (timings) fill_timings(&timings[k], r.times, c);
+    record(k + 1, lam);
+  }
+  const mlg::Level& L = c.level(nlev);
+  if (d_final_coeffs) mlg::deinterleave(c, L, nr, nev, nullptr, u.get(), 1, d_final_coeffs);
+  if (final_coeffs) {
+    mlg::DevBuf<double> out(L.nint() * nev);
+    mlg::deinterleave(c, L, nr, nev, nullptr, u.get(), 1, out.get());
+    out.download(final_coeffs, L.nint() * nev, c.stream);
+  }
+  c.sync();
 }
 
 }  // namespace
@@ -476,32 +558,47 @@ int mlg_multilevel_correction(mlg_ctx* ctx, int last_level, double* lambdas,
                               double* final_coeffs, double* d_final_coeffs, int* matched,
                               mlg_step_timings* timings) {
   return guarded([&] {
+    multilevel_impl(ctx, last_level, 0, nullptr, nullptr, lambdas, nullptr, nullptr, nullptr,
+                    final_coeffs, d_final_coeffs, matched, timings);
+  });
+}
+
+int mlg_multilevel_correction_refs(mlg_ctx* ctx, int last_level, int n_refs,
+                                   const double* ref_lambdas, const mlg_exact_mode* ref_modes,
+                                   double* lambdas, double* eig_err, double* l2_err,
+                                   double* h1_err, double* final_coeffs, int* matched,
+                                   mlg_step_timings* timings) {
+  return guarded([&] {
+    multilevel_impl(ctx, last_level, n_refs, ref_lambdas, ref_modes, lambdas, eig_err, l2_err,
+                    h1_err, final_coeffs, nullptr, matched, timings);
+  });
+}
+
+int mlg_make_reference(int example, int nev, const double* domain, double* lambdas,
+                       mlg_exact_mode* modes) {
+  return guarded([&] {
+    const mlg::ReferenceSet r = mlg::make_reference(example, nev, domain);
+    for (int i = 0; i < nev; ++i) {
+      if (lambdas) lambdas[i] = r.lambdas[static_cast<std::size_t>(i)];
+      if (modes) modes[i] = to_c(r.modes[static_cast<std::size_t>(i)]);
+    }
+  });
+}
+
+int mlg_compute_errors(mlg_ctx* ctx, int level, const double* coeffs_full, double lambda_h,
+                       double lambda_ref, const mlg_exact_mode* reference,
+                       mlg_error_report* out) {
+  return guarded([&] {
     mlg::Ctx& c = C(ctx);
-    const int nlev = last_level > 0 ? last_level : c.cfg.n_levels;
-    const int nev = c.cfg.nev;
-    const int nr = mlg::nr_for(nev);
-    mlg::DevBuf<double> u, u2;
-    std::vector<double> lam = mlg::coarse_eigensolve(c, 1, nev, u);
-    std::copy(lam.begin(), lam.end(), lambdas);
-    if (matched) matched[0] = 1;
-    if (timings) std::memset(&timings[0], 0, sizeof(mlg_step_timings));
-    for (int k = 1; k < nlev; ++k) {
-      reset_kernel_stats(c);
-      const mlg::StepResult r = mlg::correction_step(c, k, k + 1, nev, lam.data(), u.get(), u2);
-      std::swap(u, u2);
-      lam = r.lambdas;
-      std::copy(lam.begin(), lam.end(), lambdas + static_cast<std::size_t>(k) * nev);
-      if (matched) matched[k] = r.matched ? 1 : 0;
-      if (timings) fill_timings(&timings[k], r.times, c);
-    }
-    const mlg::Level& L = c.level(nlev);
-    if (d_final_coeffs) mlg::deinterleave(c, L, nr, nev, nullptr, u.get(), 1, d_final_coeffs);
-    if (final_coeffs) {
-      mlg::DevBuf<double> out(L.nint() * nev);
-      mlg::deinterleave(c, L, nr, nev, nullptr, u.get(), 1, out.get());
-      out.download(final_coeffs, L.nint() * nev, c.stream);
-    }
-    c.sync();
+    const mlg::Level& L = c.level(level);
+    if (!coeffs_full || !out) throw mlg::ConfigError("compute_errors: null argument");
+    mlg::DevBuf<double> d(static_cast<std::size_t>(L.ndofs()));
+    d.upload(coeffs_full, static_cast<std::size_t>(L.ndofs()), c.stream);
+    mlg::ExactMode md;
+    if (reference) md = from_c(*reference);
+    const mlg::ErrorReport r = mlg::compute_errors(c, L, d.get(), 1, 0, lambda_h, lambda_ref,
+                                                   reference ? &md : nullptr);
+    *out = {r.eig_err, r.l2_err, r.h1_err};
   });
 }
 

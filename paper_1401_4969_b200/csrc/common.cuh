@@ -34,6 +34,9 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     throw CudaError(std::string("CUDA error in ") + what + " (" + file + ":" +
                     std::to_string(line) + "): " + cudaGetErrorString(e));
 }
+// Per-thread message of the last failed C-ABI call (mlg_last_error, capi.cu).
+std::string& last_error_slot();
+
 // Process-wide count of this library's kernel launches (bench evidence).
 inline std::atomic<long long>& launch_counter() {
   static std::atomic<long long> n{0};

@@ -527,9 +527,8 @@ void validate_config(const Config& cfg) {  // corrector.cpp:76-88
   if (cfg.workers < 1) throw ConfigError("workers must be at least 1");
   if (cfg.example != 0 && cfg.example != 1)
     throw ConfigError("unknown example id (expected laplace or variable)");
-  // Scope of the B200 path: P1, constant Laplace coefficients.
+  // Scope of the B200 path: P1 elements (Laplace or variable field).
   if (cfg.degree != 1) throw ConfigError("degree 2 (P2) is not on the B200 path");
-  if (cfg.example != 0) throw ConfigError("the variable-coefficient example is not on the B200 path");
 }
 
 static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-121

@@ -45,7 +45,7 @@ struct Config {
   int n_levels = 5;
   int degree = 1;
   int nev = 5;
-  int example = 0;  // 0 laplace (1 variable: not on this path)
+  int example = 0;  // 0 laplace, 1 variable (CoefficientField, fespace.cpp:105-123)
   int workers = 1;
   double cg_tol = 1e-10;
   int deterministic = 1;

@@ -65,13 +65,14 @@ def digests(n0, levels, m, delta):
     return out
 
 
-def multilevel(name, domain, H, delta, m, levels, nev, workers=8, save_vec=None):
+def multilevel(name, domain, H, delta, m, levels, nev, workers=8, save_vec=None, example=0):
     t = time.time()
     h = ref.RefHierarchy(domain=domain, H=H, delta=delta, m=m, n_levels=levels, nev=nev,
-                         workers=workers)
+                         workers=workers, example=example)
     lam, co, matched, times = h.multilevel(levels, nev)
     out = {
-        "config": dict(domain=domain, H=H, delta=delta, m=m, n_levels=levels, nev=nev),
+        "config": dict(domain=domain, H=H, delta=delta, m=m, n_levels=levels, nev=nev,
+                       example=["laplace", "variable"][example]),
         "lambdas": lam.tolist(),
         "matched": matched.tolist(),
         "projections": projections(co),
@@ -82,6 +83,22 @@ def multilevel(name, domain, H, delta, m, levels, nev, workers=8, save_vec=None)
         np.save(OUT / save_vec, co)
     h.close()
     print(name, out["lambdas"][-1], f"{out['seconds']:.1f}s", flush=True)
+    return out
+
+
+def variable_values():
+    """Variable-field operator values at (-1,1)^2, H=0.25, level 3: exact digests
+    (for the record: exp() differs between libms, so consumers compare values to
+    a few ulp) and the sums of |values| with the row_ptr/cols digests."""
+    h = ref.RefHierarchy(domain=SQUARE, H=0.25, delta=0.25, m=4, n_levels=3, nev=1, example=1)
+    h.extend_to(3)
+    out = {}
+    for form in ("stiffness", "mass"):
+        rp, cols, v = h.csr(3, form)
+        out[form] = {"row_ptr": ref.fnv1a64(rp), "cols": ref.fnv1a64(cols),
+                     "values": ref.fnv1a64(v), "abs_sum": float(np.abs(v).sum()),
+                     "diag_head": v[rp[:-1]][:16].tolist()}
+    h.close()
     return out
 
 
@@ -138,6 +155,18 @@ def main():
         if name not in g["multilevel"]:
             g["multilevel"][name] = multilevel(name, dom, H, d, m, L, nev, save_vec=vec)
             path.write_text(json.dumps(g, indent=1))
+    # CoefficientField::variable (fespace.cpp:114-123), the reference's Example 2
+    var_runs = {
+        "variable_square_L4_m4_nev3": (SQUARE, 0.25, 0.25, 4, 4, 3, "variable_L4_u.npy"),
+        "variable_square_L6_m16_nev2": (SQUARE, 0.125, 0.125, 16, 6, 2, None),
+    }
+    for name, (dom, H, d, m, L, nev, vec) in var_runs.items():
+        if name not in g["multilevel"]:
+            g["multilevel"][name] = multilevel(name, dom, H, d, m, L, nev, save_vec=vec,
+                                               example=1)
+            path.write_text(json.dumps(g, indent=1))
+    if "variable_values" not in g:
+        g["variable_values"] = variable_values()
     if "cg" not in g:
         g["cg"] = cg_iterations()
     if args.big and "32_7" not in g["digests"]:

@@ -42,3 +42,47 @@ def test_cpp_driver_config_error_exit_code():
     out = subprocess.run([str(DRIVER), "0", "1", "0", "1", "0.3", "0.1", "4", "2", "1"],
                          capture_output=True, text=True, timeout=120)
     assert out.returncode == 2 and "does not divide" in out.stderr
+
+
+GOOD_CFG = """{
+  "domain": {"x_min": -1.0, "x_max": 1.0, "y_min": -1.0, "y_max": 1.0},
+  "H": 0.5, "delta": 0.5, "m": 1, "n_levels": 3, "degree": 1, "nev": 2,
+  "example": "laplace", "cg_tol": 1e-10, "workers": 1, "deterministic": true
+}"""
+
+
+@pytest.mark.gpu
+def test_cpp_cli_run_table_vtk(tmp_path, oracle_ref):
+    """`mlg_run run/table/export-vtk` (the reference CLI's subcommands,
+    mleig_main.cpp:13-71) through the C++ header: CSV rows agree with the
+    reference's run_experiment, the table is the reference's printer output."""
+    if not DRIVER.exists():
+        from paper_1401_4969_b200 import _build
+        _build.build_driver()
+    cfg = tmp_path / "c.json"
+    cfg.write_text(GOOD_CFG)
+    out = subprocess.run([str(DRIVER), "run", str(cfg), "-o", str(tmp_path / "r.csv")],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    ref_csv = tmp_path / "ref.csv"
+    oracle_ref.run_experiment(ref_csv, domain=(-1.0, 1.0, -1.0, 1.0), H=0.5, delta=0.5, m=1,
+                              n_levels=3, nev=2)
+    a = (tmp_path / "r.csv").read_text().splitlines()
+    b = ref_csv.read_text().splitlines()
+    assert a[0] == b[0] and len(a) == len(b)
+    for la, lb in zip(a[1:], b[1:]):
+        fa, fb = la.split(","), lb.split(",")
+        assert fa[:4] == fb[:4]
+        assert abs(float(fa[4]) - float(fb[4])) <= 1e-10 * float(fb[4])
+    t = subprocess.run([str(DRIVER), "table", str(tmp_path / "r.csv")], capture_output=True,
+                       text=True, timeout=60)
+    assert t.returncode == 0 and t.stdout.startswith("eigenvalue 1:")
+    assert t.stdout.splitlines()[1] == oracle_ref.print_table(ref_csv).splitlines()[1]
+    v = subprocess.run([str(DRIVER), "export-vtk", str(cfg), "-o", str(tmp_path / "vtk")],
+                       capture_output=True, text=True, timeout=300)
+    assert v.returncode == 0, v.stderr
+    assert (tmp_path / "vtk" / "eigenfunctions.vtk").read_text().startswith(
+        "# vtk DataFile Version 3.0")
+    bad = subprocess.run([str(DRIVER), "run", "/nonexistent.json", "-o", "x.csv"],
+                         capture_output=True, text=True, timeout=60)
+    assert bad.returncode == 4
