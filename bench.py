@@ -2,7 +2,7 @@
 """Benchmark of the B200 correction step (BASELINE.json metric: fine-grid DOF/s
 per correction step; local-solve SpMV HBM GB/s vs B200 peak).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c4|c5]
     python bench.py --impl reference ...        # the reference's CPU path (oracle/_ref)
 
 A "step" is one correction step L-1 -> L (one_correction_step,
@@ -40,6 +40,12 @@ WORKLOADS = {
                     "32x32 coarse squares, 7 levels (4096^2 cells), 8x8 overlapping subdomains, "
                     "delta=1/32, nev=4; step level 6 -> 7",
                H=1 / 32, delta=1 / 32, m=64, n_levels=7, nev=4),
+    "c4": dict(desc="config 4 (reference-valid partition m=16): unit square, "
+                    "-div(a grad u) + c u = lambda u, a = 1 + 0.5 sin(2 pi k1 x) sin(2 pi k2 y), "
+                    "c = 1 + x^2 + y^2 at centroids, (k1,k2) = (4,2) from seed 0, P1 FP64, "
+                    "16x16 coarse squares, 7 levels (2048^2 cells), 4x4 overlapping subdomains, "
+                    "delta=1/16, nev=1; step level 6 -> 7 (no reference code path)",
+               H=1 / 16, delta=1 / 16, m=16, n_levels=7, nev=1, example="reaction", seed=0),
 }
 FALLBACK_HBM = 6650.0
 
@@ -185,6 +191,10 @@ def run_reference(args, ws, rank):
         return
     wl = WORKLOADS[args.workload]
     cores = os.cpu_count() or 1
+    if wl.get("example", "laplace") == "reaction":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no code path "
+                          "for config 4's reaction/centroid-coefficient field"}))
+        return
     try:
         from oracle import ref
         if not ref.available():
@@ -215,6 +225,13 @@ def run_reference(args, ws, rank):
                               "aug": statistics.mean(s[2] for s in r["splits"]),
                               "level_build": r["build_s"], "region_systems": r["regions_s"]},
     }
+    if extra4:
+        line["config4_workload"] = {
+            "workload": WORKLOADS["c4"]["desc"], "value": extra4["value"], "unit": "DOF/s",
+            "ms_per_step": extra4["ms_per_step"], "n_interior": extra4["n_int"],
+            "level_build_s": extra4["build_s"], "timings": extra4["timings"],
+            "roofline": extra4.get("roofline"), "lambdas": extra4["lam"],
+            "clocks": extra4["clocks"]}
     print(json.dumps(line), flush=True)
 
 
@@ -232,7 +249,8 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cfg = mlg.RunConfig(domain=mlg.DomainRect(0.0, 1.0, 0.0, 1.0), H=wl["H"], delta=wl["delta"],
-                        m=wl["m"], n_levels=L, nev=nev, cg_tol=1e-10, device=local)
+                        m=wl["m"], n_levels=L, nev=nev, cg_tol=1e-10, device=local,
+                        example=wl.get("example", "laplace"), seed=wl.get("seed", 0))
     hy = mlg.Hierarchy(cfg)
     t0 = time.time()
     hy.extend_to(L - 1)
@@ -336,7 +354,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-north-star", action="store_true",
-                    help="skip the extra config-5 (4096^2) measurement")
+                    help="skip the extra config-5 (4096^2) and config-4 measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
@@ -345,9 +363,11 @@ def main():
         return
     wl = WORKLOADS[args.workload]
     res = run_ours(args, ws, rank, local, args.workload, args.steps, args.warmup)
-    extra = None
+    extra = extra4 = None
     if not args.no_north_star and args.workload != "c5":
         extra = run_ours(args, ws, rank, local, "c5", steps=2, warmup=1, with_e2e=False)
+    if not args.no_north_star and args.workload != "c4":
+        extra4 = run_ours(args, ws, rank, local, "c4", steps=2, warmup=1, with_e2e=False)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -386,6 +406,13 @@ def main():
             "level_build_s": extra["build_s"], "timings": extra["timings"],
             "roofline": extra.get("roofline"), "lambdas": extra["lam"],
             "clocks": extra["clocks"], "spmv_microbench": extra["spmv_microbench"]}
+    if extra4:
+        line["config4_workload"] = {
+            "workload": WORKLOADS["c4"]["desc"], "value": extra4["value"], "unit": "DOF/s",
+            "ms_per_step": extra4["ms_per_step"], "n_interior": extra4["n_int"],
+            "level_build_s": extra4["build_s"], "timings": extra4["timings"],
+            "roofline": extra4.get("roofline"), "lambdas": extra4["lam"],
+            "clocks": extra4["clocks"]}
     print(json.dumps(line), flush=True)
 
 

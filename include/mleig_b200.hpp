@@ -69,6 +69,7 @@ struct RunConfig {  // corrector.hpp:21-33
   int workers = 1;
   bool deterministic = true;
   int device = 0;
+  unsigned long long seed = 0;  // example "reaction" (BASELINE config 4)
 };
 
 struct SolveReport {  // sparse.hpp:103-107
@@ -123,7 +124,11 @@ inline mlg_config to_c(const RunConfig& config) {
   c.n_levels = config.n_levels;
   c.degree = config.degree;
   c.nev = config.nev;
-  c.example = config.example == "laplace" ? 0 : (config.example == "variable" ? 1 : -1);
+  c.example = config.example == "laplace"    ? 0
+              : config.example == "variable" ? 1
+              : config.example == "reaction" ? 2
+                                             : -1;
+  c.seed = config.seed;
   if (c.example < 0)
     throw ConfigError("unknown example id \"" + config.example +
                       "\" (expected laplace or variable)");
@@ -143,7 +148,8 @@ inline RunConfig from_c(const mlg_config& c) {
   r.n_levels = c.n_levels;
   r.degree = c.degree;
   r.nev = c.nev;
-  r.example = c.example == 1 ? "variable" : "laplace";
+  r.example = c.example == 2 ? "reaction" : (c.example == 1 ? "variable" : "laplace");
+  r.seed = c.seed;
   r.cg_tol = c.cg_tol;
   r.workers = c.workers;
   r.deterministic = c.deterministic != 0;
@@ -302,6 +308,7 @@ struct ReferenceSet {  // corrector.hpp
 inline int example_id(const std::string& example) {
   if (example == "laplace") return 0;
   if (example == "variable") return 1;
+  if (example == "reaction") return 2;
   throw ConfigError("no reference data for example \"" + example + "\"");
 }
 

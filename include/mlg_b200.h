@@ -41,7 +41,11 @@ extern "C" {
 #define MLG_ERR_IO 4     /* mleig::IoError,     errors.hpp:20-22 */
 #define MLG_ERR_CUDA 5
 
-/* RunConfig (corrector.hpp:21-33). example: 0 = "laplace", 1 = "variable". */
+/* RunConfig (corrector.hpp:21-33). example: 0 = "laplace", 1 = "variable"
+ * (CoefficientField, fespace.cpp:105-123), 2 = "reaction": the B200 extension
+ * for BASELINE config 4 (no reference code path), -div(a grad u) + c u = lambda u
+ * with a = 1 + 0.5 sin(2 pi k1 x) sin(2 pi k2 y), c = 1 + x^2 + y^2 evaluated
+ * at triangle centroids, (k1, k2) in {1..4}^2 drawn from `seed` by splitmix64. */
 typedef struct mlg_config {
   double x_min, x_max, y_min, y_max; /* DomainRect (mesh.hpp:22-27) */
   double H;                          /* coarse mesh size */
@@ -55,6 +59,7 @@ typedef struct mlg_config {
   double cg_tol;
   int deterministic;
   int device; /* CUDA device ordinal of the context (B200-specific) */
+  uint64_t seed; /* example 2 only: coefficient seed */
 } mlg_config;
 
 typedef struct mlg_ctx mlg_ctx;

@@ -209,11 +209,43 @@ def local_matrices_variable(mesh):
     return KA, KM
 
 
-def local_matrices(mesh, example="laplace"):
+def reaction_modes(seed):
+    """BASELINE config 4: (k1, k2) = 1 + (splitmix64 outputs 1 and 2 of seed) >> 62."""
+    M64 = 0xFFFFFFFFFFFFFFFF
+    out = []
+    for _ in range(2):
+        seed = (seed + 0x9E3779B97F4A7C15) & M64
+        z = seed
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+        z ^= z >> 31
+        out.append(1 + (z >> 62))
+    return tuple(out)
+
+
+def local_matrices_reaction(mesh, seed):
+    """BASELINE config 4 (no reference code path; the B200 definition in
+    csrc/assemble.cu): -div(a grad u) + c u with a = 1 + 0.5 sin(2 pi k1 x)
+    sin(2 pi k2 y), c = 1 + x^2 + y^2 at the centroid; element stiffness
+    a*K + c*M from the Laplace K and M, element mass M."""
+    KA, KM = local_matrices(mesh, "laplace")
+    k1, k2 = reaction_modes(seed)
+    v = mesh.vertices[mesh.triangles]
+    xc = (v[:, 0, 0] + v[:, 1, 0] + v[:, 2, 0]) / 3.0
+    yc = (v[:, 0, 1] + v[:, 1, 1] + v[:, 2, 1]) / 3.0
+    two_pi = 6.283185307179586476925286766559
+    ac = 1.0 + 0.5 * np.sin(two_pi * k1 * xc) * np.sin(two_pi * k2 * yc)
+    cc = 1.0 + xc * xc + yc * yc
+    return ac[:, None, None] * KA + cc[:, None, None] * KM, KM
+
+
+def local_matrices(mesh, example="laplace", seed=0):
     """Element stiffness and mass, P1, Laplace field, 3-point rule, in the exact
     operation order of local_matrix/element_geometry (fespace.cpp:169-217)."""
     if example == "variable":
         return local_matrices_variable(mesh)
+    if example == "reaction":
+        return local_matrices_reaction(mesh, seed)
     v = mesh.vertices[mesh.triangles]                            # [T,3,2]
     x0, y0, x1, y1, x2, y2 = (v[:, 0, 0], v[:, 0, 1], v[:, 1, 0], v[:, 1, 1], v[:, 2, 0],
                               v[:, 2, 1])
@@ -263,8 +295,8 @@ def from_upper_triplets(n, rows, cols, vals):  # sparse.cpp:24-61
     return np.cumsum(row_ptr).astype(np.int32), fc.astype(np.int32), fv
 
 
-def assemble(space, example="laplace"):  # assemble_form fespace.cpp:314-341, both forms
-    KA, KM = local_matrices(space.mesh, example)
+def assemble(space, example="laplace", seed=0):  # assemble_form fespace.cpp:314-341
+    KA, KM = local_matrices(space.mesh, example, seed)
     iu, ju = np.triu_indices(3)                                  # i<=j, row-major order
     gi, gj = space.connectivity[:, iu], space.connectivity[:, ju]
     rows = np.minimum(gi, gj).reshape(-1).astype(np.int64)
@@ -502,15 +534,15 @@ class Level:
 
 class Hierarchy:  # corrector.cpp:111-181
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), H=0.25, delta=0.1, m=4, n_levels=5,
-                 nev=5, cg_tol=1e-10, example="laplace"):
+                 nev=5, cg_tol=1e-10, example="laplace", seed=0):
         self.n_levels, self.nev, self.cg_tol = n_levels, nev, cg_tol
-        self.example = example
+        self.example, self.seed = example, seed
         mesh = build_structured_mesh(domain, H)
         cell = mesh.dx
         dc = max(1, int(np.ceil(delta / cell - 1e-9)))         # corrector.cpp:117-121
         self.part = build_partition(mesh, m, dc * cell)
         sp0 = build_space(mesh)
-        self.levels = [Level(mesh, sp0, *assemble(sp0, example))]
+        self.levels = [Level(mesh, sp0, *assemble(sp0, example, seed))]
         self._dense = None
 
     def extend_to(self, level):  # corrector.cpp:131-146
@@ -518,7 +550,7 @@ class Hierarchy:  # corrector.cpp:111-181
             prev = self.levels[-1]
             mesh = refine_regular(prev.mesh)
             s = build_space(mesh)
-            self.levels.append(Level(mesh, s, *assemble(s, self.example),
+            self.levels.append(Level(mesh, s, *assemble(s, self.example, self.seed),
                                      prolongation(prev.space, s)))
 
     def prolong(self, full, a, b):  # corrector.cpp:158-163

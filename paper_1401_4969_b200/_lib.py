@@ -48,6 +48,7 @@ class MlgConfig(C.Structure):
         ("m", C.c_int), ("n_levels", C.c_int), ("degree", C.c_int),
         ("nev", C.c_int), ("example", C.c_int), ("workers", C.c_int),
         ("cg_tol", C.c_double), ("deterministic", C.c_int), ("device", C.c_int),
+        ("seed", C.c_uint64),
     ]
 
 

@@ -53,13 +53,14 @@ class RunConfig:  # corrector.hpp:21-33
     workers: int = 1
     deterministic: bool = True
     device: int = 0  # CUDA device of the context (B200-specific)
+    seed: int = 0    # example "reaction" (BASELINE config 4): draws (k1, k2)
 
     def to_c(self) -> MlgConfig:
-        ex = {"laplace": 0, "variable": 1}.get(self.example, -1)
+        ex = {"laplace": 0, "variable": 1, "reaction": 2}.get(self.example, -1)
         return MlgConfig(self.domain.x_min, self.domain.x_max, self.domain.y_min,
                          self.domain.y_max, self.H, self.delta, self.m, self.n_levels,
                          self.degree, self.nev, ex, self.workers, self.cg_tol,
-                         int(self.deterministic), self.device)
+                         int(self.deterministic), self.device, self.seed)
 
 
 @dataclass

@@ -71,7 +71,25 @@ struct LevelGeom {
   int nx, ny;
   double x0, y0, dx, dy;
   const unsigned* geo;
+  int k1 = 0, k2 = 0;  // example 2 (reaction) modes
 };
+
+// Example 2 (BASELINE config 4, no reference code path): piecewise-constant
+// coefficients at the centroid, a = 1 + 0.5 sin(2 pi k1 x) sin(2 pi k2 y),
+// c = 1 + x^2 + y^2; element stiffness a*K + c*M (K, M the P1 Laplace
+// stiffness and mass of local_entry), element mass M.  The tests' numpy restatement
+// restates the same operation sequence.
+__device__ __forceinline__ void reaction_entry(double v0x, double v0y, double v1x, double v1y,
+                                               double v2x, double v2y, int k1, int k2,
+                                               double* a_io, double m) {
+  const double kTwoPi = 6.283185307179586476925286766559;
+  const double xc = xdiv(xadd(xadd(v0x, v1x), v2x), 3.0);
+  const double yc = xdiv(xadd(xadd(v0y, v1y), v2y), 3.0);
+  const double ac = xadd(1.0, xmul(xmul(0.5, sin(xmul(xmul(kTwoPi, k1), xc))),
+                                   sin(xmul(xmul(kTwoPi, k2), yc))));
+  const double cc = xadd(xadd(1.0, xmul(xc, xc)), xmul(yc, yc));
+  *a_io = xadd(xmul(ac, *a_io), xmul(cc, m));
+}
 
 // Canonical vertex k of the L/U triangle of cell (cx,cy):
 //   L: (cx,cy), (cx+1,cy), (cx+1,cy+1)     U: (cx,cy), (cx+1,cy+1), (cx,cy+1)
@@ -90,6 +108,7 @@ __device__ __forceinline__ void canon_vertex(int cx, int cy, int upper, int k, i
 
 // Contribution of triangle (cell, upper) to the pair of canonical vertices
 // (kd, kn) (kd == kn for a diagonal entry).
+template <int EX>
 __device__ __forceinline__ bool contribution(const LevelGeom& G, int cx, int cy, int upper,
                                              int kd, int kn, Contrib* out) {
   if (cx < 0 || cy < 0 || cx >= G.nx || cy >= G.ny) return false;
@@ -106,6 +125,8 @@ __device__ __forceinline__ bool contribution(const LevelGeom& G, int cx, int cy,
   const int ld = (kd - rot + 3) % 3, ln = (kn - rot + 3) % 3;
   local_entry(vx[0], vy[0], vx[1], vy[1], vx[2], vy[2], min(ld, ln), max(ld, ln), &out->a,
               &out->m);
+  if (EX == 2)
+    reaction_entry(vx[0], vy[0], vx[1], vy[1], vx[2], vy[2], G.k1, G.k2, &out->a, out->m);
   out->e = code >> 2;
   return true;
 }
@@ -261,6 +282,7 @@ __global__ void __launch_bounds__(kBlock) k_assemble_var(LevelGeom G, Stencil* s
   dinv[d] = 1.0 / A.c;
 }
 
+template <int EX>
 __global__ void __launch_bounds__(kBlock) k_assemble(LevelGeom G, Stencil* stA, Stencil* stM,
                                                      double* dinv) {
   const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
@@ -272,29 +294,29 @@ __global__ void __launch_bounds__(kBlock) k_assemble(LevelGeom G, Stencil* stA, 
   Stencil A{0.0, 0.0, 0.0, 0.0}, M{0.0, 0.0, 0.0, 0.0};
   // diagonal: the six triangles around (ix,iy) with the dof's canonical index
   n = 0;
-  n += contribution(G, ix, iy, 0, 0, 0, c + n);
-  n += contribution(G, ix, iy, 1, 0, 0, c + n);
-  n += contribution(G, ix - 1, iy, 0, 1, 1, c + n);
-  n += contribution(G, ix, iy - 1, 1, 2, 2, c + n);
-  n += contribution(G, ix - 1, iy - 1, 0, 2, 2, c + n);
-  n += contribution(G, ix - 1, iy - 1, 1, 1, 1, c + n);
+  n += contribution<EX>(G, ix, iy, 0, 0, 0, c + n);
+  n += contribution<EX>(G, ix, iy, 1, 0, 0, c + n);
+  n += contribution<EX>(G, ix - 1, iy, 0, 1, 1, c + n);
+  n += contribution<EX>(G, ix, iy - 1, 1, 2, 2, c + n);
+  n += contribution<EX>(G, ix - 1, iy - 1, 0, 2, 2, c + n);
+  n += contribution<EX>(G, ix - 1, iy - 1, 1, 1, 1, c + n);
   ordered_sum<6>(c, n, &A.c, &M.c);
   if (ix < G.nx) {  // E: L(ix,iy) (0,1), U(ix,iy-1) (2,1)
     n = 0;
-    n += contribution(G, ix, iy, 0, 0, 1, c + n);
-    n += contribution(G, ix, iy - 1, 1, 2, 1, c + n);
+    n += contribution<EX>(G, ix, iy, 0, 0, 1, c + n);
+    n += contribution<EX>(G, ix, iy - 1, 1, 2, 1, c + n);
     ordered_sum<2>(c, n, &A.e, &M.e);
   }
   if (iy < G.ny) {  // N: U(ix,iy) (0,2), L(ix-1,iy) (1,2)
     n = 0;
-    n += contribution(G, ix, iy, 1, 0, 2, c + n);
-    n += contribution(G, ix - 1, iy, 0, 1, 2, c + n);
+    n += contribution<EX>(G, ix, iy, 1, 0, 2, c + n);
+    n += contribution<EX>(G, ix - 1, iy, 0, 1, 2, c + n);
     ordered_sum<2>(c, n, &A.n, &M.n);
   }
   if (ix < G.nx && iy < G.ny) {  // NE: L(ix,iy) (0,2), U(ix,iy) (0,1)
     n = 0;
-    n += contribution(G, ix, iy, 0, 0, 2, c + n);
-    n += contribution(G, ix, iy, 1, 0, 1, c + n);
+    n += contribution<EX>(G, ix, iy, 0, 0, 2, c + n);
+    n += contribution<EX>(G, ix, iy, 1, 0, 1, c + n);
     ordered_sum<2>(c, n, &A.ne, &M.ne);
   }
   stA[d] = A;
@@ -405,9 +427,13 @@ void assemble_level(Ctx& c, Level& L) {
     }
     k_assemble_var<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
                                                                   L.dinv.get());
+  } else if (c.cfg.example == 2) {
+    reaction_modes(c.cfg.seed, &G.k1, &G.k2);
+    k_assemble<2><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
+                                                                 L.dinv.get());
   } else {
-    k_assemble<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
-                                                              L.dinv.get());
+    k_assemble<0><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
+                                                                 L.dinv.get());
   }
   MLG_LAUNCH_CHECK();
   // Constant-coefficient detection for the CG fast path (MLG_GENERAL_STENCIL=1

@@ -204,6 +204,7 @@ int mlg_create(const mlg_config* cfg, mlg_ctx** out) {
     c.cg_tol = cfg->cg_tol;
     c.deterministic = cfg->deterministic;
     c.device = cfg->device;
+    c.seed = cfg->seed;
     auto h = std::make_unique<mlg_ctx>();
     h->c = std::make_unique<mlg::Ctx>(c);
     *out = h.release();

@@ -525,8 +525,8 @@ void validate_config(const Config& cfg) {  // corrector.cpp:76-88
   if (cfg.nev < 1) throw ConfigError("nev must be at least 1");
   if (!(cfg.cg_tol > 0.0)) throw ConfigError("cg_tol must be positive");
   if (cfg.workers < 1) throw ConfigError("workers must be at least 1");
-  if (cfg.example != 0 && cfg.example != 1)
-    throw ConfigError("unknown example id (expected laplace or variable)");
+  if (cfg.example < 0 || cfg.example > 2)
+    throw ConfigError("unknown example id (expected laplace, variable or reaction)");
   // Scope of the B200 path: P1 elements (Laplace or variable field).
   if (cfg.degree != 1) throw ConfigError("degree 2 (P2) is not on the B200 path");
 }

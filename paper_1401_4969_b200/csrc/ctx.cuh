@@ -45,12 +45,27 @@ struct Config {
   int n_levels = 5;
   int degree = 1;
   int nev = 5;
-  int example = 0;  // 0 laplace, 1 variable (CoefficientField, fespace.cpp:105-123)
+  int example = 0;  // 0 laplace, 1 variable (CoefficientField, fespace.cpp:105-123),
+                    // 2 reaction (BASELINE config 4, B200 extension)
   int workers = 1;
   double cg_tol = 1e-10;
   int deterministic = 1;
   int device = 0;
+  unsigned long long seed = 0;  // example 2
 };
+
+// Example 2 coefficients: (k1, k2) = 1 + (splitmix64 outputs 1, 2 of seed) >> 62.
+inline void reaction_modes(unsigned long long seed, int* k1, int* k2) {
+  auto next = [&seed]() {
+    seed += 0x9E3779B97F4A7C15ULL;
+    unsigned long long z = seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  };
+  *k1 = 1 + static_cast<int>(next() >> 62);
+  *k2 = 1 + static_cast<int>(next() >> 62);
+}
 
 struct IRect {
   int x0 = 0, y0 = 0, x1 = 0, y1 = 0;

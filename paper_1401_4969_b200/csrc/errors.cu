@@ -256,6 +256,7 @@ ReferenceSet make_reference(int example, int nev, const double* domain) {
     refs.modes.assign(static_cast<std::size_t>(nev), ExactMode{});
     return refs;
   }
+  if (example == 2) throw ConfigError("no reference data for example \"reaction\"");
   throw ConfigError("no reference data for example id " + std::to_string(example));
 }
 

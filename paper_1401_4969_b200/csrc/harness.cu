@@ -306,8 +306,8 @@ void validate(const mlg_config& c) {
   if (c.nev < 1) throw mlg::ConfigError("nev must be at least 1");
   if (!(c.cg_tol > 0.0)) throw mlg::ConfigError("cg_tol must be positive");
   if (c.workers < 1) throw mlg::ConfigError("workers must be at least 1");
-  if (c.example != 0 && c.example != 1)
-    throw mlg::ConfigError("unknown example id (expected laplace or variable)");
+  if (c.example < 0 || c.example > 2)
+    throw mlg::ConfigError("unknown example id (expected laplace, variable or reaction)");
 }
 
 mlg_config parse_json(const std::string& text) {
@@ -317,8 +317,13 @@ mlg_config parse_json(const std::string& text) {
   static const std::vector<std::string> keys = {"domain",  "H",       "delta",  "m",
                                                 "n_levels", "degree", "nev",    "example",
                                                 "cg_tol",   "workers", "deterministic"};
+  // "seed" is the one key beyond the reference's schema, accepted only with the
+  // B200 extension example "reaction" (BASELINE config 4).
+  const JVal* exv = field(j, "example");
+  const bool reaction = exv && exv->kind == JVal::Str && exv->s == "reaction";
   for (const auto& kv : j.obj)
-    if (std::find(keys.begin(), keys.end(), kv.first) == keys.end())
+    if (std::find(keys.begin(), keys.end(), kv.first) == keys.end() &&
+        !(reaction && kv.first == "seed"))
       throw mlg::ConfigError("unknown config field \"" + kv.first + "\"");
   for (const auto& k : keys)
     if (!field(j, k)) throw mlg::ConfigError("missing config field \"" + k + "\"");
@@ -348,6 +353,14 @@ mlg_config parse_json(const std::string& text) {
     c.example = 0;
   } else if (ex == "variable") {
     c.example = 1;
+  } else if (ex == "reaction") {
+    c.example = 2;
+    if (field(j, "seed")) {
+      const JVal* sv = field(j, "seed");
+      if (sv->kind != JVal::Int || sv->i < 0)
+        throw mlg::ConfigError("config field \"seed\" must be a nonnegative integer");
+      c.seed = static_cast<uint64_t>(sv->i);
+    }
   } else {
     validate(c);  // the reference reports field errors first, then the example
     throw mlg::ConfigError("unknown example id \"" + ex + "\" (expected laplace or variable)");

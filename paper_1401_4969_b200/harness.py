@@ -16,14 +16,14 @@ from ._lib import (MlgConfig, MlgErrorReport, MlgExactMode, MlgReportRow, MlgSte
 from .corrector import (DomainRect, EigenPair, Hierarchy, LevelTrace, RunConfig, StepTimings,
                         _dp, _f64, _ip)
 
-EXAMPLES = ("laplace", "variable")
+EXAMPLES = ("laplace", "variable", "reaction")
 
 
 def _config_from_c(c: MlgConfig) -> RunConfig:
     return RunConfig(domain=DomainRect(c.x_min, c.x_max, c.y_min, c.y_max), H=c.H,
                      delta=c.delta, m=c.m, n_levels=c.n_levels, degree=c.degree, nev=c.nev,
                      example=EXAMPLES[c.example], cg_tol=c.cg_tol, workers=c.workers,
-                     deterministic=bool(c.deterministic), device=c.device)
+                     deterministic=bool(c.deterministic), device=c.device, seed=c.seed)
 
 
 def parse_config_json(text: str) -> RunConfig:  # harness.cpp:58-102

@@ -86,6 +86,19 @@ def multilevel(name, domain, H, delta, m, levels, nev, workers=8, save_vec=None,
     return out
 
 
+def reaction_run(domain, H, delta, m, levels, nev, seed):
+    from oracle import restate as R
+    t = time.time()
+    hy = R.Hierarchy(domain=domain, H=H, delta=delta, m=m, n_levels=levels, nev=nev,
+                     example="reaction", seed=seed)
+    lams, state = R.multilevel_correction(hy)
+    co = np.stack([v for _, v in state])
+    return {"config": dict(domain=domain, H=H, delta=delta, m=m, n_levels=levels, nev=nev,
+                           example="reaction", seed=seed, k=list(R.reaction_modes(seed))),
+            "lambdas": np.asarray(lams).tolist(), "projections": projections(co),
+            "generator": "oracle/restate.py", "seconds": time.time() - t}
+
+
 def variable_values():
     """Variable-field operator values at (-1,1)^2, H=0.25, level 3: exact digests
     (for the record: exp() differs between libms, so consumers compare values to
@@ -167,6 +180,17 @@ def main():
             path.write_text(json.dumps(g, indent=1))
     if "variable_values" not in g:
         g["variable_values"] = variable_values()
+    # Example "reaction" (BASELINE config 4): no reference code path, so these
+    # fixtures come from the numpy restatement (oracle/restate.py) -- parity
+    # unpinned against the reference, pinned against our own restatement.
+    g.setdefault("reaction", {})
+    for name, (dom, H, d, m, L, nev, seed) in {
+            "unit8_L4_m4_nev2_seed0": (UNIT, 1 / 8, 1 / 8, 4, 4, 2, 0),
+            "unit8_L3_m4_nev1_seed3": (UNIT, 1 / 8, 1 / 8, 4, 3, 1, 3)}.items():
+        if name not in g["reaction"]:
+            g["reaction"][name] = reaction_run(dom, H, d, m, L, nev, seed)
+            print(name, g["reaction"][name]["lambdas"][-1], flush=True)
+            path.write_text(json.dumps(g, indent=1))
     if "cg" not in g:
         g["cg"] = cg_iterations()
     if args.big and "32_7" not in g["digests"]:

@@ -200,3 +200,16 @@ def test_print_table_identical(H, mlg, oracle_ref, ref_csv, tmp_path):
         H.print_table(str(bad))
     with pytest.raises(mlg.IoError, match="cannot open output file"):
         H.write_csv(H.ExperimentReport(None, []), "/nonexistent/dir/x.csv")
+
+
+def test_reaction_seed_key_only_with_reaction(H, mlg):
+    """"seed" is the one key beyond the reference's schema, accepted only for the
+    B200 extension example "reaction" (BASELINE config 4)."""
+    txt = GOOD.replace('"laplace"', '"reaction"').replace('"workers": 1', '"workers": 1, "seed": 5')
+    cfg = H.parse_config_json(txt)
+    assert cfg.example == "reaction" and cfg.seed == 5
+    assert H.parse_config_json(GOOD.replace('"laplace"', '"reaction"')).seed == 0
+    with pytest.raises(mlg.ConfigError, match='unknown config field "seed"'):
+        H.parse_config_json(GOOD.replace('"workers": 1', '"workers": 1, "seed": 5'))
+    with pytest.raises(mlg.ConfigError, match="seed"):
+        H.parse_config_json(txt.replace('"seed": 5', '"seed": -1'))
