@@ -12,6 +12,7 @@
 //   one_correction_step          corrector.cpp:336-412
 //   solve_interior_eigenproblem  sparse.cpp:326-355 (level-1 direct solve)
 #include <algorithm>
+#include <cfloat>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -458,6 +459,151 @@ __global__ void k_build_aug(int mc, int k, const int* keep, const double* cc, co
   out[idx] = v;
 }
 
+// ---- augmented eigenproblem with ONE candidate: arrowhead form ----------
+// corrector.cpp:256-334 solves the (mc+1) pencil [[A_cc, a],[a', a_uu]] vs
+// [[B_cc, b],[b', b_uu]] densely.  With the cached coarse spectrum
+// A_cc V = B_cc V Lam (V'B_cc V = I) and c = V'b, d = V'a, the B-orthogonal
+// change of basis x = [V (w_c - c x_u); x_u], x_u = w_u / sqrt(s_b) with the
+// Schur complement s_b = b_uu - c'c turns it into the standard symmetric
+// arrowhead problem [[Lam, e],[e', f]] w = mu w, e = (d - Lam c)/sqrt(s_b),
+// f = (a_uu - 2 c'd + c'Lam c)/s_b, whose eigenvalues below lam_0 are the roots
+// of the secular function g(mu) = f - mu - sum e_i^2 / (lam_i - mu) -- no dense
+// factorisation per step.  s_b is exactly the reference's dependence test
+// (b_uu - b'B_cc^{-1} b, corrector.cpp:285-292): below 1e-10^2 the candidate is
+// dropped and the coarse pair (lam_0, V_0) is the answer.  One CTA; root by
+// safeguarded Newton on g inside its bracket, block reductions in fixed order.
+constexpr int kArrowThreads = 1024;
+
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = a;
+    red[32 + warp] = b;
+  }
+  __syncthreads();
+  a = 0.0;
+  b = 0.0;
+  for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) {
+    a += red[k];
+    b += red[32 + k];
+  }
+}
+
+__global__ void __launch_bounds__(kArrowThreads) k_aug_arrow(
+    int mc, const double* lamc, const double* V, const double* a_cu, const double* b_cu,
+    const double* auu, const double* buu, double* work, double* out_lam, double* out_cp,
+    double* out_coef, int* out_flag) {
+  __shared__ double red[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double* c = work;
+  double* d = work + mc;
+  double* e = work + 2 * mc;
+  for (int i = warp; i < mc; i += nw) {  // c = V'b, d = V'a (column i of V is contiguous)
+    double sc = 0.0, sd = 0.0;
+    const double* vi = V + static_cast<long long>(i) * mc;
+    for (int j = lane; j < mc; j += 32) {
+      const double v = vi[j];
+      sc += v * b_cu[j];
+      sd += v * a_cu[j];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      sc += __shfl_xor_sync(0xffffffffu, sc, o);
+      sd += __shfl_xor_sync(0xffffffffu, sd, o);
+    }
+    if (lane == 0) {
+      c[i] = sc;
+      d[i] = sd;
+    }
+  }
+  __syncthreads();
+  double cc = 0.0, cd = 0.0, clc = 0.0, dummy = 0.0;
+  for (int i = tid; i < mc; i += blockDim.x) {
+    cc += c[i] * c[i];
+    cd += c[i] * d[i];
+    clc += lamc[i] * c[i] * c[i];
+  }
+  block_sum2(cc, cd, red);
+  block_sum2(clc, dummy, red);
+  const double s_b = buu[0] - cc;
+  if (!(sqrt(fmax(s_b, 0.0)) >= 1e-10)) {  // dropped: the coarse pair
+    for (int r = tid; r < mc; r += blockDim.x) out_cp[r] = V[r];
+    if (tid == 0) {
+      out_lam[0] = lamc[0];
+      out_coef[0] = 0.0;
+      *out_flag = 2;
+    }
+    return;
+  }
+  const double sq = sqrt(s_b);
+  const double f = (auu[0] - 2.0 * cd + clc) / s_b;
+  double ee = 0.0;
+  for (int i = tid; i < mc; i += blockDim.x) {
+    const double v = (d[i] - lamc[i] * c[i]) / sq;
+    e[i] = v;
+    ee += v * v;
+  }
+  block_sum2(ee, dummy, red);
+  __syncthreads();
+  // smallest root of g in (lo, lam_0); start from the 2x2 problem [[lam_0, e_0],[e_0, f]]
+  const double l0 = lamc[0], e0 = e[0];
+  double lo = fmin(l0, f) - sqrt(ee) - 1.0, hi = l0;
+  const double h = 0.5 * (l0 - f);
+  double mu = 0.5 * (l0 + f) - sqrt(h * h + e0 * e0);
+  if (!(mu > lo && mu < hi)) mu = 0.5 * (lo + hi);
+  for (int it = 0; it < 200; ++it) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = tid; i < mc; i += blockDim.x) {
+      const double t = e[i] / (lamc[i] - mu);
+      s1 += e[i] * t;
+      s2 += t * t;
+    }
+    block_sum2(s1, s2, red);
+    const double g = f - mu - s1, gp = -1.0 - s2;
+    if (g > 0.0)
+      lo = mu;
+    else if (g < 0.0)
+      hi = mu;
+    else
+      break;
+    double nx = mu - g / gp;
+    if (!(nx > lo && nx < hi)) nx = 0.5 * (lo + hi);
+    const bool done = fabs(nx - mu) <= 2.0 * DBL_EPSILON * fabs(mu) || !(hi - lo > 2.0 * DBL_EPSILON * fabs(hi));
+    mu = nx;
+    if (done) break;
+  }
+  // mu on (or within rounding of) the pole lam_0: deflated case, left to the dense path
+  if (!(l0 - mu > 8.0 * DBL_EPSILON * fabs(l0))) {
+    if (tid == 0) *out_flag = 1;
+    return;
+  }
+  // eigenvector w = [e_i / (mu - lam_i); 1] / ||.||, then back to the pencil's basis
+  double nn = 0.0;
+  for (int i = tid; i < mc; i += blockDim.x) {
+    const double t = e[i] / (mu - lamc[i]);
+    nn += t * t;
+  }
+  block_sum2(nn, dummy, red);
+  const double scale = 1.0 / sqrt(1.0 + nn);
+  const double xu = scale / sq;
+  for (int i = tid; i < mc; i += blockDim.x) d[i] = e[i] / (mu - lamc[i]) * scale - c[i] * xu;
+  __syncthreads();
+  for (int r = tid; r < mc; r += blockDim.x) {  // x_c = V t, V column-major
+    double acc = 0.0;
+    for (int i = 0; i < mc; ++i) acc += V[static_cast<long long>(i) * mc + r] * d[i];
+    out_cp[r] = acc;
+  }
+  if (tid == 0) {
+    out_lam[0] = mu;
+    out_coef[0] = xu;
+    *out_flag = 0;
+  }
+}
+
 #define NR_DISPATCH(nr, kernel, grid, ...)                                      \
   do {                                                                          \
     switch (nr) {                                                               \
@@ -679,6 +825,35 @@ void Ctx::ensure_coarse_dense() {
   coarse_ready = true;
 }
 
+void Ctx::ensure_coarse_spectrum() {
+  if (spectrum_ready) return;
+  ensure_coarse_dense();
+  Workspace& w = W(*this);
+  coarse_lam.alloc(static_cast<std::size_t>(mc));
+  coarse_vec.alloc(static_cast<std::size_t>(mc) * mc);
+  DevBuf<double> b(static_cast<std::size_t>(mc) * mc);
+  MLG_CUDA(cudaMemcpyAsync(coarse_vec.get(), coarse_a.get(), sizeof(double) * mc * mc,
+                           cudaMemcpyDeviceToDevice, stream));
+  MLG_CUDA(cudaMemcpyAsync(b.get(), coarse_b.get(), sizeof(double) * mc * mc,
+                           cudaMemcpyDeviceToDevice, stream));
+  int lwork = 0;
+  cusolverDnDsygvd_bufferSize(solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                              CUBLAS_FILL_MODE_LOWER, mc, coarse_vec.get(), mc, b.get(), mc,
+                              coarse_lam.get(), &lwork);
+  w.work.ensure(std::max(lwork, 1));
+  w.info.ensure(1);
+  if (cusolverDnDsygvd(solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                       CUBLAS_FILL_MODE_LOWER, mc, coarse_vec.get(), mc, b.get(), mc,
+                       coarse_lam.get(), w.work.get(), lwork,
+                       w.info.get()) != CUSOLVER_STATUS_SUCCESS)
+    throw CudaError("cusolverDnDsygvd failed to launch");
+  int info = 0;
+  w.info.download(&info, 1, stream);
+  sync();
+  if (info != 0) throw SolverError("coarse pencil eigensolve failed");
+  spectrum_ready = true;
+}
+
 // ---------------------------------------------------------------------------
 // building blocks
 // ---------------------------------------------------------------------------
@@ -738,6 +913,16 @@ std::vector<double> mdot(Ctx& c, int nr, const Level& L, const double* U, const 
   w.dots.download(out.data(), out.size(), c.stream);
   c.sync();
   return out;
+}
+
+// mdot into device memory (no host round trip): d_out[r*nr+s].
+void mdot_dev(Ctx& c, int nr, const Level& L, const double* U, const double* V, double* d_out) {
+  Workspace& w = W(c);
+  const int nb = 296;
+  w.part.ensure(static_cast<std::size_t>(nb) * nr * nr);
+  NR_DISPATCH(nr, k_mdot, nb, L.ndofs(), U, V, w.part.get());
+  k_mdot_final<<<1, 64, 0, c.stream>>>(nb, nr * nr, w.part.get(), d_out);
+  MLG_LAUNCH_CHECK();
 }
 
 void fix_sign_lanes(Ctx& c, int nr, const Level& L, double* v) {
@@ -1007,6 +1192,58 @@ int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const Lam& l
 // glued: full-lattice interleaved (nr lanes, first k_in used).  Output: sorted
 // lambdas; u_out = normalised, sign-fixed coefficients (interleaved, nr lanes).
 // ---------------------------------------------------------------------------
+// Expansion of the augmented eigenvectors (corrector.cpp:318-332): prolong the
+// coarse parts (device, [nev][mc]) through all levels, add coef x candidates,
+// M-normalise, fix_sign, stable sort by lambda.
+static std::vector<double> expand_augmented(Ctx& c, Level& F, int level, int nr, int nev, int k,
+                                            const double* d_cp, const std::vector<double>& lam_in,
+                                            const double* glued, DevBuf<double>& u_out) {
+  const Level& L0 = c.level(0);
+  Workspace& w = W(c);
+  const long long nd = F.ndofs();
+  DevBuf<double>& c0 = w.aug_c0;
+  c0.ensure(L0.ndofs() * nr);
+  NR_DISPATCH(nr, k_interleave, grid_for(L0.ndofs(), kB), L0.nx, L0.ny, nev, d_cp, 1, c0.get());
+  w.full.ensure(nd * nr);
+  prolong_chain(c, nr, c0.get(), 0, level, w.full.get());
+  NR_DISPATCH(nr, k_candidates, grid_for(nd, kB), nd, k, w.keep.get(), w.coef.get(), glued,
+              w.full.get());
+  w.mfull.ensure(nd * nr);
+  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), w.full.get(),
+              nullptr, w.mfull.get());
+  const auto q = mdot(c, nr, F, w.full.get(), w.mfull.get());
+  Lam s{};
+  for (int r = 0; r < 8; ++r) s.v[r] = 1.0;
+  for (int i = 0; i < nev; ++i) {
+    const double qi = q[i * nr + i];
+    if (qi <= 0.0) throw SolverError("augmented eigenvector with nonpositive mass norm");
+    s.v[i] = std::sqrt(qi);
+  }
+  NR_DISPATCH(nr, k_div_lanes, grid_for(nd, kB), nd, s, w.full.get());
+  fix_sign_lanes(c, nr, F, w.full.get());
+  // stable sort by lambda (corrector.cpp:331-332)
+  std::vector<int> order(nev);
+  for (int i = 0; i < nev; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return lam_in[a] < lam_in[b]; });
+  Lam perm{};
+  for (int r = 0; r < 8; ++r) perm.v[r] = r < nev ? order[r] : r;
+  u_out.ensure(nd * nr);
+  NR_DISPATCH(nr, k_permute_lanes, grid_for(nd, kB), nd, perm, w.full.get(), u_out.get());
+  std::vector<double> lam(nev);
+  for (int i = 0; i < nev; ++i) lam[i] = lam_in[order[i]];
+  c.sync();
+  return lam;
+}
+
+static bool arrow_enabled() {  // A/B hook: MLG_AUG=0/1/2 forces the dense cuSOLVER path
+  static const bool on = [] {
+    const char* e = std::getenv("MLG_AUG");
+    return e == nullptr || e[0] == '\0' || std::strcmp(e, "arrow") == 0;
+  }();
+  return on;
+}
+
 std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double* glued, int nev,
                               DevBuf<double>& u_out) {
   Level& F = c.level(level);
@@ -1019,15 +1256,43 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
   w.bu.ensure(nd * nr);
   NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), glued,
               w.au.get(), w.bu.get());
-  const auto a_uu = mdot(c, nr, F, glued, w.au.get());
-  const auto b_uu = mdot(c, nr, F, glued, w.bu.get());
   const double* a0 = restrict_chain(c, nr, w.au.get(), level, 0);
   const double* b0 = restrict_chain(c, nr, w.bu.get(), level, 1);
   w.a_cu.ensure(static_cast<std::size_t>(mc) * nr);
   w.b_cu.ensure(static_cast<std::size_t>(mc) * nr);
   NR_DISPATCH(nr, k_gather_coarse, grid_for(mc, kB), L0.nx, L0.ny, a0, w.a_cu.get());
   NR_DISPATCH(nr, k_gather_coarse, grid_for(mc, kB), L0.nx, L0.ny, b0, w.b_cu.get());
+  w.coef.ensure(64);
+  w.keep.ensure(8);
 
+  if (nev == 1 && k_in == 1 && nr == 1 && arrow_enabled()) {
+    c.ensure_coarse_spectrum();
+    w.dots.ensure(4);
+    mdot_dev(c, 1, F, glued, w.au.get(), w.dots.get());
+    mdot_dev(c, 1, F, glued, w.bu.get(), w.dots.get() + 1);
+    w.aug_ctmp.ensure(static_cast<std::size_t>(3) * mc);
+    w.aug_cp.ensure(static_cast<std::size_t>(mc));
+    w.aug_uu_a.ensure(2);
+    w.info.ensure(1);
+    MLG_CUDA(cudaMemsetAsync(w.coef.get(), 0, 64 * sizeof(double), c.stream));
+    const int zero = 0;
+    w.keep.upload(&zero, 1, c.stream);
+    k_aug_arrow<<<1, kArrowThreads, 0, c.stream>>>(
+        mc, c.coarse_lam.get(), c.coarse_vec.get(), w.a_cu.get(), w.b_cu.get(), w.dots.get(),
+        w.dots.get() + 1, w.aug_ctmp.get(), w.aug_uu_a.get(), w.aug_cp.get(), w.coef.get(),
+        w.info.get());
+    MLG_LAUNCH_CHECK();
+    double mu = 0.0;
+    int flag = 0;
+    w.aug_uu_a.download(&mu, 1, c.stream);
+    w.info.download(&flag, 1, c.stream);
+    c.sync();
+    if (flag != 1)  // 0: candidate kept, 2: dropped (coef 0); 1: deflated -> dense path
+      return expand_augmented(c, F, level, nr, 1, 1, w.aug_cp.get(), {mu}, glued, u_out);
+  }
+
+  const auto a_uu = mdot(c, nr, F, glued, w.au.get());
+  const auto b_uu = mdot(c, nr, F, glued, w.bu.get());
   // Dependence drop through the cached coarse Cholesky (corrector.cpp:285-292).
   std::vector<double> bcu(static_cast<std::size_t>(mc) * nr), csol(bcu.size());
   DevBuf<double>& ctmp = w.aug_ctmp;
@@ -1051,7 +1316,6 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
   if (nev < 1 || nev > dim)
     throw ConfigError("augmented eigenproblem smaller than the requested nev");
 
-  w.keep.ensure(8);
   w.keep.upload(keep.data(), keep.size(), c.stream);
   DevBuf<double>& uu_a = w.aug_uu_a;
   DevBuf<double>& uu_b = w.aug_uu_b;
@@ -1072,53 +1336,20 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
   // The reference's explicit LLT check on b_aug happens inside sygvd (info > n).
   const auto pairs = dense_gen_eigensolve_dev(c, dim, w.dense_a.get(), w.dense_b.get(), nev);
 
-  // Expansion: prolong the coarse part through all levels, add candidates.
   std::vector<double> coarse_part(static_cast<std::size_t>(mc) * nev);
   std::vector<double> coef(8 * 8, 0.0);
+  std::vector<double> lam(nev);
   for (int i = 0; i < nev; ++i) {
     std::copy(pairs[i].vec.begin(), pairs[i].vec.begin() + mc,
               coarse_part.begin() + static_cast<long>(i) * mc);
     for (int l = 0; l < k; ++l) coef[i * 8 + l] = pairs[i].vec[mc + l];
+    lam[i] = pairs[i].lambda;
   }
   DevBuf<double>& cp = w.aug_cp;
   cp.ensure(coarse_part.size());
   cp.upload(coarse_part.data(), coarse_part.size(), c.stream);
-  w.coef.ensure(64);
   w.coef.upload(coef.data(), 64, c.stream);
-  DevBuf<double>& c0 = w.aug_c0;
-  c0.ensure(L0.ndofs() * nr);
-  NR_DISPATCH(nr, k_interleave, grid_for(L0.ndofs(), kB), L0.nx, L0.ny, nev, cp.get(), 1,
-              c0.get());
-  w.full.ensure(nd * nr);
-  prolong_chain(c, nr, c0.get(), 0, level, w.full.get());
-  NR_DISPATCH(nr, k_candidates, grid_for(nd, kB), nd, k, w.keep.get(), w.coef.get(), glued,
-              w.full.get());
-  w.mfull.ensure(nd * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), w.full.get(),
-              nullptr, w.mfull.get());
-  const auto q = mdot(c, nr, F, w.full.get(), w.mfull.get());
-  Lam s{};
-  for (int r = 0; r < 8; ++r) s.v[r] = 1.0;
-  for (int i = 0; i < nev; ++i) {
-    const double qi = q[i * nr + i];
-    if (qi <= 0.0) throw SolverError("augmented eigenvector with nonpositive mass norm");
-    s.v[i] = std::sqrt(qi);
-  }
-  NR_DISPATCH(nr, k_div_lanes, grid_for(nd, kB), nd, s, w.full.get());
-  fix_sign_lanes(c, nr, F, w.full.get());
-  // stable sort by lambda (corrector.cpp:331-332)
-  std::vector<int> order(nev);
-  for (int i = 0; i < nev; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int a, int b) { return pairs[a].lambda < pairs[b].lambda; });
-  Lam perm{};
-  for (int r = 0; r < 8; ++r) perm.v[r] = r < nev ? order[r] : r;
-  u_out.ensure(nd * nr);
-  NR_DISPATCH(nr, k_permute_lanes, grid_for(nd, kB), nd, perm, w.full.get(), u_out.get());
-  std::vector<double> lam(nev);
-  for (int i = 0; i < nev; ++i) lam[i] = pairs[order[i]].lambda;
-  c.sync();
-  return lam;
+  return expand_augmented(c, F, level, nr, nev, k, cp.get(), lam, glued, u_out);
 }
 
 // ---------------------------------------------------------------------------

@@ -161,6 +161,11 @@ class Ctx {
   int mc = 0;
   bool coarse_ready = false;
   void ensure_coarse_dense();
+  // Spectrum of the coarse pencil A_cc V = B_cc V diag(lam), V'B_cc V = I
+  // (ascending), cached for the arrowhead form of the augmented problem.
+  DevBuf<double> coarse_lam, coarse_vec;
+  bool spectrum_ready = false;
+  void ensure_coarse_spectrum();
 
   // Scratch (grow-only) owned by the context.
   DevBuf<double> io_in, io_out, io_u_in, io_u_out;  // C-ABI step marshalling

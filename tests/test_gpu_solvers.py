@@ -195,3 +195,30 @@ def test_config_errors(mlg):
     with pytest.raises(mlg.ConfigError, match="next level"):
         st = mlg.CorrectionState(1, mlg.coarse_eigensolve(hy, 1, 1))
         mlg.one_correction_step(hy, st, 3)
+
+
+@pytest.mark.parametrize("case", ["candidate", "in_coarse_space", "unit8"])
+def test_augmented_single_candidate_arrowhead(mlg, oracle_ref, case):
+    """nev = 1: the device arrowhead/secular solve of the augmented pencil vs the
+    reference's dense generalized solve (corrector.cpp:256-334), including the
+    dependence drop when the candidate lies in V_H (corrector.cpp:285-292)."""
+    spec = UNIT8 if case == "unit8" else SMALL
+    L = 3
+    hy, rh = pair(mlg, oracle_ref, spec, L, 1)
+    rh.extend_to(L)
+    hy.extend_to(L)
+    if case == "in_coarse_space":
+        lam0, co0 = rh.coarse_eigensolve(0, 1)
+        glued = rh.prolong(hy.expand_interior(0, co0[0]), 0, L)
+    else:
+        lam, co = rh.coarse_eigensolve(L - 1, 1)
+        u = rh.prolong(hy.expand_interior(L - 1, co[0]), L - 1, L)
+        m = spec["m"]
+        corr = np.stack([rh.local_bvp_solve(L, j, lam[0], u, 1e-10)[0] for j in range(m)])
+        glued = rh.interface_solve(L, lam[0], u, corr, 1e-10)[0]
+    pairs = mlg.augmented_eigensolve(hy, L, glued[None, :], 1)
+    lam_r, co_r = rh.augmented_eigensolve(L, glued[None, :], 1)
+    am, ex = mass_ops(hy, rh, L)
+    compare_pairs([p.lam for p in pairs], [p.coeffs for p in pairs], lam_r, co_r, am, ex)
+    if case == "in_coarse_space":
+        assert abs(pairs[0].lam - lam0[0]) <= 1e-10 * lam0[0]
