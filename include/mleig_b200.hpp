@@ -70,6 +70,7 @@ struct RunConfig {  // corrector.hpp:21-33
   bool deterministic = true;
   int device = 0;
   unsigned long long seed = 0;  // example "reaction" (BASELINE config 4)
+  DomainRect hole{0.0, 0.0, 0.0, 0.0};  // corner hole: L-shaped domain (config 3)
 };
 
 struct SolveReport {  // sparse.hpp:103-107
@@ -129,6 +130,10 @@ inline mlg_config to_c(const RunConfig& config) {
               : config.example == "reaction" ? 2
                                              : -1;
   c.seed = config.seed;
+  c.hole_x_min = config.hole.x_min;
+  c.hole_x_max = config.hole.x_max;
+  c.hole_y_min = config.hole.y_min;
+  c.hole_y_max = config.hole.y_max;
   if (c.example < 0)
     throw ConfigError("unknown example id \"" + config.example +
                       "\" (expected laplace or variable)");
@@ -150,6 +155,7 @@ inline RunConfig from_c(const mlg_config& c) {
   r.nev = c.nev;
   r.example = c.example == 2 ? "reaction" : (c.example == 1 ? "variable" : "laplace");
   r.seed = c.seed;
+  r.hole = {c.hole_x_min, c.hole_x_max, c.hole_y_min, c.hole_y_max};
   r.cg_tol = c.cg_tol;
   r.workers = c.workers;
   r.deterministic = c.deterministic != 0;
@@ -194,9 +200,9 @@ class Hierarchy {
   std::vector<double> expand_interior(int level, const std::vector<double>& coeffs) const {
     const mlg_level_info i = info(level);
     std::vector<double> full(static_cast<std::size_t>(i.ndofs), 0.0);
-    std::size_t k = 0;
-    for (int iy = 1; iy < i.ny; ++iy)
-      for (int ix = 1; ix < i.nx; ++ix) full[static_cast<std::size_t>(iy) * (i.nx + 1) + ix] = coeffs[k++];
+    std::vector<int> d(static_cast<std::size_t>(i.n_interior));
+    check(mlg_export_space(ctx_, level, nullptr, d.data(), nullptr, nullptr));
+    for (std::size_t k = 0; k < d.size(); ++k) full[static_cast<std::size_t>(d[k])] = coeffs[k];
     return full;
   }
   mlg_ctx* handle() const { return ctx_; }

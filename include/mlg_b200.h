@@ -60,6 +60,13 @@ typedef struct mlg_config {
   int deterministic;
   int device; /* CUDA device ordinal of the context (B200-specific) */
   uint64_t seed; /* example 2 only: coefficient seed */
+  /* Corner hole [hole_x_min, hole_x_max] x [hole_y_min, hole_y_max] removed
+   * from the rectangle -> an L-shaped domain (BASELINE config 3; B200
+   * extension, the reference meshes rectangles only).  All zero = none.  Must
+   * lie on the coarse lattice and touch exactly one corner.  Full vectors stay
+   * on the bounding lattice: points strictly inside the hole are inactive
+   * (zero, empty rows), points on its edges are Dirichlet boundary. */
+  double hole_x_min, hole_x_max, hole_y_min, hole_y_max;
 } mlg_config;
 
 typedef struct mlg_ctx mlg_ctx;
@@ -215,6 +222,12 @@ typedef struct mlg_error_report {
  * may be NULL). */
 int mlg_make_reference(int example, int nev, const double* domain, double* lambdas,
                        mlg_exact_mode* modes);
+
+/* The reference set run_experiment uses for a configuration: make_reference
+ * on the configured rectangle, or the L-shaped domain's table when cfg has
+ * the unit corner hole of (-1,1)^2 (config 3). */
+int mlg_make_reference_for(const mlg_config* cfg, int nev, double* lambdas,
+                           mlg_exact_mode* modes);
 
 /* compute_errors (fespace.cpp:434-488) of a full coefficient vector at
  * `level` against lambda_ref and (if non-NULL with mx > 0) the closed form:

@@ -113,6 +113,54 @@ def build_structured_mesh(domain, H):  # mesh.cpp:68-104
     return m
 
 
+def hole_cells(domain, H, nx, ny, hole):
+    """B200 extension (BASELINE config 3, no reference code path): the corner
+    hole [x0,x1]x[y0,y1] in coarse cells (csrc/mesh.cu hole_cells)."""
+    def cell(v, lo):
+        return int(np.floor((v - lo) / H + 0.5))
+    h = (cell(hole[0], domain[0]), cell(hole[2], domain[2]), cell(hole[1], domain[0]),
+         cell(hole[3], domain[2]))  # x0, y0, x1, y1
+    if not ((h[0] == 0) != (h[2] == nx) and (h[1] == 0) != (h[3] == ny)):
+        raise ConfigError("hole must touch exactly one corner of the domain rectangle (L-shape)")
+    return h
+
+
+def _cell_active(h, nx, ny, cx, cy):
+    cx, cy = np.asarray(cx), np.asarray(cy)
+    inside = (cx >= 0) & (cy >= 0) & (cx < nx) & (cy < ny)
+    in_hole = (cx >= h[0]) & (cx < h[2]) & (cy >= h[1]) & (cy < h[3])
+    return inside & ~in_hole
+
+
+def build_structured_mesh_hole(domain, H, hole):
+    """The B200 definition of an L-shaped level 0 (csrc/mesh.cu k_level0_hole):
+    vertices = lattice points touching an element-carrying cell, lexicographic
+    (y, x); two triangles per such cell, cells lexicographic, the split of
+    mesh.cpp:96-97."""
+    nx = checked_cell_count(domain[1] - domain[0], H, "x")
+    ny = checked_cell_count(domain[3] - domain[2], H, "y")
+    h = hole_cells(domain, H, nx, ny, hole)
+    iy, ix = np.mgrid[0:ny + 1, 0:nx + 1]
+    act = (_cell_active(h, nx, ny, ix, iy) | _cell_active(h, nx, ny, ix - 1, iy) |
+           _cell_active(h, nx, ny, ix, iy - 1) | _cell_active(h, nx, ny, ix - 1, iy - 1)).ravel()
+    vid = np.full((ny + 1) * (nx + 1), -1, np.int64)
+    vid[act] = np.arange(int(act.sum()))
+    lat = np.stack([ix.ravel()[act], iy.ravel()[act]], axis=1).astype(np.int32)
+    cy, cx = np.mgrid[0:ny, 0:nx]
+    cact = _cell_active(h, nx, ny, cx, cy).ravel()
+    cx, cy = cx.ravel()[cact], cy.ravel()[cact]
+    p00 = cy * (nx + 1) + cx
+    v00, v10, v01, v11 = vid[p00], vid[p00 + 1], vid[p00 + nx + 1], vid[p00 + nx + 2]
+    tri = np.empty((2 * len(cx), 3), np.int32)
+    tri[0::2] = np.stack([v00, v10, v11], axis=1)
+    tri[1::2] = np.stack([v00, v11, v01], axis=1)
+    m = Mesh(tuple(domain), 0, nx, ny, _coords(domain, nx, ny, lat), lat, tri,
+             _boundary_edges(tri, len(lat)), np.zeros(0, np.int32))
+    m.h_max = _h_max(m)
+    m.hole = h
+    return m
+
+
 def refine_regular(mesh):  # mesh.cpp:106-155
     nv = len(mesh.vertices)
     nx, ny = 2 * mesh.nx, 2 * mesh.ny
@@ -133,6 +181,8 @@ def refine_regular(mesh):  # mesh.cpp:106-155
     m = Mesh(mesh.domain, mesh.level + 1, nx, ny, _coords(mesh.domain, nx, ny, lat), lat, tri,
              _boundary_edges(tri, len(lat)), parent)
     m.h_max = _h_max(m)
+    if getattr(mesh, "hole", None) is not None:
+        m.hole = tuple(2 * v for v in mesh.hole)
     return m
 
 
@@ -163,6 +213,26 @@ def build_space(mesh):  # fespace.cpp:230-312 (degree 1)
     iidx = np.full(len(uk), -1, np.int32)
     iidx[interior] = np.arange(len(interior), dtype=np.int32)
     return FeSpace(mesh, len(uk), dof_lattice, interior, iidx, conn)
+
+
+def build_space_lattice(mesh):
+    """B200 convention for domains with a hole: dofs on the bounding lattice
+    (dof = iy*(nx+1)+ix, points strictly inside the hole inactive: no element,
+    empty rows); interior = element-touching points off the boundary edges."""
+    nx, ny = mesh.nx, mesh.ny
+    nd = (nx + 1) * (ny + 1)
+    iy, ix = np.divmod(np.arange(nd), nx + 1)
+    dof_lattice = np.stack([2 * ix, 2 * iy], axis=1).astype(np.int32)
+    ldof = (mesh.lattice[:, 1].astype(np.int64) * (nx + 1) + mesh.lattice[:, 0])
+    conn = ldof[mesh.triangles].astype(np.int32)
+    active = np.zeros(nd, bool)
+    active[ldof] = True
+    on_b = np.zeros(nd, bool)
+    on_b[ldof[mesh.boundary_edges.reshape(-1)]] = True
+    interior = np.nonzero(active & ~on_b)[0].astype(np.int32)
+    iidx = np.full(nd, -1, np.int32)
+    iidx[interior] = np.arange(len(interior), dtype=np.int32)
+    return FeSpace(mesh, nd, dof_lattice, interior, iidx, conn)
 
 
 QUAD2 = (np.array([[0.5, 0.5, 0.0], [0.0, 0.5, 0.5], [0.5, 0.0, 0.5]]), 1.0 / 3.0)  # :41-47
@@ -390,7 +460,34 @@ class Partition:  # decomp.hpp:59-93
     inners: list = field(default_factory=list)
 
 
-def build_partition(coarse, m, delta):  # decomp.cpp:24-86
+def build_partition_hole(coarse, m, delta):
+    """Partition of a domain with a corner hole (B200 extension, csrc/corrector.cu
+    build_partition): blocks inside the hole are dropped; inner regions follow
+    decomp.cpp:73-80 (the hole's edges are shrunk from like block sides)."""
+    p = build_partition(coarse, m, delta, keep_all=True)
+    h = coarse.hole
+    bw, bh = coarse.nx // p.side, coarse.ny // p.side
+    if h[0] % bw or h[2] % bw or h[1] % bh or h[3] % bh:
+        raise ConfigError("hole does not align with the subdomain block grid")
+
+    def in_hole(c, rb):
+        return c * bw >= h[0] and (c + 1) * bw <= h[2] and rb * bh >= h[1] and (rb + 1) * bh <= h[3]
+
+    q = Partition(0, p.side, p.delta_cells, p.nx0, p.ny0)
+    for r in range(p.side):
+        for c in range(p.side):
+            rb = p.side - 1 - r
+            if in_hole(c, rb):
+                continue
+            x0, y0, x1, y1 = p.blocks[r * p.side + c]
+            q.blocks.append((x0, y0, x1, y1))
+            q.overlaps.append(p.overlaps[r * p.side + c])
+            q.inners.append(p.inners[r * p.side + c])  # hole edges shrink like block sides
+    q.m = len(q.blocks)
+    return q
+
+
+def build_partition(coarse, m, delta, keep_all=False):  # decomp.cpp:24-86
     side = int(np.floor(np.sqrt(m) + 0.5))
     if m < 1 or side * side != m:
         raise ConfigError("subdomain count m must be a perfect square")
@@ -534,14 +631,18 @@ class Level:
 
 class Hierarchy:  # corrector.cpp:111-181
     def __init__(self, domain=(-1.0, 1.0, -1.0, 1.0), H=0.25, delta=0.1, m=4, n_levels=5,
-                 nev=5, cg_tol=1e-10, example="laplace", seed=0):
+                 nev=5, cg_tol=1e-10, example="laplace", seed=0, hole=None):
         self.n_levels, self.nev, self.cg_tol = n_levels, nev, cg_tol
         self.example, self.seed = example, seed
-        mesh = build_structured_mesh(domain, H)
+        self.hole = hole
+        mesh = (build_structured_mesh(domain, H) if hole is None
+                else build_structured_mesh_hole(domain, H, hole))
+        self._space = build_space if hole is None else build_space_lattice
         cell = mesh.dx
         dc = max(1, int(np.ceil(delta / cell - 1e-9)))         # corrector.cpp:117-121
-        self.part = build_partition(mesh, m, dc * cell)
-        sp0 = build_space(mesh)
+        self.part = (build_partition(mesh, m, dc * cell) if hole is None
+                     else build_partition_hole(mesh, m, dc * cell))
+        sp0 = self._space(mesh)
         self.levels = [Level(mesh, sp0, *assemble(sp0, example, seed))]
         self._dense = None
 
@@ -549,7 +650,7 @@ class Hierarchy:  # corrector.cpp:111-181
         while len(self.levels) - 1 < level:
             prev = self.levels[-1]
             mesh = refine_regular(prev.mesh)
-            s = build_space(mesh)
+            s = self._space(mesh)
             self.levels.append(Level(mesh, s, *assemble(s, self.example, self.seed),
                                      prolongation(prev.space, s)))
 

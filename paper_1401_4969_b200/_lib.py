@@ -49,6 +49,8 @@ class MlgConfig(C.Structure):
         ("nev", C.c_int), ("example", C.c_int), ("workers", C.c_int),
         ("cg_tol", C.c_double), ("deterministic", C.c_int), ("device", C.c_int),
         ("seed", C.c_uint64),
+        ("hole_x_min", C.c_double), ("hole_x_max", C.c_double),
+        ("hole_y_min", C.c_double), ("hole_y_max", C.c_double),
     ]
 
 
@@ -132,6 +134,8 @@ SIGNATURES = {
                                        c_double_p, c_double_p, c_double_p, c_int_p,
                                        C.POINTER(MlgStepTimings)],
     "mlg_make_reference": [C.c_int, C.c_int, c_double_p, c_double_p, C.POINTER(MlgExactMode)],
+    "mlg_make_reference_for": [C.POINTER(MlgConfig), C.c_int, c_double_p,
+                               C.POINTER(MlgExactMode)],
     "mlg_compute_errors": [C.c_void_p, C.c_int, c_double_p, C.c_double, C.c_double,
                            C.POINTER(MlgExactMode), C.POINTER(MlgErrorReport)],
     "mlg_parse_config_json": [C.c_char_p, C.POINTER(MlgConfig)],

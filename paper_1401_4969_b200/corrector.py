@@ -54,13 +54,16 @@ class RunConfig:  # corrector.hpp:21-33
     deterministic: bool = True
     device: int = 0  # CUDA device of the context (B200-specific)
     seed: int = 0    # example "reaction" (BASELINE config 4): draws (k1, k2)
+    hole: DomainRect | None = None  # corner hole -> L-shaped domain (BASELINE config 3)
 
     def to_c(self) -> MlgConfig:
         ex = {"laplace": 0, "variable": 1, "reaction": 2}.get(self.example, -1)
+        h = self.hole or DomainRect(0.0, 0.0, 0.0, 0.0)
         return MlgConfig(self.domain.x_min, self.domain.x_max, self.domain.y_min,
                          self.domain.y_max, self.H, self.delta, self.m, self.n_levels,
                          self.degree, self.nev, ex, self.workers, self.cg_tol,
-                         int(self.deterministic), self.device, self.seed)
+                         int(self.deterministic), self.device, self.seed,
+                         h.x_min, h.x_max, h.y_min, h.y_max)
 
 
 @dataclass
@@ -269,17 +272,23 @@ class Hierarchy:
         self.extend_to(level)
         return int(self.level_info(level).ndofs)
 
+    def _interior(self, level: int) -> np.ndarray:
+        cache = self.__dict__.setdefault("_interior_cache", {})
+        if level not in cache:
+            i = self.level_info(level)
+            d = np.empty(i.n_interior, np.int32)
+            check(lib().mlg_export_space(self._h, level, None, _ip(d), None, None))
+            cache[level] = d
+        return cache[level]
+
     def expand_interior(self, level: int, coeffs) -> np.ndarray:  # fespace.cpp:408-415
         i = self.level_info(level)
         full = np.zeros(i.ndofs, np.float64)
-        full.reshape(i.ny + 1, i.nx + 1)[1:-1, 1:-1] = np.asarray(coeffs).reshape(i.ny - 1,
-                                                                                   i.nx - 1)
+        full[self._interior(level)] = np.asarray(coeffs).reshape(-1)
         return full
 
     def restrict_interior(self, level: int, full) -> np.ndarray:  # fespace.cpp:417-423
-        i = self.level_info(level)
-        return np.ascontiguousarray(
-            np.asarray(full).reshape(i.ny + 1, i.nx + 1)[1:-1, 1:-1]).reshape(-1)
+        return np.ascontiguousarray(np.asarray(full)[self._interior(level)])
 
     def set_profiling(self, on: bool) -> None:
         check(lib().mlg_set_profiling(self._h, int(on)))

@@ -19,6 +19,8 @@
 // sequence (unfused __d*_rn), sorts the contributions by element id and sums
 // them.  Output is the 4-entry upper stencil {C,E,N,NE} of A and M per dof
 // (64 B/dof written, coalesced); CSR export is a second closed-form pass.
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -113,6 +115,7 @@ __device__ __forceinline__ bool contribution(const LevelGeom& G, int cx, int cy,
                                              int kd, int kn, Contrib* out) {
   if (cx < 0 || cy < 0 || cx >= G.nx || cy >= G.ny) return false;
   const unsigned code = G.geo[2 * (static_cast<std::int64_t>(cy) * G.nx + cx) + upper];
+  if (code == 0xFFFFFFFFu) return false;  // removed cell (domain with a hole)
   const int rot = static_cast<int>(code & 3u);
   double vx[3], vy[3];
 #pragma unroll
@@ -209,6 +212,7 @@ __device__ __forceinline__ bool elem_matrix_var(const LevelGeom& G, int cx, int 
                                                 int* rot) {
   if (cx < 0 || cy < 0 || cx >= G.nx || cy >= G.ny) return false;
   const unsigned code = G.geo[2 * (static_cast<std::int64_t>(cy) * G.nx + cx) + upper];
+  if (code == 0xFFFFFFFFu) return false;  // removed cell (domain with a hole)
   *rot = static_cast<int>(code & 3u);
   *e = code >> 2;
   double vx[3], vy[3];
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(kBlock) k_assemble_var(LevelGeom G, Stencil* s
   ordered_sum<2>(cne, nne_, &A.ne, &M.ne);
   stA[d] = A;
   stM[d] = M;
-  dinv[d] = 1.0 / A.c;
+  dinv[d] = A.c != 0.0 ? 1.0 / A.c : 0.0;  // inactive points of a hole: empty rows
 }
 
 template <int EX>
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(kBlock) k_assemble(LevelGeom G, Stencil* stA, 
   }
   stA[d] = A;
   stM[d] = M;
-  dinv[d] = 1.0 / A.c;  // JacobiPreconditioner: inv_diag = 1.0 / coeff(r,r)
+  dinv[d] = A.c != 0.0 ? 1.0 / A.c : 0.0;  // JacobiPreconditioner inv_diag (0 for inactive points)
 }
 
 // row_ptr of the full 7-point pattern in closed form.
@@ -362,22 +366,108 @@ __global__ void k_export_csr(int nx, int ny, long long nnz, const Stencil* st, i
 
 // to_dense(extract_submatrix(a, interior_dofs)) (sparse.cpp:156-184),
 // column-major n x n with n = (nx-1)(ny-1); entries mirror bitwise.
-__global__ void k_interior_dense(int nx, int ny, const Stencil* st, double* dense) {
+__global__ void k_interior_dense(IMap im, const Stencil* st, double* dense) {
   const std::int64_t k = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-  const int w = nx - 1, h = ny - 1;
-  const std::int64_t n = static_cast<std::int64_t>(w) * h;
+  const std::int64_t n = im.count();
   if (k >= n) return;
-  const int i = static_cast<int>(k % w), j = static_cast<int>(k / w);
-  const std::int64_t d = static_cast<std::int64_t>(j + 1) * (nx + 1) + (i + 1);
+  int ix, iy;
+  im.point(k, &ix, &iy);
+  const std::int64_t s = im.nx + 1;
+  const std::int64_t d = static_cast<std::int64_t>(iy) * s + ix;
+  auto put = [&](int jx, int jy, double v) {
+    const long long col_k = im.index(jx, jy);
+    if (col_k >= 0) dense[col_k * n + k] = v;
+  };
+  put(ix - 1, iy - 1, st[d - s - 1].ne);
+  put(ix, iy - 1, st[d - s].n);
+  put(ix - 1, iy, st[d - 1].e);
+  put(ix, iy, st[d].c);
+  put(ix + 1, iy, st[d].e);
+  put(ix, iy + 1, st[d].n);
+  put(ix + 1, iy + 1, st[d].ne);
+}
+
+// ---- domains with a corner hole (config 3) ----
+// Structural existence of the couplings of row (ix,iy) in the order SW, S, W,
+// C, E, N, NE (a coupling exists iff an element contains both dofs).
+__device__ __forceinline__ void hole_row_pattern(const Hole& h, int nx, int ny, int ix, int iy,
+                                                 bool e[7]) {
+  const bool c00 = cell_active(h, nx, ny, ix - 1, iy - 1), c10 = cell_active(h, nx, ny, ix, iy - 1);
+  const bool c01 = cell_active(h, nx, ny, ix - 1, iy), c11 = cell_active(h, nx, ny, ix, iy);
+  e[0] = c00;
+  e[1] = c00 || c10;
+  e[2] = c00 || c01;
+  e[3] = c00 || c10 || c01 || c11;
+  e[4] = c10 || c11;
+  e[5] = c01 || c11;
+  e[6] = c11;
+}
+
+__global__ void k_csr_count_hole(int nx, int ny, Hole h, int* cnt) {
+  const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t nd = static_cast<std::int64_t>(nx + 1) * (ny + 1);
+  if (d > nd) return;
+  if (d == nd) {
+    cnt[d] = 0;
+    return;
+  }
+  const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
+  bool e[7];
+  hole_row_pattern(h, nx, ny, ix, iy, e);
+  int n = 0;
+  for (int k = 0; k < 7; ++k) n += e[k];
+  cnt[d] = n;
+}
+
+__global__ void k_export_csr_hole(int nx, int ny, Hole h, const Stencil* st, const int* rp,
+                                  int* cols, double* vals) {
+  const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t nd = static_cast<std::int64_t>(nx + 1) * (ny + 1);
+  if (d >= nd) return;
+  const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
+  bool e[7];
+  hole_row_pattern(h, nx, ny, ix, iy, e);
   const std::int64_t s = nx + 1;
-  auto put = [&](std::int64_t col_k, double v) { dense[col_k * n + k] = v; };
-  if (j > 0 && i > 0) put(k - w - 1, st[d - s - 1].ne);
-  if (j > 0) put(k - w, st[d - s].n);
-  if (i > 0) put(k - 1, st[d - 1].e);
-  put(k, st[d].c);
-  if (i < w - 1) put(k + 1, st[d].e);
-  if (j < h - 1) put(k + w, st[d].n);
-  if (j < h - 1 && i < w - 1) put(k + w + 1, st[d].ne);
+  const std::int64_t col[7] = {d - s - 1, d - s, d - 1, d, d + 1, d + s, d + s + 1};
+  long long k = rp[d];
+  for (int q = 0; q < 7; ++q) {
+    if (!e[q]) continue;
+    double v;
+    switch (q) {
+      case 0: v = st[d - s - 1].ne; break;
+      case 1: v = st[d - s].n; break;
+      case 2: v = st[d - 1].e; break;
+      case 3: v = st[d].c; break;
+      case 4: v = st[d].e; break;
+      case 5: v = st[d].n; break;
+      default: v = st[d].ne; break;
+    }
+    if (cols) cols[k] = static_cast<int>(col[q]);
+    if (vals) vals[k] = v;
+    ++k;
+  }
+}
+
+// CG operator of a domain with a hole: extract_submatrix(A, interior) on the
+// bounding lattice -- couplings touching a non-interior point are 0 and
+// non-interior rows are identity, so a window that covers part of the hole
+// keeps exact zeros there (zero rhs, zero iterates) and every dot product
+// equals the restricted system's.
+__global__ void k_cg_stencil(IMap im, const Stencil* st, const double* dinv, Stencil* out,
+                             double* dinv_out) {
+  const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const int nx = im.nx, ny = im.ny;
+  if (d >= static_cast<std::int64_t>(nx + 1) * (ny + 1)) return;
+  const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
+  if (!im.interior(ix, iy)) {
+    out[d] = Stencil{1.0, 0.0, 0.0, 0.0};
+    dinv_out[d] = 1.0;
+    return;
+  }
+  const Stencil a = st[d];
+  out[d] = Stencil{a.c, im.interior(ix + 1, iy) ? a.e : 0.0, im.interior(ix, iy + 1) ? a.n : 0.0,
+                   im.interior(ix + 1, iy + 1) ? a.ne : 0.0};
+  dinv_out[d] = dinv[d];
 }
 
 // Clears *flag if any interior row of st / dinv differs bitwise from row (1,1).
@@ -400,6 +490,8 @@ __global__ void k_uniform_check(int nx, int ny, const Stencil* st, const double*
 }  // namespace
 
 std::int64_t csr_nnz(const Level& L) {
+  if (L.hole.any())  // diagonal per vertex + 2 per mesh edge, E = (3T + B) / 2
+    return L.nv + 3 * L.nt + L.nb;
   const std::int64_t n = L.nx, m = L.ny;
   // sum over rows: (3nx+1)(ny+1) + (2nx+1)*2ny
   return (3 * n + 1) * (m + 1) + (2 * n + 1) * 2 * m;
@@ -439,6 +531,16 @@ void assemble_level(Ctx& c, Level& L) {
   // Constant-coefficient detection for the CG fast path (MLG_GENERAL_STENCIL=1
   // forces the general per-row path, used by the tests to cover both).
   L.uniform = 0;
+  if (L.hole.any()) {  // CG operator with identity rows on the non-interior points
+    L.stCG.alloc(nd);
+    L.dinvCG.alloc(nd);
+    k_cg_stencil<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(L.imap(), L.stA.get(),
+                                                                L.dinv.get(), L.stCG.get(),
+                                                                L.dinvCG.get());
+    MLG_LAUNCH_CHECK();
+    c.sync();
+    return;
+  }
   const char* env = std::getenv("MLG_GENERAL_STENCIL");
   if (L.nx >= 2 && L.ny >= 2 && !(env && env[0] == '1')) {
     DevBuf<int> flag(1);
@@ -460,6 +562,33 @@ void assemble_level(Ctx& c, Level& L) {
 }
 
 void export_csr(Ctx& c, const Level& L, int form, int* row_ptr, int* cols, double* vals) {
+  if (L.hole.any()) {
+    const std::int64_t nd = L.ndofs();
+    DevBuf<int> cnt(nd + 1), rp(nd + 1);
+    k_csr_count_hole<<<grid_for(nd + 1, kBlock), kBlock, 0, c.stream>>>(L.nx, L.ny, L.hole,
+                                                                       cnt.get());
+    MLG_LAUNCH_CHECK();
+    std::size_t tb = 0;
+    MLG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), rp.get(),
+                                           static_cast<int>(nd + 1), c.stream));
+    void* tmp = c.scratch_bytes(tb);
+    MLG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt.get(), rp.get(), static_cast<int>(nd + 1),
+                                           c.stream));
+    int nnz = 0;
+    MLG_CUDA(cudaMemcpyAsync(&nnz, rp.get() + nd, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    DevBuf<int> cl(cols ? nnz : 0);
+    DevBuf<double> vl(vals ? nnz : 0);
+    k_export_csr_hole<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(
+        L.nx, L.ny, L.hole, form == 0 ? L.stA.get() : L.stM.get(), rp.get(),
+        cols ? cl.get() : nullptr, vals ? vl.get() : nullptr);
+    MLG_LAUNCH_CHECK();
+    if (row_ptr) rp.download(row_ptr, nd + 1, c.stream);
+    if (cols) cl.download(cols, nnz, c.stream);
+    if (vals) vl.download(vals, nnz, c.stream);
+    c.sync();
+    return;
+  }
   const std::int64_t nd = L.ndofs(), nnz = csr_nnz(L);
   DevBuf<int> rp(row_ptr ? nd + 1 : 0), cl(cols ? nnz : 0);
   DevBuf<double> vl(vals ? nnz : 0);
@@ -477,7 +606,7 @@ void interior_dense(Ctx& c, const Level& L, int form, double* d_dense) {
   const std::int64_t n = L.nint();
   MLG_CUDA(cudaMemsetAsync(d_dense, 0, sizeof(double) * n * n, c.stream));
   k_interior_dense<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(
-      L.nx, L.ny, form == 0 ? L.stA.get() : L.stM.get(), d_dense);
+      L.imap(), form == 0 ? L.stA.get() : L.stM.get(), d_dense);
   MLG_LAUNCH_CHECK();
 }
 

@@ -205,6 +205,10 @@ int mlg_create(const mlg_config* cfg, mlg_ctx** out) {
     c.deterministic = cfg->deterministic;
     c.device = cfg->device;
     c.seed = cfg->seed;
+    c.hole_x0 = cfg->hole_x_min;
+    c.hole_x1 = cfg->hole_x_max;
+    c.hole_y0 = cfg->hole_y_min;
+    c.hole_y1 = cfg->hole_y_max;
     auto h = std::make_unique<mlg_ctx>();
     h->c = std::make_unique<mlg::Ctx>(c);
     *out = h.release();
@@ -294,10 +298,11 @@ int mlg_region_dofs(mlg_ctx* ctx, int level, int kind, int j, int zero_trace, in
     if ((kind >= 1 && kind <= 3) && (j < 0 || j >= c.part.m))
       throw mlg::ConfigError("subdomain index out of range");
     const int S = 1 << level;
+    const mlg::IMap im = L.imap();
     int64_t n = 0;
     for (int iy = 1; iy < L.ny; ++iy)
       for (int ix = 1; ix < L.nx; ++ix)
-        if (keep_dof(c.part, kind, j, zero_trace != 0, S, ix, iy)) {
+        if (im.interior(ix, iy) && keep_dof(c.part, kind, j, zero_trace != 0, S, ix, iy)) {
           if (out) out[n] = iy * (L.nx + 1) + ix;
           ++n;
         }
@@ -314,7 +319,7 @@ int mlg_region_elements(mlg_ctx* ctx, int level, int kind, int j, int* out, int6
     std::vector<int> all;
     switch (kind) {
       case 0:
-        all.resize(2 * p.nx0 * p.ny0);
+        all.resize(static_cast<std::size_t>(p.nt0));
         for (std::size_t e = 0; e < all.size(); ++e) all[e] = static_cast<int>(e);
         base = &all;
         break;
@@ -579,6 +584,28 @@ int mlg_make_reference(int example, int nev, const double* domain, double* lambd
                        mlg_exact_mode* modes) {
   return guarded([&] {
     const mlg::ReferenceSet r = mlg::make_reference(example, nev, domain);
+    for (int i = 0; i < nev; ++i) {
+      if (lambdas) lambdas[i] = r.lambdas[static_cast<std::size_t>(i)];
+      if (modes) modes[i] = to_c(r.modes[static_cast<std::size_t>(i)]);
+    }
+  });
+}
+
+int mlg_make_reference_for(const mlg_config* cfg, int nev, double* lambdas,
+                           mlg_exact_mode* modes) {
+  return guarded([&] {
+    if (!cfg) throw mlg::ConfigError("null argument");
+    mlg::Config c;
+    c.x_min = cfg->x_min;
+    c.x_max = cfg->x_max;
+    c.y_min = cfg->y_min;
+    c.y_max = cfg->y_max;
+    c.example = cfg->example;
+    c.hole_x0 = cfg->hole_x_min;
+    c.hole_x1 = cfg->hole_x_max;
+    c.hole_y0 = cfg->hole_y_min;
+    c.hole_y1 = cfg->hole_y_max;
+    const mlg::ReferenceSet r = mlg::make_reference_for(c, nev);
     for (int i = 0; i < nev; ++i) {
       if (lambdas) lambdas[i] = r.lambdas[static_cast<std::size_t>(i)];
       if (modes) modes[i] = to_c(r.modes[static_cast<std::size_t>(i)]);

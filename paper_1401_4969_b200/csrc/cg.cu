@@ -1250,8 +1250,10 @@ int resident_persist() {
 
 SweepArgs sweep_args(const Level& L, const unsigned char* mask) {
   SweepArgs A{};
-  A.st = L.stA.get();
-  A.dinv = L.dinv.get();
+  // domains with a hole: the interior-restricted operator (identity rows on
+  // the hole, see assemble.cu k_cg_stencil)
+  A.st = L.hole.any() ? L.stCG.get() : L.stA.get();
+  A.dinv = L.hole.any() ? L.dinvCG.get() : L.dinv.get();
   A.nxp1 = L.nx + 1;
   A.mask = mask;
   A.sg = L.strip_geom;

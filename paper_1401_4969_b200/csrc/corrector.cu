@@ -31,14 +31,24 @@ constexpr int kB = 256;
 // y = P x for one refinement: fine dof at a coarse vertex -> 1.0 x_c, at an
 // axis or SW-NE diagonal edge midpoint -> 0.5 x_a + 0.5 x_b (a < b), summed
 // from 0.0 in ascending coarse column order.
+// With a hole (fine scale hf) the fine points strictly inside it carry no row
+// of P (they lie in no coarse element): 0.
+__device__ __forceinline__ bool point_live(const Hole& h, int nx, int ny, int ix, int iy) {
+  return !h.any() || cell_active(h, nx, ny, ix, iy) || cell_active(h, nx, ny, ix - 1, iy) ||
+         cell_active(h, nx, ny, ix, iy - 1) || cell_active(h, nx, ny, ix - 1, iy - 1);
+}
+
 template <int NR>
-__global__ void k_prolong(int nxc, int nxf, int nyf, const double* xc, double* xf) {
+__global__ void k_prolong(int nxc, int nxf, int nyf, Hole hf, const double* xc, double* xf) {
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(nxf + 1) * (nyf + 1)) return;
   const int fx = static_cast<int>(d % (nxf + 1)), fy = static_cast<int>(d / (nxf + 1));
   const long long sc = nxc + 1;
   double y[NR], a[NR], b[NR];
-  if (!(fx & 1) && !(fy & 1)) {
+  if (!point_live(hf, nxf, nyf, fx, fy)) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) y[r] = 0.0;
+  } else if (!(fx & 1) && !(fy & 1)) {
     ldv<NR>(xc + (static_cast<long long>(fy / 2) * sc + fx / 2) * NR, a);
 #pragma unroll
     for (int r = 0; r < NR; ++r) y[r] = xadd(0.0, xmul(1.0, a[r]));
@@ -56,7 +66,8 @@ __global__ void k_prolong(int nxc, int nxf, int nyf, const double* xc, double* x
 // y = P^T x: coarse c gathers its <=7 fine rows in ascending fine-row order
 // (multiply_transpose scatters row by row), weights 0.5 / 1.0.
 template <int NR>
-__global__ void k_restrict(int nxf, int nyf, int nxc, int nyc, const double* xf, double* xc) {
+__global__ void k_restrict(int nxf, int nyf, int nxc, int nyc, Hole hf, const double* xf,
+                           double* xc) {
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(nxc + 1) * (nyc + 1)) return;
   const int cx = static_cast<int>(d % (nxc + 1)), cy = static_cast<int>(d / (nxc + 1));
@@ -67,6 +78,7 @@ __global__ void k_restrict(int nxf, int nyf, int nxc, int nyc, const double* xf,
   for (int r = 0; r < NR; ++r) y[r] = 0.0;
   auto acc = [&](int fx, int fy, double w) {
     if (fx < 0 || fy < 0 || fx > nxf || fy > nyf) return;
+    if (!point_live(hf, nxf, nyf, fx, fy)) return;  // no row of P
     ldv<NR>(xf + (static_cast<long long>(fy) * sf + fx) * NR, t);
 #pragma unroll
     for (int r = 0; r < NR; ++r) y[r] = xadd(y[r], xmul(w, t[r]));
@@ -85,21 +97,24 @@ __global__ void k_restrict(int nxf, int nyf, int nxc, int nyc, const double* xf,
 
 // res = lam * (M u) - (A u) at interior dofs (corrector.cpp:201,237); 0 on the boundary.
 template <int NR>
-__global__ void k_residual(int nx, int ny, const Stencil* stA, const Stencil* stM,
+__global__ void k_residual(IMap im, const Stencil* stA, const Stencil* stM,
                            const double* u, const double* w, Lam lam, double* out,
                            const unsigned char* only_mask) {
+  const int nx = im.nx, ny = im.ny;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(nx + 1) * (ny + 1)) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
   double y[NR];
-  if (ix == 0 || iy == 0 || ix == nx || iy == ny || (only_mask && !only_mask[d])) {
-    if (!only_mask) {
+  // Non-interior points get 0 (the CG windows of a domain with a hole cover
+  // hole points, which must see a zero rhs); masked-out interior points are
+  // never read.
+  if (!im.interior(ix, iy)) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r) y[r] = 0.0;
-      stv<NR>(out + d * NR, y);
-    }
+    for (int r = 0; r < NR; ++r) y[r] = 0.0;
+    stv<NR>(out + d * NR, y);
     return;
   }
+  if (only_mask && !only_mask[d]) return;
   double mu[NR], aw[NR];
   full_row<NR>(stM, u, ix, iy, nx, ny, mu);
   full_row<NR>(stA, w, ix, iy, nx, ny, aw);
@@ -111,13 +126,14 @@ __global__ void k_residual(int nx, int ny, const Stencil* stA, const Stencil* st
 // ya = A x, ym = M x at interior rows (boundary rows 0; they never reach the
 // interior of a coarser level nor a dot product with an interior vector).
 template <int NR>
-__global__ void k_dual(int nx, int ny, const Stencil* stA, const Stencil* stM, const double* x,
+__global__ void k_dual(IMap im, const Stencil* stA, const Stencil* stM, const double* x,
                        double* ya, double* ym) {
+  const int nx = im.nx, ny = im.ny;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(nx + 1) * (ny + 1)) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
   double y[NR];
-  const bool inner = !(ix == 0 || iy == 0 || ix == nx || iy == ny);
+  const bool inner = im.interior(ix, iy);
   if (ya) {
     if (inner) full_row<NR>(stA, x, ix, iy, nx, ny, y);
     else
@@ -201,6 +217,7 @@ struct PartDev {
   int m;
   IRect inner[256];
   IRect overlap[256];
+  short blk2j[256];  // block (bottom-up row-major) -> subdomain, -1: removed (hole)
 };
 
 // Subdomain whose closed inner region G_j contains the fine lattice point,
@@ -210,7 +227,8 @@ struct PartDev {
 __device__ __forceinline__ int inner_owner(const PartDev& P, int ix, int iy) {
   const int c = min(ix / (P.bw * P.scale), P.side - 1);
   const int rb = min(iy / (P.bh * P.scale), P.side - 1);
-  const int j = (P.side - 1 - rb) * P.side + c;
+  const int j = P.blk2j[rb * P.side + c];
+  if (j < 0) return -1;
   const IRect& g = P.inner[j];
   if (ix >= g.x0 * P.scale && ix <= g.x1 * P.scale && iy >= g.y0 * P.scale &&
       iy <= g.y1 * P.scale)
@@ -218,11 +236,12 @@ __device__ __forceinline__ int inner_owner(const PartDev& P, int ix, int iy) {
   return -1;
 }
 
-__global__ void k_strip_mask(int nx, int ny, PartDev P, unsigned char* mask) {
+__global__ void k_strip_mask(IMap im, PartDev P, unsigned char* mask) {
+  const int nx = im.nx, ny = im.ny;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(nx + 1) * (ny + 1)) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
-  const bool interior = ix > 0 && iy > 0 && ix < nx && iy < ny;
+  const bool interior = im.interior(ix, iy);
   mask[d] = (interior && inner_owner(P, ix, iy) < 0) ? 1 : 0;
 }
 
@@ -230,15 +249,16 @@ __global__ void k_strip_mask(int nx, int ny, PartDev P, unsigned char* mask) {
 // e_j of eigenvector r comes from the batched local CG: system j*nev + r
 // (window-compact X) ...
 template <int NR>
-__global__ void k_glue_cg(int nx, int ny, PartDev P, int nev, const CgSys* sys, const double* X,
+__global__ void k_glue_cg(IMap im, PartDev P, int nev, const CgSys* sys, const double* X,
                           const double* u, double* glued) {
+  const int nx = im.nx, ny = im.ny;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(nx + 1) * (ny + 1)) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
   double y[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) y[r] = 0.0;
-  if (ix > 0 && iy > 0 && ix < nx && iy < ny) {
+  if (im.interior(ix, iy)) {
     const int j = inner_owner(P, ix, iy);
     if (j >= 0) {
       double uu[NR];
@@ -255,13 +275,14 @@ __global__ void k_glue_cg(int nx, int ny, PartDev P, int nev, const CgSys* sys, 
 }
 
 // ... or from caller-provided full-space corrections (NR = 1 test entry point).
-__global__ void k_glue_full(int nx, int ny, PartDev P, long long ndofs, const double* corr,
+__global__ void k_glue_full(IMap im, PartDev P, long long ndofs, const double* corr,
                             const double* u, double* glued) {
+  const int nx = im.nx;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= ndofs) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
   double y = 0.0;
-  if (ix > 0 && iy > 0 && ix < nx && iy < ny) {
+  if (im.interior(ix, iy)) {
     const int j = inner_owner(P, ix, iy);
     if (j >= 0) y = xadd(u[d], corr[static_cast<long long>(j) * ndofs + d]);
   }
@@ -290,21 +311,22 @@ __global__ void k_strip_scatter(int nx, int nev, const CgSys* sys, const unsigne
 
 // rhs-major [k][n_src] (full or interior order) -> interleaved full lattice.
 template <int NR>
-__global__ void k_interleave(int nx, int ny, int k_in, const double* src, int interior_src,
+__global__ void k_interleave(IMap im, int k_in, const double* src, int interior_src,
                              double* dst) {
+  const int nx = im.nx, ny = im.ny;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long nd = static_cast<long long>(nx + 1) * (ny + 1);
   if (d >= nd) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
-  const bool inner = ix > 0 && iy > 0 && ix < nx && iy < ny;
-  const long long ni = static_cast<long long>(nx - 1) * (ny - 1);
+  const long long ki = im.index(ix, iy);
+  const long long ni = im.count();
   double y[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     double v = 0.0;
     if (r < k_in) {
       if (interior_src) {
-        if (inner) v = src[r * ni + static_cast<long long>(iy - 1) * (nx - 1) + (ix - 1)];
+        if (ki >= 0) v = src[r * ni + ki];
       } else {
         v = src[r * nd + d];
       }
@@ -316,29 +338,32 @@ __global__ void k_interleave(int nx, int ny, int k_in, const double* src, int in
 
 // interleaved full lattice -> rhs-major (interior or full order), lanes perm[r].
 template <int NR>
-__global__ void k_deinterleave(int nx, int ny, int k_out, const int* perm, const double* src,
+__global__ void k_deinterleave(IMap im, int k_out, const int* perm, const double* src,
                                int interior_dst, double* dst) {
+  const int nx = im.nx, ny = im.ny;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long nd = static_cast<long long>(nx + 1) * (ny + 1);
   if (d >= nd) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
-  const bool inner = ix > 0 && iy > 0 && ix < nx && iy < ny;
-  if (interior_dst && !inner) return;
-  const long long ni = static_cast<long long>(nx - 1) * (ny - 1);
+  const long long ki = im.index(ix, iy);
+  if (interior_dst && ki < 0) return;
+  const long long ni = im.count();
   double v[NR];
   ldv<NR>(src + d * NR, v);
-  const long long o = interior_dst ? static_cast<long long>(iy - 1) * (nx - 1) + (ix - 1) : d;
+  const long long o = interior_dst ? ki : d;
   const long long n = interior_dst ? ni : nd;
   for (int r = 0; r < k_out; ++r) dst[r * n + o] = v[perm ? perm[r] : r];
 }
 
 // Interior coarse dofs of a full-lattice vector -> column-major mc x NR.
 template <int NR>
-__global__ void k_gather_coarse(int nx, int ny, const double* src, double* dst) {
+__global__ void k_gather_coarse(IMap im, const double* src, double* dst) {
   const long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  const long long mc = static_cast<long long>(nx - 1) * (ny - 1);
+  const long long mc = im.count();
   if (k >= mc) return;
-  const long long d = (k / (nx - 1) + 1) * (nx + 1) + (k % (nx - 1) + 1);
+  int ix, iy;
+  im.point(k, &ix, &iy);
+  const long long d = static_cast<long long>(iy) * (im.nx + 1) + ix;
   double v[NR];
   ldv<NR>(src + d * NR, v);
 #pragma unroll
@@ -629,6 +654,7 @@ PartDev part_dev(const Ctx& c, int level) {
     P.inner[j] = p.inners[j];
     P.overlap[j] = p.overlaps[j];
   }
+  for (int b = 0; b < p.side * p.side; ++b) P.blk2j[b] = static_cast<short>(p.blk2j[b]);
   return P;
 }
 
@@ -682,7 +708,7 @@ static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-
   const double cell = L0.dx;
   const int delta_cells = std::max(1, static_cast<int>(std::ceil(c.cfg.delta / cell - 1e-9)));
   const double delta = delta_cells * cell;
-  const int m = c.cfg.m;
+  int m = c.cfg.m;  // the block grid; a hole drops the blocks it contains
   const int side = static_cast<int>(std::lround(std::sqrt(static_cast<double>(m))));
   if (m < 1 || side * side != m) throw ConfigError("subdomain count m must be a perfect square");
   const double hx = L0.dx, hy = L0.dy;
@@ -699,14 +725,28 @@ static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-
   if (2 * dc >= bw || 2 * dc >= bh)
     throw ConfigError("overlap width leaves a degenerate inner region (2*delta >= block side)");
   Partition& p = c.part;
-  p.m = m;
   p.side = side;
   p.delta_cells = dc;
   p.nx0 = L0.nx;
   p.ny0 = L0.ny;
   p.cell_h = hx;
+  p.nt0 = static_cast<int>(L0.nt);
+  p.blk2j.assign(static_cast<std::size_t>(side) * side, -1);
+  // Domains with a corner hole (config 3, B200 extension): blocks inside the
+  // hole are dropped ("subdomains on the grid clipped to the domain").
+  const Hole& H0 = L0.hole;
+  auto block_in_hole = [&](int col, int rb) {
+    return H0.any() && col * bw >= H0.x0 && (col + 1) * bw <= H0.x1 && rb * bh >= H0.y0 &&
+           (rb + 1) * bh <= H0.y1;
+  };
+  if (H0.any() && (H0.x0 % bw || H0.x1 % bw || H0.y0 % bh || H0.y1 % bh))
+    throw ConfigError("hole does not align with the subdomain block grid");
+  m = 0;
   for (int r = 0; r < side; ++r)
     for (int col = 0; col < side; ++col) {
+      const int rb = side - 1 - r;
+      if (block_in_hole(col, rb)) continue;
+      p.blk2j[static_cast<std::size_t>(rb) * side + col] = m++;
       IRect d;
       d.x0 = col * bw;
       d.x1 = (col + 1) * bw;
@@ -719,13 +759,16 @@ static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-
       om.y0 = std::max(0, d.y0 - dc);
       om.y1 = std::min(L0.ny, d.y1 + dc);
       p.overlaps.push_back(om);
-      IRect g;
+      IRect g;  // decomp.cpp:73-80; with a hole its edges are shrunk from like
+                // interior block sides (the strip then runs along them too),
+                // which keeps G_j the closed form the strip CG kernels use
       g.x0 = (d.x0 == 0) ? 0 : d.x0 + dc;
       g.x1 = (d.x1 == L0.nx) ? L0.nx : d.x1 - dc;
       g.y0 = (d.y0 == 0) ? 0 : d.y0 + dc;
       g.y1 = (d.y1 == L0.ny) ? L0.ny : d.y1 - dc;
       p.inners.push_back(g);
     }
+  p.m = m;
   // Level-0 element sets by integer centroid-in-open-rect (decomp.cpp:13-18,101-121);
   // element 2*cell is the lower triangle (centroid*3 = (3ix+2, 3iy+1)), 2*cell+1
   // the upper one ((3ix+1, 3iy+2)).
@@ -736,8 +779,12 @@ static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-
   auto open_in = [](const IRect& r, int cx3, int cy3) {
     return cx3 > 3 * r.x0 && cx3 < 3 * r.x1 && cy3 > 3 * r.y0 && cy3 < 3 * r.y1;
   };
-  for (int e = 0; e < 2 * L0.nx * L0.ny; ++e) {
-    const int cell_id = e / 2, ix = cell_id % L0.nx, iy = cell_id / L0.nx;
+  std::vector<int> cell_of;  // element pair -> lattice cell (holes skip removed cells)
+  for (int cy = 0; cy < L0.ny; ++cy)
+    for (int cx = 0; cx < L0.nx; ++cx)
+      if (!H0.cell_in(cx, cy)) cell_of.push_back(cy * L0.nx + cx);
+  for (int e = 0; e < 2 * static_cast<int>(cell_of.size()); ++e) {
+    const int cell_id = cell_of[e / 2], ix = cell_id % L0.nx, iy = cell_id / L0.nx;
     const int cx3 = (e & 1) ? 3 * ix + 1 : 3 * ix + 2;
     const int cy3 = (e & 1) ? 3 * iy + 2 : 3 * iy + 1;
     bool in_inner = false;
@@ -878,7 +925,7 @@ void prolong_chain(Ctx& c, int nr, const double* src, int from, int to, double* 
       bufs[k & 1]->ensure(F.ndofs() * nr);
       out = bufs[k & 1]->get();
     }
-    NR_DISPATCH(nr, k_prolong, grid_for(F.ndofs(), kB), C.nx, F.nx, F.ny, cur, out);
+    NR_DISPATCH(nr, k_prolong, grid_for(F.ndofs(), kB), C.nx, F.nx, F.ny, F.hole, cur, out);
     cur = out;
   }
 }
@@ -894,7 +941,8 @@ const double* restrict_chain(Ctx& c, int nr, const double* src, int from, int sl
     const Level& C = c.level(k - 1);
     DevBuf<double>& out = w.chain[2 * (k - 1) + slot];
     out.ensure(C.ndofs() * nr);
-    NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, cur, out.get());
+    NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, F.hole, cur,
+                out.get());
     cur = out.get();
   }
   return cur;
@@ -1070,10 +1118,10 @@ std::vector<double> coarse_eigensolve(Ctx& c, int level, int nev, DevBuf<double>
   DevBuf<double> tmp(host.size());
   tmp.upload(host.data(), host.size(), c.stream);
   u_out.ensure(L.ndofs() * nr);
-  NR_DISPATCH(nr, k_interleave, grid_for(L.ndofs(), kB), L.nx, L.ny, nev, tmp.get(), 1,
+  NR_DISPATCH(nr, k_interleave, grid_for(L.ndofs(), kB), L.imap(), nev, tmp.get(), 1,
               u_out.get());
   w.mfull.ensure(L.ndofs() * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(L.ndofs(), kB), L.nx, L.ny, L.stA.get(), L.stM.get(),
+  NR_DISPATCH(nr, k_dual, grid_for(L.ndofs(), kB), L.imap(), L.stA.get(), L.stM.get(),
               u_out.get(), nullptr, w.mfull.get());
   const auto q = mdot(c, nr, L, u_out.get(), w.mfull.get());
   Lam s{};
@@ -1147,7 +1195,7 @@ void ensure_strip_mask(Ctx& c, Level& F) {
   g.ny0 = c.part.ny0;
   g.scale = 1 << F.level;
   F.strip_mask.alloc(F.ndofs());
-  k_strip_mask<<<grid_for(F.ndofs(), kB), kB, 0, c.stream>>>(F.nx, F.ny, part_dev(c, F.level),
+  k_strip_mask<<<grid_for(F.ndofs(), kB), kB, 0, c.stream>>>(F.imap(), part_dev(c, F.level),
                                                              F.strip_mask.get());
   MLG_LAUNCH_CHECK();
 }
@@ -1166,7 +1214,7 @@ int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const Lam& l
   *empty = !any_strip;
   if (!any_strip) return 0;  // m = 1: G_1 is the whole domain, the strip is empty
   w.load.ensure(F.ndofs() * nr);
-  NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.nx, F.ny, F.stA.get(), F.stM.get(), u,
+  NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.imap(), F.stA.get(), F.stM.get(), u,
               glued, lam, w.load.get(), F.strip_mask.get());
   std::vector<CgSys> sys;
   for (int i = 0; i < nev; ++i) {
@@ -1203,13 +1251,13 @@ static std::vector<double> expand_augmented(Ctx& c, Level& F, int level, int nr,
   const long long nd = F.ndofs();
   DevBuf<double>& c0 = w.aug_c0;
   c0.ensure(L0.ndofs() * nr);
-  NR_DISPATCH(nr, k_interleave, grid_for(L0.ndofs(), kB), L0.nx, L0.ny, nev, d_cp, 1, c0.get());
+  NR_DISPATCH(nr, k_interleave, grid_for(L0.ndofs(), kB), L0.imap(), nev, d_cp, 1, c0.get());
   w.full.ensure(nd * nr);
   prolong_chain(c, nr, c0.get(), 0, level, w.full.get());
   NR_DISPATCH(nr, k_candidates, grid_for(nd, kB), nd, k, w.keep.get(), w.coef.get(), glued,
               w.full.get());
   w.mfull.ensure(nd * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), w.full.get(),
+  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), w.full.get(),
               nullptr, w.mfull.get());
   const auto q = mdot(c, nr, F, w.full.get(), w.mfull.get());
   Lam s{};
@@ -1254,14 +1302,14 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
   const long long nd = F.ndofs();
   w.au.ensure(nd * nr);
   w.bu.ensure(nd * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), glued,
+  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), glued,
               w.au.get(), w.bu.get());
   const double* a0 = restrict_chain(c, nr, w.au.get(), level, 0);
   const double* b0 = restrict_chain(c, nr, w.bu.get(), level, 1);
   w.a_cu.ensure(static_cast<std::size_t>(mc) * nr);
   w.b_cu.ensure(static_cast<std::size_t>(mc) * nr);
-  NR_DISPATCH(nr, k_gather_coarse, grid_for(mc, kB), L0.nx, L0.ny, a0, w.a_cu.get());
-  NR_DISPATCH(nr, k_gather_coarse, grid_for(mc, kB), L0.nx, L0.ny, b0, w.b_cu.get());
+  NR_DISPATCH(nr, k_gather_coarse, grid_for(mc, kB), L0.imap(), a0, w.a_cu.get());
+  NR_DISPATCH(nr, k_gather_coarse, grid_for(mc, kB), L0.imap(), b0, w.b_cu.get());
   w.coef.ensure(64);
   w.keep.ensure(8);
 
@@ -1378,7 +1426,7 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
 
   Timer t0(c.stream);
   w.res.ensure(nd * nr);
-  NR_DISPATCH(nr, k_residual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), w.u.get(),
+  NR_DISPATCH(nr, k_residual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), w.u.get(),
               w.u.get(), lam, w.res.get(), nullptr);
   std::vector<SolveReport> lrep;
   out.times.local_iters_max =
@@ -1393,7 +1441,7 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
   Timer t1(c.stream);
 
   w.glued.ensure(nd * nr);
-  NR_DISPATCH(nr, k_glue_cg, grid_for(nd, kB), F.nx, F.ny, part_dev(c, to), nev,
+  NR_DISPATCH(nr, k_glue_cg, grid_for(nd, kB), F.imap(), part_dev(c, to), nev,
               w.local.sys_dev(), w.local.x(), w.u.get(), w.glued.get());
   std::vector<SolveReport> srep;
   bool empty = false;
@@ -1410,7 +1458,7 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
 
   // matching diagnostic (corrector.cpp:383-399)
   w.mfull.ensure(nd * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.nx, F.ny, F.stA.get(), F.stM.get(), u_out.get(),
+  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), u_out.get(),
               nullptr, w.mfull.get());
   const auto m = mdot(c, nr, F, w.u.get(), w.mfull.get());
   out.matched = true;
@@ -1439,13 +1487,13 @@ const CgBatch& local_batch(Ctx& c) { return W(c).local; }
 
 void interleave(Ctx& c, const Level& L, int nr, int k_in, const double* src, int interior_src,
                 double* dst) {
-  NR_DISPATCH(nr, k_interleave, grid_for(L.ndofs(), kB), L.nx, L.ny, k_in, src, interior_src,
+  NR_DISPATCH(nr, k_interleave, grid_for(L.ndofs(), kB), L.imap(), k_in, src, interior_src,
               dst);
 }
 
 void deinterleave(Ctx& c, const Level& L, int nr, int k_out, const int* perm, const double* src,
                   int interior_dst, double* dst) {
-  NR_DISPATCH(nr, k_deinterleave, grid_for(L.ndofs(), kB), L.nx, L.ny, k_out, perm, src,
+  NR_DISPATCH(nr, k_deinterleave, grid_for(L.ndofs(), kB), L.imap(), k_out, perm, src,
               interior_dst, dst);
 }
 
@@ -1479,14 +1527,14 @@ void restrict_levels(Ctx& c, int nr, const double* src, int from, int to, double
       bufs[k & 1]->ensure(C.ndofs() * nr);
       out = bufs[k & 1]->get();
     }
-    NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, cur, out);
+    NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, F.hole, cur, out);
     cur = out;
   }
 }
 
 void glue_full(Ctx& c, int level, const double* corr, const double* u, double* glued) {
   const Level& F = c.level(level);
-  k_glue_full<<<grid_for(F.ndofs(), kB), kB, 0, c.stream>>>(F.nx, F.ny, part_dev(c, level),
+  k_glue_full<<<grid_for(F.ndofs(), kB), kB, 0, c.stream>>>(F.imap(), part_dev(c, level),
                                                            F.ndofs(), corr, u, glued);
   MLG_LAUNCH_CHECK();
 }
@@ -1494,7 +1542,7 @@ void glue_full(Ctx& c, int level, const double* corr, const double* u, double* g
 void residual(Ctx& c, const Level& F, int nr, const double* u, const double* lam, double* out) {
   Lam l{};
   for (int r = 0; r < nr; ++r) l.v[r] = lam[r];
-  NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.nx, F.ny, F.stA.get(), F.stM.get(), u,
+  NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.imap(), F.stA.get(), F.stM.get(), u,
               u, l, out, nullptr);
 }
 

@@ -19,6 +19,7 @@
 
 #include <cusolverDn.h>
 
+#include <algorithm>
 #include <memory>
 #include <string>
 #include <vector>
@@ -37,6 +38,101 @@ struct StripGeom {
   int side = 1, bw = 1, bh = 1, dc = 0, nx0 = 1, ny0 = 1, scale = 1;
 };
 
+// A rectangular hole [x0, x1) x [y0, y1) (lattice cells of one level) cut at
+// a corner of the bounding rectangle: the L-shaped domains of BASELINE config 3
+// (a B200 extension; the reference meshes rectangles only).  x1 == 0 means no
+// hole.  Everything stays on the bounding lattice: lattice points strictly
+// inside the hole belong to no element ("inactive" dofs, always zero, empty
+// rows); points on the hole's edges are Dirichlet boundary.
+struct Hole {
+  int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+  __host__ __device__ bool any() const { return x1 > x0; }
+  __host__ __device__ bool cell_in(int cx, int cy) const {
+    return cx >= x0 && cx < x1 && cy >= y0 && cy < y1;
+  }
+  __host__ __device__ Hole scaled(int s) const { return Hole{x0 * s, y0 * s, x1 * s, y1 * s}; }
+};
+
+// Cell (cx, cy) of an nx x ny lattice carries elements.
+__host__ __device__ __forceinline__ bool cell_active(const Hole& h, int nx, int ny, int cx,
+                                                     int cy) {
+  return cx >= 0 && cy >= 0 && cx < nx && cy < ny && !h.cell_in(cx, cy);
+}
+
+// Interior points and their row-major order (FeSpace::interior_dofs is
+// ascending in dof id = iy*(nx+1)+ix, fespace.cpp:290-310).  With a corner
+// hole every interior row is one contiguous x range, so the map is closed form.
+struct IMap {
+  int nx = 0, ny = 0;
+  Hole h;  // at this level's scale
+  // closed hole rows [bya, byb] (clamped to 1..ny-1) and their x range [bxa, bxb]
+  int bya = 1, byb = 0, bxa = 1, bxb = 0;
+  __host__ __device__ int wfull() const { return nx - 1; }
+  __host__ __device__ int wband() const { return bxb - bxa + 1; }
+  __host__ __device__ bool in_band(int iy) const { return iy >= bya && iy <= byb; }
+  __host__ __device__ bool interior(int ix, int iy) const {
+    if (ix <= 0 || iy <= 0 || ix >= nx || iy >= ny) return false;
+    return !in_band(iy) || (ix >= bxa && ix <= bxb);
+  }
+  // rows 1..iy-1 before row iy
+  __host__ __device__ long long prefix(int iy) const {
+    const long long full = static_cast<long long>(iy - 1) * wfull();
+    if (byb < bya) return full;
+    const int nb = max(0, min(iy - 1, byb) - bya + 1);  // band rows below iy
+    return full + static_cast<long long>(nb) * (wband() - wfull());
+  }
+  __host__ __device__ long long index(int ix, int iy) const {  // -1 if not interior
+    if (!interior(ix, iy)) return -1;
+    return prefix(iy) + (ix - (in_band(iy) ? bxa : 1));
+  }
+  __host__ __device__ long long count() const { return prefix(ny); }
+  __host__ __device__ void point(long long k, int* ix, int* iy) const {
+    // rows come in (at most) three runs: full rows below the band, band rows,
+    // full rows above the band
+    const int W = wfull();
+    if (byb < bya) {
+      *iy = static_cast<int>(k / W) + 1;
+      *ix = static_cast<int>(k % W) + 1;
+      return;
+    }
+    const long long below = static_cast<long long>(bya - 1) * W;
+    if (k < below) {
+      *iy = static_cast<int>(k / W) + 1;
+      *ix = static_cast<int>(k % W) + 1;
+      return;
+    }
+    const long long kb = k - below, nbw = static_cast<long long>(byb - bya + 1) * wband();
+    if (kb < nbw) {
+      *iy = bya + static_cast<int>(kb / wband());
+      *ix = bxa + static_cast<int>(kb % wband());
+      return;
+    }
+    const long long ka = kb - nbw;
+    *iy = byb + 1 + static_cast<int>(ka / W);
+    *ix = static_cast<int>(ka % W) + 1;
+  }
+};
+
+inline IMap make_imap(int nx, int ny, const Hole& h) {
+  IMap m;
+  m.nx = nx;
+  m.ny = ny;
+  m.h = h;
+  if (h.any()) {
+    // closed hole in points: [x0, x1] x [y0, y1]; interior rows it cuts
+    m.bya = std::max(h.y0, 1);
+    m.byb = std::min(h.y1, ny - 1);
+    if (h.x0 == 0) {  // hole on the left: band rows keep x in (x1, nx)
+      m.bxa = h.x1 + 1;
+      m.bxb = nx - 1;
+    } else {  // hole on the right
+      m.bxa = 1;
+      m.bxb = h.x0 - 1;
+    }
+  }
+  return m;
+}
+
 struct Config {
   double x_min = -1.0, x_max = 1.0, y_min = -1.0, y_max = 1.0;
   double H = 0.25;
@@ -52,6 +148,8 @@ struct Config {
   int deterministic = 1;
   int device = 0;
   unsigned long long seed = 0;  // example 2
+  // corner hole (coordinates; hole_x1 <= hole_x0 means none): L-shaped domain
+  double hole_x0 = 0.0, hole_x1 = 0.0, hole_y0 = 0.0, hole_y1 = 0.0;
 };
 
 // Example 2 coefficients: (k1, k2) = 1 + (splitmix64 outputs 1, 2 of seed) >> 62.
@@ -80,6 +178,10 @@ struct Partition {
   // contiguous descendant ranges [t*4^L, (t+1)*4^L) (children are 4t+c).
   std::vector<std::vector<int>> block_elems, overlap_elems, inner_elems;
   std::vector<int> strip_elems;
+  // block (bottom-up row rb, column c) -> subdomain j, -1 for blocks removed
+  // by a hole; the reference's order j = (side-1-rb)*side + c otherwise.
+  std::vector<int> blk2j;
+  int nt0 = 0;  // level-0 elements
 };
 
 struct Level {
@@ -100,8 +202,17 @@ struct Level {
   Stencil ust{0.0, 0.0, 0.0, 0.0};
   double udinv = 0.0;
 
+  Hole hole;  // in this level's cells (none for rectangles)
+  IMap imap() const { return make_imap(nx, ny, hole); }
+  // CG operator for domains with a hole: the interior restriction of A with
+  // identity rows at non-interior points (see corrector.cu ensure_cg_stencil).
+  DevBuf<Stencil> stCG;
+  DevBuf<double> dinvCG;
+
   std::int64_t ndofs() const { return static_cast<std::int64_t>(nx + 1) * (ny + 1); }
-  std::int64_t nint() const { return static_cast<std::int64_t>(nx - 1) * (ny - 1); }
+  std::int64_t nint() const {
+    return hole.any() ? imap().count() : static_cast<std::int64_t>(nx - 1) * (ny - 1);
+  }
 };
 
 struct StepTimes {

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kEB) k_errors(ErrGeom G, ExactMode md, const d
     const int upper = static_cast<int>(t & 1);
     const long long cell = t >> 1;
     const int cx = static_cast<int>(cell % G.nx), cy = static_cast<int>(cell / G.nx);
+    if (G.geo[t] == 0xFFFFFFFFu) continue;  // removed cell (domain with a hole)
     const int rot = static_cast<int>(G.geo[t] & 3u);
     double vx[3], vy[3], c[3];
 #pragma unroll
@@ -258,6 +259,32 @@ ReferenceSet make_reference(int example, int nev, const double* domain) {
   }
   if (example == 2) throw ConfigError("no reference data for example \"reaction\"");
   throw ConfigError("no reference data for example id " + std::to_string(example));
+}
+
+// Reference set of a configuration: make_reference on the configured
+// rectangle, or -- for the L-shaped domain (-1,1)^2 minus a unit corner
+// quadrant (BASELINE config 3, B200 extension) -- its well-known spectrum
+// lambda = 9.6397238440, 15.1972519265, 2 pi^2, 29.5214811153, 31.9126359570
+// (the corner singularity leaves only lambda_3 with a closed form,
+// sin(pi x) sin(pi y), b-normalised on the L by sqrt(4/3)).
+ReferenceSet make_reference_for(const Config& cfg, int nev) {
+  const double dom[4] = {cfg.x_min, cfg.x_max, cfg.y_min, cfg.y_max};
+  if (!(cfg.hole_x1 > cfg.hole_x0)) return make_reference(cfg.example, nev, dom);
+  const bool square = cfg.x_min == -1.0 && cfg.x_max == 1.0 && cfg.y_min == -1.0 &&
+                      cfg.y_max == 1.0;
+  const bool quadrant = cfg.hole_x1 - cfg.hole_x0 == 1.0 && cfg.hole_y1 - cfg.hole_y0 == 1.0;
+  if (cfg.example != 0 || !square || !quadrant)
+    throw ConfigError("no reference data for this domain with a hole");
+  constexpr double kPi = 3.14159265358979323846;
+  const std::vector<double> table = {9.6397238440219, 15.1972519265, 2.0 * kPi * kPi,
+                                     29.5214811153, 31.9126359570};
+  if (nev > static_cast<int>(table.size()))
+    throw ConfigError("reference eigenvalues for the L-shaped domain cover 5 modes only");
+  ReferenceSet r;
+  r.lambdas.assign(table.begin(), table.begin() + nev);
+  r.modes.assign(static_cast<std::size_t>(nev), ExactMode{});
+  if (nev > 2) r.modes[2] = ExactMode{2, 2, -1.0, 2.0, -1.0, 2.0, std::sqrt(4.0 / 3.0)};
+  return r;
 }
 
 }  // namespace mlg

@@ -33,4 +33,8 @@ ErrorReport compute_errors(Ctx& c, const Level& L, const double* d_coeffs, int s
 // or nullptr for the reference's (-1,1)^2 table.
 ReferenceSet make_reference(int example, int nev, const double* domain);
 
+// The reference set a configuration's experiment reports against (adds the
+// L-shaped domain's table).
+ReferenceSet make_reference_for(const Config& cfg, int nev);
+
 }  // namespace mlg

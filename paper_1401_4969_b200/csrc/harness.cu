@@ -386,10 +386,9 @@ struct Ctx {  // RAII over mlg_create / mlg_destroy
 std::vector<mlg_report_row> experiment_rows(const mlg_config& cfg) {
   validate(cfg);
   const int nev = cfg.nev, nl = cfg.n_levels;
-  const double dom[4] = {cfg.x_min, cfg.x_max, cfg.y_min, cfg.y_max};
   std::vector<double> ref_l(static_cast<std::size_t>(nev));
   std::vector<mlg_exact_mode> ref_m(static_cast<std::size_t>(nev));
-  ok(mlg_make_reference(cfg.example, nev, dom, ref_l.data(), ref_m.data()));
+  ok(mlg_make_reference_for(&cfg, nev, ref_l.data(), ref_m.data()));
   Ctx ctx(cfg);
   ok(mlg_extend_to(ctx.h, nl));
   const std::size_t nn = static_cast<std::size_t>(nl) * nev;

@@ -63,6 +63,102 @@ __global__ void k_level0_triangles(int nx, int ny, int* tri, unsigned* geo) {
   geo[2 * c + 1] = static_cast<unsigned>(2 * c + 1) << 2;
 }
 
+// ---- level 0 of a domain with a corner hole (B200 extension, config 3) ----
+// Vertices: the lattice points touching an element, lexicographic (y, x) --
+// the order build_structured_mesh uses for rectangles (mesh.cpp:80-90);
+// triangles: two per element-carrying cell, cells lexicographic, the same
+// split {v00,v10,v11},{v00,v11,v01} (mesh.cpp:96-97).
+__device__ __forceinline__ bool point_active(const Hole& h, int nx, int ny, int ix, int iy) {
+  return cell_active(h, nx, ny, ix, iy) || cell_active(h, nx, ny, ix - 1, iy) ||
+         cell_active(h, nx, ny, ix, iy - 1) || cell_active(h, nx, ny, ix - 1, iy - 1);
+}
+
+__global__ void k_hole_flags(int nx, int ny, Hole h, int* pflag, int* cflag) {
+  const std::int64_t v = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t np = static_cast<std::int64_t>(nx + 1) * (ny + 1);
+  if (v < np) {
+    const int ix = static_cast<int>(v % (nx + 1)), iy = static_cast<int>(v / (nx + 1));
+    pflag[v] = point_active(h, nx, ny, ix, iy) ? 1 : 0;
+  }
+  if (v < static_cast<std::int64_t>(nx) * ny) {
+    const int cx = static_cast<int>(v % nx), cy = static_cast<int>(v / nx);
+    cflag[v] = cell_active(h, nx, ny, cx, cy) ? 1 : 0;
+  }
+}
+
+__global__ void k_level0_hole(int nx, int ny, Hole h, double x0, double y0, double dx,
+                              double dy, const int* prank, const int* crank, int* lat,
+                              double* xy, int* vid, int* tri, unsigned* geo) {
+  const std::int64_t v = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t np = static_cast<std::int64_t>(nx + 1) * (ny + 1);
+  if (v < np) {
+    const int ix = static_cast<int>(v % (nx + 1)), iy = static_cast<int>(v / (nx + 1));
+    if (point_active(h, nx, ny, ix, iy)) {
+      const int id = prank[v];
+      lat[2 * id] = ix;
+      lat[2 * id + 1] = iy;
+      xy[2 * id] = lattice_coord(x0, ix, dx);
+      xy[2 * id + 1] = lattice_coord(y0, iy, dy);
+      vid[v] = id;
+    } else {
+      vid[v] = -1;
+    }
+  }
+  if (v < static_cast<std::int64_t>(nx) * ny) {
+    const int cx = static_cast<int>(v % nx), cy = static_cast<int>(v / nx);
+    if (!cell_active(h, nx, ny, cx, cy)) {
+      geo[2 * v] = geo[2 * v + 1] = 0xFFFFFFFFu;
+      return;
+    }
+    const std::int64_t r = crank[v];
+    const std::int64_t p00 = static_cast<std::int64_t>(cy) * (nx + 1) + cx;
+    const int v00 = prank[p00], v10 = prank[p00 + 1], v01 = prank[p00 + nx + 1],
+              v11 = prank[p00 + nx + 2];
+    int* t = tri + 6 * r;
+    t[0] = v00;
+    t[1] = v10;
+    t[2] = v11;
+    t[3] = v00;
+    t[4] = v11;
+    t[5] = v01;
+    geo[2 * v] = static_cast<unsigned>(2 * r) << 2;
+    geo[2 * v + 1] = static_cast<unsigned>(2 * r + 1) << 2;
+  }
+}
+
+// Boundary edges of a domain with a hole: lattice edges with exactly one
+// element-carrying cell beside them (count-1 edges, mesh.cpp:50-64).  Keys are
+// appended in any order; k_rank_keys then orders them like std::map.
+__global__ void k_boundary_keys_hole(int nx, int ny, Hole h, const int* vid, std::int64_t nv,
+                                     long long* keys, int* n_out) {
+  const std::int64_t e = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t nh = static_cast<std::int64_t>(nx) * (ny + 1);
+  const std::int64_t nvv = static_cast<std::int64_t>(nx + 1) * ny;
+  if (e >= nh + nvv) return;
+  int ax, ay, bx, by;
+  bool c1, c2;
+  if (e < nh) {  // horizontal (ax,ay)-(ax+1,ay): cells below / above
+    ax = static_cast<int>(e % nx);
+    ay = static_cast<int>(e / nx);
+    bx = ax + 1;
+    by = ay;
+    c1 = cell_active(h, nx, ny, ax, ay - 1);
+    c2 = cell_active(h, nx, ny, ax, ay);
+  } else {  // vertical (ax,ay)-(ax,ay+1): cells left / right
+    const std::int64_t f = e - nh;
+    ax = static_cast<int>(f % (nx + 1));
+    ay = static_cast<int>(f / (nx + 1));
+    bx = ax;
+    by = ay + 1;
+    c1 = cell_active(h, nx, ny, ax - 1, ay);
+    c2 = cell_active(h, nx, ny, ax, ay);
+  }
+  if (c1 == c2) return;
+  const long long u = vid[static_cast<std::int64_t>(ay) * (nx + 1) + ax];
+  const long long w = vid[static_cast<std::int64_t>(by) * (nx + 1) + bx];
+  keys[atomicAdd(n_out, 1)] = (u < w) ? u * nv + w : w * nv + u;
+}
+
 // Position of a triangle (given its vertex lattices in element order) on the
 // lattice: cell, L/U type and the rotation rot with t[k] = canonical[(rot+k)%3].
 __device__ __forceinline__ unsigned geo_slot(int x0, int y0, int x1, int y1, int x2, int y2,
@@ -115,8 +211,24 @@ __global__ void k_ref_parent_verts(std::int64_t nv, const int* lat_c, int nxf, d
   vid_f[static_cast<std::int64_t>(iy) * (nxf + 1) + ix] = static_cast<int>(v);
 }
 
+// The lattice edge from (ix,iy) in direction d (E, W, N, S, NE, SW) is a mesh
+// edge iff one of the cells containing it carries elements (with a corner
+// hole two active points can face each other across a removed cell).
+__device__ __forceinline__ bool edge_exists(const Hole& h, int nx, int ny, int ix, int iy,
+                                            int d) {
+  if (!h.any()) return true;
+  switch (d) {
+    case 0: return cell_active(h, nx, ny, ix, iy) || cell_active(h, nx, ny, ix, iy - 1);
+    case 1: return cell_active(h, nx, ny, ix - 1, iy) || cell_active(h, nx, ny, ix - 1, iy - 1);
+    case 2: return cell_active(h, nx, ny, ix, iy) || cell_active(h, nx, ny, ix - 1, iy);
+    case 3: return cell_active(h, nx, ny, ix, iy - 1) || cell_active(h, nx, ny, ix - 1, iy - 1);
+    case 4: return cell_active(h, nx, ny, ix, iy);
+    default: return cell_active(h, nx, ny, ix - 1, iy - 1);
+  }
+}
+
 __global__ void k_ref_count(std::int64_t nv, const int* lat_c, const int* vid_c, int nxc,
-                            int nyc, int* count) {
+                            int nyc, Hole hc, int* count) {
   const std::int64_t a = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
   if (a >= nv) return;
   const int ix = lat_c[2 * a], iy = lat_c[2 * a + 1];
@@ -125,6 +237,7 @@ __global__ void k_ref_count(std::int64_t nv, const int* lat_c, const int* vid_c,
   for (int d = 0; d < 6; ++d) {
     const int jx = ix + kNbDx[d], jy = iy + kNbDy[d];
     if (jx < 0 || jy < 0 || jx > nxc || jy > nyc) continue;
+    if (!edge_exists(hc, nxc, nyc, ix, iy, d)) continue;
     if (vid_c[static_cast<std::int64_t>(jy) * (nxc + 1) + jx] > a) ++cnt;
   }
   count[a] = cnt;
@@ -132,7 +245,7 @@ __global__ void k_ref_count(std::int64_t nv, const int* lat_c, const int* vid_c,
 
 // Midpoint ids: V + rank in ascending (min*nv+max) order (mesh.cpp:121-135).
 __global__ void k_ref_midpoints(std::int64_t nv, const int* lat_c, const int* vid_c, int nxc,
-                                int nyc, const int* off, int nxf, double x0, double y0,
+                                int nyc, Hole hc, const int* off, int nxf, double x0, double y0,
                                 double dxf, double dyf, int* lat_f, double* xy_f, int* vid_f) {
   const std::int64_t a = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
   if (a >= nv) return;
@@ -142,6 +255,7 @@ __global__ void k_ref_midpoints(std::int64_t nv, const int* lat_c, const int* vi
   for (int d = 0; d < 6; ++d) {
     const int jx = ix + kNbDx[d], jy = iy + kNbDy[d];
     if (jx < 0 || jy < 0 || jx > nxc || jy > nyc) continue;
+    if (!edge_exists(hc, nxc, nyc, ix, iy, d)) continue;
     const int b = vid_c[static_cast<std::int64_t>(jy) * (nxc + 1) + jx];
     if (b <= a) continue;
     // insertion by id
@@ -255,6 +369,30 @@ __global__ void k_rank_keys(const long long* keys, int n, std::int64_t nv, int* 
 }
 
 void boundary_edges(Ctx& c, Level& L) {
+  if (L.hole.any()) {
+    // outer boundary + the two inner sides of the hole (the hole touches one
+    // corner, so the count is the rectangle's)
+    const int nb = 2 * (L.nx + L.ny);
+    L.nb = nb;
+    L.bedges.alloc(2 * static_cast<std::size_t>(nb));
+    DevBuf<long long> keys(nb);
+    DevBuf<int> n(1);
+    n.zero(c.stream);
+    const std::int64_t ne = static_cast<std::int64_t>(L.nx) * (L.ny + 1) +
+                            static_cast<std::int64_t>(L.nx + 1) * L.ny;
+    k_boundary_keys_hole<<<grid_for(ne, kBlock), kBlock, 0, c.stream>>>(
+        L.nx, L.ny, L.hole, L.vid.get(), L.nv, keys.get(), n.get());
+    MLG_LAUNCH_CHECK();
+    int got = 0;
+    n.download(&got, 1, c.stream);
+    c.sync();
+    if (got != nb) throw SolverError("boundary of the L-shaped mesh has an unexpected length");
+    k_rank_keys<<<grid_for(nb, kBlock), kBlock, 0, c.stream>>>(keys.get(), nb, L.nv,
+                                                              L.bedges.get());
+    MLG_LAUNCH_CHECK();
+    c.sync();
+    return;
+  }
   const int nb = 2 * (L.nx + L.ny);
   L.nb = nb;
   L.bedges.alloc(2 * static_cast<std::size_t>(nb));
@@ -273,14 +411,14 @@ __global__ void k_dof_lattice(int nx, int ny, int* dof_lattice) {
   dof_lattice[2 * d + 1] = 2 * static_cast<int>(d / (nx + 1));
 }
 
-__global__ void k_interior_lists(int nx, int ny, int* interior_dofs, int* interior_index) {
+__global__ void k_interior_lists(IMap m, int* interior_dofs, int* interior_index) {
+  const int nx = m.nx, ny = m.ny;
   const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<std::int64_t>(nx + 1) * (ny + 1)) return;
   const int ix = static_cast<int>(d % (nx + 1)), iy = static_cast<int>(d / (nx + 1));
-  const bool interior = ix > 0 && iy > 0 && ix < nx && iy < ny;
-  const int k = interior ? (iy - 1) * (nx - 1) + (ix - 1) : -1;
-  if (interior_index) interior_index[d] = k;
-  if (interior && interior_dofs) interior_dofs[k] = static_cast<int>(d);
+  const long long k = m.index(ix, iy);
+  if (interior_index) interior_index[d] = static_cast<int>(k);
+  if (k >= 0 && interior_dofs) interior_dofs[k] = static_cast<int>(d);
 }
 
 __global__ void k_connectivity(std::int64_t nt, const int* tri, const int* lat, int nx,
@@ -294,6 +432,30 @@ __global__ void k_connectivity(std::int64_t nt, const int* tri, const int* lat, 
 }
 
 }  // namespace
+
+// The config's corner hole in coarse cells (aligned to H, touching exactly one
+// corner of the bounding rectangle, strictly smaller in both directions).
+Hole hole_cells(const Config& cfg, int nx, int ny) {
+  if (!(cfg.hole_x1 > cfg.hole_x0) && !(cfg.hole_y1 > cfg.hole_y0)) return Hole{};
+  auto cell = [&](double v, double lo, int n, const char* what) {
+    const double r = (v - lo) / cfg.H;
+    const int k = static_cast<int>(std::lround(r));
+    if (std::abs(r - k) > 1e-9 * std::max(1.0, std::abs(r)) || k < 0 || k > n)
+      throw ConfigError(std::string("hole ") + what + " is not on the coarse lattice");
+    return k;
+  };
+  Hole h;
+  h.x0 = cell(cfg.hole_x0, cfg.x_min, nx, "x_min");
+  h.x1 = cell(cfg.hole_x1, cfg.x_min, nx, "x_max");
+  h.y0 = cell(cfg.hole_y0, cfg.y_min, ny, "y_min");
+  h.y1 = cell(cfg.hole_y1, cfg.y_min, ny, "y_max");
+  if (!(h.x1 > h.x0) || !(h.y1 > h.y0))
+    throw ConfigError("hole rectangle must have positive side lengths");
+  const bool cx = (h.x0 == 0) != (h.x1 == nx), cy = (h.y0 == 0) != (h.y1 == ny);
+  if (!cx || !cy)
+    throw ConfigError("hole must touch exactly one corner of the domain rectangle (L-shape)");
+  return h;
+}
 
 void build_level0(Ctx& c) {
   auto L = std::make_unique<Level>();
@@ -315,6 +477,45 @@ void build_level0(Ctx& c) {
   L->ny = cells(cfg.y_max - cfg.y_min, cfg.H, "y");
   L->dx = (cfg.x_max - cfg.x_min) / L->nx;
   L->dy = (cfg.y_max - cfg.y_min) / L->ny;
+  L->hole = hole_cells(cfg, L->nx, L->ny);
+  if (L->hole.any()) {
+    const std::int64_t np = L->ndofs(), ncell = static_cast<std::int64_t>(L->nx) * L->ny;
+    DevBuf<int> pflag(np + 1), cflag(ncell + 1), prank(np + 1), crank(ncell + 1);
+    pflag.zero(c.stream);
+    cflag.zero(c.stream);
+    k_hole_flags<<<grid_for(np, kBlock), kBlock, 0, c.stream>>>(L->nx, L->ny, L->hole,
+                                                               pflag.get(), cflag.get());
+    MLG_LAUNCH_CHECK();
+    std::size_t tb1 = 0, tb2 = 0;
+    MLG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb1, pflag.get(), prank.get(),
+                                           static_cast<int>(np + 1), c.stream));
+    MLG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cflag.get(), crank.get(),
+                                           static_cast<int>(ncell + 1), c.stream));
+    void* tmp = c.scratch_bytes(std::max(tb1, tb2));
+    MLG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb1, pflag.get(), prank.get(),
+                                           static_cast<int>(np + 1), c.stream));
+    int nvh = 0, nch = 0;
+    MLG_CUDA(cudaMemcpyAsync(&nvh, prank.get() + np, sizeof(int), cudaMemcpyDeviceToHost,
+                             c.stream));
+    c.sync();
+    MLG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb2, cflag.get(), crank.get(),
+                                           static_cast<int>(ncell + 1), c.stream));
+    MLG_CUDA(cudaMemcpyAsync(&nch, crank.get() + ncell, sizeof(int), cudaMemcpyDeviceToHost,
+                             c.stream));
+    c.sync();
+    L->nv = nvh;
+    L->nt = 2LL * nch;
+    L->lat.alloc(2 * L->nv);
+    L->xy.alloc(2 * L->nv);
+    L->vid.alloc(np);
+    L->tri.alloc(3 * L->nt);
+    L->geo.alloc(2 * ncell);
+    k_level0_hole<<<grid_for(np, kBlock), kBlock, 0, c.stream>>>(
+        L->nx, L->ny, L->hole, cfg.x_min, cfg.y_min, L->dx, L->dy, prank.get(), crank.get(),
+        L->lat.get(), L->xy.get(), L->vid.get(), L->tri.get(), L->geo.get());
+    MLG_LAUNCH_CHECK();
+    c.sync();
+  } else {
   L->nv = L->ndofs();
   L->nt = 2LL * L->nx * L->ny;
   L->lat.alloc(2 * L->nv);
@@ -328,6 +529,7 @@ void build_level0(Ctx& c) {
   k_level0_triangles<<<grid_for(static_cast<std::int64_t>(L->nx) * L->ny, kBlock), kBlock, 0,
                        c.stream>>>(L->nx, L->ny, L->tri.get(), L->geo.get());
   MLG_LAUNCH_CHECK();
+  }
   boundary_edges(c, *L);
   auto* hm = static_cast<double*>(c.scratch_bytes(sizeof(double)));
   MLG_CUDA(cudaMemsetAsync(hm, 0, sizeof(double), c.stream));
@@ -346,15 +548,25 @@ void refine_level(Ctx& c, const Level& C, Level& F) {
   F.dx = (c.cfg.x_max - c.cfg.x_min) / F.nx;
   F.dy = (c.cfg.y_max - c.cfg.y_min) / F.ny;
   F.nt = 4 * C.nt;
-  const std::int64_t nvf_max = F.ndofs();
+  F.hole = C.hole.scaled(2);
+  std::int64_t nvf_max = F.ndofs();
+  if (F.hole.any()) {  // lattice points strictly inside the hole carry no vertex
+    const std::int64_t ix = F.hole.x0 == 0 ? F.hole.x1 : F.nx - F.hole.x0;
+    const std::int64_t iy = F.hole.y0 == 0 ? F.hole.y1 : F.ny - F.hole.y0;
+    nvf_max -= ix * iy;
+  }
   if (F.nt >= (1LL << 30) || nvf_max >= (1LL << 31))
     throw ConfigError("refined mesh exceeds the 32-bit index range of the reference layout");
   F.lat.alloc(2 * nvf_max);
   F.xy.alloc(2 * nvf_max);
-  F.vid.alloc(nvf_max);
+  F.vid.alloc(F.ndofs());
   F.tri.alloc(3 * F.nt);
   F.parent.alloc(F.nt);
-  F.geo.alloc(F.nt);
+  F.geo.alloc(2LL * F.nx * F.ny);
+  if (F.hole.any()) {  // absent points / cells
+    MLG_CUDA(cudaMemsetAsync(F.vid.get(), 0xFF, sizeof(int) * F.ndofs(), c.stream));
+    MLG_CUDA(cudaMemsetAsync(F.geo.get(), 0xFF, sizeof(unsigned) * 2 * F.nx * F.ny, c.stream));
+  }
 
   const std::int64_t nv = C.nv;
   k_ref_parent_verts<<<grid_for(nv, kBlock), kBlock, 0, c.stream>>>(
@@ -365,7 +577,7 @@ void refine_level(Ctx& c, const Level& C, Level& F) {
   // count + exclusive scan (cub) -> edge ranks grouped by the min endpoint
   DevBuf<int> count(nv + 1), off(nv + 1);
   k_ref_count<<<grid_for(nv, kBlock), kBlock, 0, c.stream>>>(nv, C.lat.get(), C.vid.get(), C.nx,
-                                                            C.ny, count.get());
+                                                            C.ny, C.hole, count.get());
   MLG_LAUNCH_CHECK();
   MLG_CUDA(cudaMemsetAsync(count.get() + nv, 0, sizeof(int), c.stream));
   std::size_t tmp_bytes = 0;
@@ -383,7 +595,7 @@ void refine_level(Ctx& c, const Level& C, Level& F) {
     throw SolverError("refinement produced a non-lattice vertex set (" + std::to_string(F.nv) +
                       " vs " + std::to_string(nvf_max) + ")");
   k_ref_midpoints<<<grid_for(nv, kBlock), kBlock, 0, c.stream>>>(
-      nv, C.lat.get(), C.vid.get(), C.nx, C.ny, off.get(), F.nx, c.cfg.x_min, c.cfg.y_min, F.dx,
+      nv, C.lat.get(), C.vid.get(), C.nx, C.ny, C.hole, off.get(), F.nx, c.cfg.x_min, c.cfg.y_min, F.dx,
       F.dy, F.lat.get(), F.xy.get(), F.vid.get());
   MLG_LAUNCH_CHECK();
 
@@ -421,7 +633,7 @@ void export_space(Ctx& c, const Level& L, int* dof_lattice, int* interior_dofs,
   if (interior_dofs || interior_index) {
     DevBuf<int> di(L.nint()), ii(nd);
     k_interior_lists<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(
-        L.nx, L.ny, interior_dofs ? di.get() : nullptr, interior_index ? ii.get() : nullptr);
+        L.imap(), interior_dofs ? di.get() : nullptr, interior_index ? ii.get() : nullptr);
     MLG_LAUNCH_CHECK();
     if (interior_dofs) di.download(interior_dofs, L.nint(), c.stream);
     if (interior_index) ii.download(interior_index, nd, c.stream);

@@ -23,7 +23,9 @@ def _config_from_c(c: MlgConfig) -> RunConfig:
     return RunConfig(domain=DomainRect(c.x_min, c.x_max, c.y_min, c.y_max), H=c.H,
                      delta=c.delta, m=c.m, n_levels=c.n_levels, degree=c.degree, nev=c.nev,
                      example=EXAMPLES[c.example], cg_tol=c.cg_tol, workers=c.workers,
-                     deterministic=bool(c.deterministic), device=c.device, seed=c.seed)
+                     deterministic=bool(c.deterministic), device=c.device, seed=c.seed,
+                     hole=(DomainRect(c.hole_x_min, c.hole_x_max, c.hole_y_min, c.hole_y_max)
+                           if c.hole_x_max > c.hole_x_min else None))
 
 
 def parse_config_json(text: str) -> RunConfig:  # harness.cpp:58-102
@@ -87,6 +89,18 @@ def make_reference(example: str, nev: int, domain: DomainRect | None = None) -> 
     dom = None if domain is None else _f64([domain.x_min, domain.x_max, domain.y_min,
                                             domain.y_max])
     check(lib().mlg_make_reference(EXAMPLES.index(example), nev, _dp(dom), _dp(lam), modes))
+    fns = {i: ExactFunction(m.mx, m.my, m.x0, m.lx, m.y0, m.ly, m.amp)
+           for i, m in enumerate(modes) if m.mx > 0}
+    return ReferenceSet(lam.tolist(), fns)
+
+
+def make_reference_for(config: RunConfig, nev: int) -> ReferenceSet:
+    """The reference set run_experiment reports against for `config` (the
+    configured rectangle's table, or the L-shaped domain's for config 3)."""
+    cfg = config.to_c()
+    lam = np.empty(nev)
+    modes = (MlgExactMode * nev)()
+    check(lib().mlg_make_reference_for(C.byref(cfg), nev, _dp(lam), modes))
     fns = {i: ExactFunction(m.mx, m.my, m.x0, m.lx, m.y0, m.ly, m.amp)
            for i, m in enumerate(modes) if m.mx > 0}
     return ReferenceSet(lam.tolist(), fns)

@@ -99,6 +99,28 @@ def reaction_run(domain, H, delta, m, levels, nev, seed):
             "generator": "oracle/restate.py", "seconds": time.time() - t}
 
 
+LSHAPE_HOLE = (0.0, 1.0, -1.0, 0.0)  # (-1,1)^2 minus [0,1] x [-1,0]
+
+
+def lshape_run(H, delta, m, levels, nev):
+    from oracle import restate as R
+    t = time.time()
+    hy = R.Hierarchy(domain=SQUARE, H=H, delta=delta, m=m, n_levels=levels, nev=nev,
+                     hole=LSHAPE_HOLE)
+    lams, state = R.multilevel_correction(hy)
+    co = np.stack([v for _, v in state])
+    lv = hy.levels[levels]
+    me = lv.mesh
+    f = ref.fnv1a64
+    return {"config": dict(domain=SQUARE, hole=LSHAPE_HOLE, H=H, delta=delta, m=m,
+                           n_levels=levels, nev=nev),
+            "lambdas": np.asarray(lams).tolist(), "projections": projections(co),
+            "mesh": f(me.triangles, me.vertices, me.parent, me.boundary_edges),
+            "csr": [f(lv.A[0]), f(lv.A[1]), f(lv.A[2]), f(lv.M[2])],
+            "interior_dofs": f(lv.space.interior_dofs), "n_sub": hy.part.m,
+            "generator": "oracle/restate.py", "seconds": time.time() - t}
+
+
 def variable_values():
     """Variable-field operator values at (-1,1)^2, H=0.25, level 3: exact digests
     (for the record: exp() differs between libms, so consumers compare values to
@@ -177,6 +199,16 @@ def main():
         if name not in g["multilevel"]:
             g["multilevel"][name] = multilevel(name, dom, H, d, m, L, nev, save_vec=vec,
                                                example=1)
+            path.write_text(json.dumps(g, indent=1))
+    # L-shaped domain (BASELINE config 3): no reference code path; fixtures from
+    # the numpy restatement (oracle/restate.py, B200 definitions) -- parity
+    # unpinned against the reference, pinned against our own restatement.
+    g.setdefault("lshape", {})
+    for name, (H, d, m, L, nev) in {"H8_L3_m16_nev3": (1 / 8, 1 / 8, 16, 3, 3),
+                                    "H8_L4_m16_nev1": (1 / 8, 1 / 8, 16, 4, 1)}.items():
+        if name not in g["lshape"]:
+            g["lshape"][name] = lshape_run(H, d, m, L, nev)
+            print("lshape", name, g["lshape"][name]["lambdas"][-1], flush=True)
             path.write_text(json.dumps(g, indent=1))
     if "variable_values" not in g:
         g["variable_values"] = variable_values()
