@@ -2,7 +2,7 @@
 """Benchmark of the B200 correction step (BASELINE.json metric: fine-grid DOF/s
 per correction step; local-solve SpMV HBM GB/s vs B200 peak).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c4|c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4|c5]
     python bench.py --impl reference ...        # the reference's CPU path (oracle/_ref)
 
 A "step" is one correction step L-1 -> L (one_correction_step,
@@ -40,6 +40,13 @@ WORKLOADS = {
                     "32x32 coarse squares, 7 levels (4096^2 cells), 8x8 overlapping subdomains, "
                     "delta=1/32, nev=4; step level 6 -> 7",
                H=1 / 32, delta=1 / 32, m=64, n_levels=7, nev=4),
+    "c3": dict(desc="config 3 (B200 extension, no reference code path): L-shaped domain "
+                    "(-1,1)^2 minus [0,1]x[-1,0], Laplace P1 FP64, 3 unit squares of 16x16 "
+                    "cells (768 coarse triangles), 6 levels (3.1M fine triangles), 48 "
+                    "subdomains on the 8x8 block grid clipped to the domain, delta = 1 coarse "
+                    "cell, nev=1; step level 5 -> 6",
+               domain=(-1.0, 1.0, -1.0, 1.0), hole=(0.0, 1.0, -1.0, 0.0),
+               H=1 / 16, delta=1 / 16, m=64, n_levels=6, nev=1),
     "c4": dict(desc="config 4 (reference-valid partition m=16): unit square, "
                     "-div(a grad u) + c u = lambda u, a = 1 + 0.5 sin(2 pi k1 x) sin(2 pi k2 y), "
                     "c = 1 + x^2 + y^2 at centroids, (k1,k2) = (4,2) from seed 0, P1 FP64, "
@@ -191,9 +198,10 @@ def run_reference(args, ws, rank):
         return
     wl = WORKLOADS[args.workload]
     cores = os.cpu_count() or 1
-    if wl.get("example", "laplace") == "reaction":
+    if wl.get("example", "laplace") == "reaction" or wl.get("hole"):
         print(json.dumps({"impl": "reference", "unavailable": "the reference has no code path "
-                          "for config 4's reaction/centroid-coefficient field"}))
+                          "for this workload (config 3's L-shaped mesh / config 4's "
+                          "reaction/centroid-coefficient field)"}))
         return
     try:
         from oracle import ref
@@ -225,13 +233,6 @@ def run_reference(args, ws, rank):
                               "aug": statistics.mean(s[2] for s in r["splits"]),
                               "level_build": r["build_s"], "region_systems": r["regions_s"]},
     }
-    if extra4:
-        line["config4_workload"] = {
-            "workload": WORKLOADS["c4"]["desc"], "value": extra4["value"], "unit": "DOF/s",
-            "ms_per_step": extra4["ms_per_step"], "n_interior": extra4["n_int"],
-            "level_build_s": extra4["build_s"], "timings": extra4["timings"],
-            "roofline": extra4.get("roofline"), "lambdas": extra4["lam"],
-            "clocks": extra4["clocks"]}
     print(json.dumps(line), flush=True)
 
 
@@ -248,9 +249,11 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
     L, nev = wl["n_levels"], wl["nev"]
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    cfg = mlg.RunConfig(domain=mlg.DomainRect(0.0, 1.0, 0.0, 1.0), H=wl["H"], delta=wl["delta"],
-                        m=wl["m"], n_levels=L, nev=nev, cg_tol=1e-10, device=local,
-                        example=wl.get("example", "laplace"), seed=wl.get("seed", 0))
+    hole = wl.get("hole")
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*wl.get("domain", (0.0, 1.0, 0.0, 1.0))),
+                        H=wl["H"], delta=wl["delta"], m=wl["m"], n_levels=L, nev=nev,
+                        cg_tol=1e-10, device=local, example=wl.get("example", "laplace"),
+                        seed=wl.get("seed", 0), hole=mlg.DomainRect(*hole) if hole else None)
     hy = mlg.Hierarchy(cfg)
     t0 = time.time()
     hy.extend_to(L - 1)
@@ -354,7 +357,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-north-star", action="store_true",
-                    help="skip the extra config-5 (4096^2) and config-4 measurements")
+                    help="skip the extra config-5 (4096^2), config-4 and config-3 measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
@@ -368,6 +371,9 @@ def main():
         extra = run_ours(args, ws, rank, local, "c5", steps=2, warmup=1, with_e2e=False)
     if not args.no_north_star and args.workload != "c4":
         extra4 = run_ours(args, ws, rank, local, "c4", steps=2, warmup=1, with_e2e=False)
+    extra3 = None
+    if not args.no_north_star and args.workload != "c3":
+        extra3 = run_ours(args, ws, rank, local, "c3", steps=2, warmup=1, with_e2e=False)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -406,6 +412,13 @@ def main():
             "level_build_s": extra["build_s"], "timings": extra["timings"],
             "roofline": extra.get("roofline"), "lambdas": extra["lam"],
             "clocks": extra["clocks"], "spmv_microbench": extra["spmv_microbench"]}
+    if extra3:
+        line["config3_workload"] = {
+            "workload": WORKLOADS["c3"]["desc"], "value": extra3["value"], "unit": "DOF/s",
+            "ms_per_step": extra3["ms_per_step"], "n_interior": extra3["n_int"],
+            "level_build_s": extra3["build_s"], "timings": extra3["timings"],
+            "roofline": extra3.get("roofline"), "lambdas": extra3["lam"],
+            "clocks": extra3["clocks"]}
     if extra4:
         line["config4_workload"] = {
             "workload": WORKLOADS["c4"]["desc"], "value": extra4["value"], "unit": "DOF/s",
