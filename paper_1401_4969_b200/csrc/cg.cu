@@ -48,7 +48,10 @@ constexpr int kBlock = CgBatch::kBlock;
 // redundantly by every CTA holding one of their tiles after the grid barrier;
 // larger systems keep the last-tile reduction before it (reading hundreds of
 // partials per CTA costs more than the atomic round trip).
-constexpr int kReplTiles = 96;
+#ifndef MLG_CG_REPL
+#define MLG_CG_REPL 96
+#endif
+constexpr int kReplTiles = MLG_CG_REPL;
 constexpr unsigned kFull = 0xffffffffu;
 
 #ifdef MLG_CG_TRACE
@@ -1367,6 +1370,11 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
       }
     }
     krows = best_k;
+    static const int strip_rows = [] {
+      const char* e = std::getenv("MLG_CG_STRIP_ROWS");  // tuning hook (strip batches)
+      return e ? std::atoi(e) : 0;
+    }();
+    if (mask_ && strip_rows > 0) krows = strip_rows;
     // Persistent batches: one tile per CTA leaves the slow (edge) tiles on the
     // critical path; aim for ~`tpc` tiles per CTA so the LPT assignment can
     // pair them with cheap ones.
