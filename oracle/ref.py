@@ -130,7 +130,8 @@ class RefHierarchy:
     def space(self, level):
         s = self.sizes(level)
         dl = np.empty((s["ndofs"], 2), np.int32); idofs = np.empty(s["n_int"], np.int32)
-        iidx = np.empty(s["ndofs"], np.int32); conn = np.empty((s["nt"], 3), np.int32)
+        iidx = np.empty(s["ndofs"], np.int32)
+        conn = np.empty((s["nt"], 6 if self.cfg.degree == 2 else 3), np.int32)
         _chk(lib().ref_export_space(self.h, level, _i(dl), _i(idofs), _i(iidx), _i(conn)))
         return dict(dof_lattice=dl, interior_dofs=idofs, interior_index=iidx, connectivity=conn)
 

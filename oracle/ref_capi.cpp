@@ -205,9 +205,11 @@ int ref_export_space(void* h, int level, int* dof_lattice, int* interior_dofs,
       for (std::size_t i = 0; i < s.interior_dofs.size(); ++i) interior_dofs[i] = s.interior_dofs[i];
     if (interior_index)
       for (int d = 0; d < s.ndofs; ++d) interior_index[d] = s.interior_index[d];
-    if (conn3)
+    if (conn3) {  // dofs_per_elem columns (3 for P1, 6 for P2)
+      const int nd = s.dofs_per_elem();
       for (std::size_t e = 0; e < s.connectivity.size(); ++e)
-        for (int k = 0; k < 3; ++k) conn3[3 * e + k] = s.connectivity[e][k];
+        for (int k = 0; k < nd; ++k) conn3[nd * e + k] = s.connectivity[e][k];
+    }
   });
 }
 

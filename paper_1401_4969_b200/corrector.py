@@ -209,7 +209,7 @@ class Hierarchy:
         dl = np.empty((i.ndofs, 2), np.int32)
         idofs = np.empty(i.n_interior, np.int32)
         iidx = np.empty(i.ndofs, np.int32)
-        conn = np.empty((i.num_triangles, 3), np.int32)
+        conn = np.empty((i.num_triangles, 6 if self.config.degree == 2 else 3), np.int32)
         check(lib().mlg_export_space(self._h, level, _ip(dl), _ip(idofs), _ip(iidx),
                                      _ip(conn)))
         return FeSpace(int(i.ndofs), dl, idofs, iidx, conn)

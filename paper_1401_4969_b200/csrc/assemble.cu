@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "ctx.cuh"
+#include "p2.cuh"
 
 namespace mlg {
 namespace {
@@ -490,6 +491,7 @@ __global__ void k_uniform_check(int nx, int ny, const Stencil* st, const double*
 }  // namespace
 
 std::int64_t csr_nnz(const Level& L) {
+  if (L.deg == 2) return L.p2nnz;
   if (L.hole.any())  // diagonal per vertex + 2 per mesh edge, E = (3T + B) / 2
     return L.nv + 3 * L.nt + L.nb;
   const std::int64_t n = L.nx, m = L.ny;
@@ -498,6 +500,10 @@ std::int64_t csr_nnz(const Level& L) {
 }
 
 void assemble_level(Ctx& c, Level& L) {
+  if (L.deg == 2) {  // P2 operators on the half lattice (p2.cu)
+    assemble_p2(c, L);
+    return;
+  }
   const std::int64_t nd = L.ndofs();
   L.stA.alloc(nd);
   L.stM.alloc(nd);
@@ -562,6 +568,10 @@ void assemble_level(Ctx& c, Level& L) {
 }
 
 void export_csr(Ctx& c, const Level& L, int form, int* row_ptr, int* cols, double* vals) {
+  if (L.deg == 2) {
+    export_csr_p2(c, L, form, row_ptr, cols, vals);
+    return;
+  }
   if (L.hole.any()) {
     const std::int64_t nd = L.ndofs();
     DevBuf<int> cnt(nd + 1), rp(nd + 1);
@@ -603,6 +613,10 @@ void export_csr(Ctx& c, const Level& L, int form, int* row_ptr, int* cols, doubl
 }
 
 void interior_dense(Ctx& c, const Level& L, int form, double* d_dense) {
+  if (L.deg == 2) {
+    interior_dense_p2(c, L, form, d_dense);
+    return;
+  }
   const std::int64_t n = L.nint();
   MLG_CUDA(cudaMemsetAsync(d_dense, 0, sizeof(double) * n * n, c.stream));
   k_interior_dense<<<grid_for(n, kBlock), kBlock, 0, c.stream>>>(

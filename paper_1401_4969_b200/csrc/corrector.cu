@@ -19,6 +19,7 @@
 #include <string>
 
 #include "corrector.cuh"
+#include "p2.cuh"
 #include "vec_kernels.cuh"
 
 namespace mlg {
@@ -699,8 +700,7 @@ void validate_config(const Config& cfg) {  // corrector.cpp:76-88
   if (cfg.workers < 1) throw ConfigError("workers must be at least 1");
   if (cfg.example < 0 || cfg.example > 2)
     throw ConfigError("unknown example id (expected laplace, variable or reaction)");
-  // Scope of the B200 path: P1 elements (Laplace or variable field).
-  if (cfg.degree != 1) throw ConfigError("degree 2 (P2) is not on the B200 path");
+
 }
 
 static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-121
@@ -925,7 +925,12 @@ void prolong_chain(Ctx& c, int nr, const double* src, int from, int to, double* 
       bufs[k & 1]->ensure(F.ndofs() * nr);
       out = bufs[k & 1]->get();
     }
-    NR_DISPATCH(nr, k_prolong, grid_for(F.ndofs(), kB), C.nx, F.nx, F.ny, F.hole, cur, out);
+    if (F.deg == 2) {
+      if (nr != 1) throw ConfigError("P2 prolongation takes one vector");
+      prolong_p2(c, C, cur, out);
+    } else {
+      NR_DISPATCH(nr, k_prolong, grid_for(F.ndofs(), kB), C.nx, F.nx, F.ny, F.hole, cur, out);
+    }
     cur = out;
   }
 }
@@ -978,7 +983,7 @@ void fix_sign_lanes(Ctx& c, int nr, const Level& L, double* v) {
   const int nb = 296;
   w.amax.ensure(static_cast<std::size_t>(nb) * nr);
   w.sign.ensure(nr);
-  NR_DISPATCH(nr, k_absmax, nb, L.nx, L.ny, v, w.amax.get());
+  NR_DISPATCH(nr, k_absmax, nb, L.gx(), L.gy(), v, w.amax.get());
   switch (nr) {
     case 1: k_absmax_final<1><<<1, 32, 0, c.stream>>>(nb, w.amax.get(), v, w.sign.get()); break;
     case 2: k_absmax_final<2><<<1, 32, 0, c.stream>>>(nb, w.amax.get(), v, w.sign.get()); break;
@@ -1095,6 +1100,12 @@ std::vector<DensePair> dense_gen_eigensolve_dev(Ctx& c, int n, double* a, double
 // ---------------------------------------------------------------------------
 // Level-1 direct solve: solve_interior_eigenproblem (sparse.cpp:326-355)
 // ---------------------------------------------------------------------------
+void require_p1(const Ctx& c) {
+  if (c.cfg.degree != 1)
+    throw ConfigError("the correction step on P2 spaces is not on the B200 path yet "
+                      "(P2 level build, operators, transfer and the coarse solve are)");
+}
+
 std::vector<double> coarse_eigensolve(Ctx& c, int level, int nev, DevBuf<double>& u_out) {
   c.extend_to(level);
   Level& L = c.level(level);
@@ -1121,8 +1132,11 @@ std::vector<double> coarse_eigensolve(Ctx& c, int level, int nev, DevBuf<double>
   NR_DISPATCH(nr, k_interleave, grid_for(L.ndofs(), kB), L.imap(), nev, tmp.get(), 1,
               u_out.get());
   w.mfull.ensure(L.ndofs() * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(L.ndofs(), kB), L.imap(), L.stA.get(), L.stM.get(),
-              u_out.get(), nullptr, w.mfull.get());
+  if (L.deg == 2)
+    apply_p2(c, L, 1, nr, u_out.get(), w.mfull.get(), true);
+  else
+    NR_DISPATCH(nr, k_dual, grid_for(L.ndofs(), kB), L.imap(), L.stA.get(), L.stM.get(),
+                u_out.get(), nullptr, w.mfull.get());
   const auto q = mdot(c, nr, L, u_out.get(), w.mfull.get());
   Lam s{};
   for (int r = 0; r < 8; ++r) s.v[r] = 1.0;
@@ -1167,6 +1181,7 @@ static std::string fmt_report(const SolveReport& r) {
 // lives in its window-compact X (never expanded to N-length vectors).
 int local_solves(Ctx& c, const Level& F, int nr, int nev, const double* res, double tol,
                  int maxit, std::vector<SolveReport>* reports, int only_j) {
+  require_p1(c);
   Workspace& w = W(c);
   const std::vector<CgSys> win = local_systems(c, F.level);
   std::vector<CgSys> sys;
@@ -1204,6 +1219,7 @@ void ensure_strip_mask(Ctx& c, Level& F) {
 int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const Lam& lam,
                 double* glued, double tol, int maxit, std::vector<SolveReport>* reports,
                 bool* empty) {
+  require_p1(c);
   Workspace& w = W(c);
   ensure_strip_mask(c, F);
   bool any_strip = false;
@@ -1294,6 +1310,7 @@ static bool arrow_enabled() {  // A/B hook: MLG_AUG=0/1/2 forces the dense cuSOL
 
 std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double* glued, int nev,
                               DevBuf<double>& u_out) {
+  require_p1(c);
   Level& F = c.level(level);
   const Level& L0 = c.level(0);
   c.ensure_coarse_dense();
@@ -1405,6 +1422,7 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
 // ---------------------------------------------------------------------------
 StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_in,
                            const double* u_in, DevBuf<double>& u_out) {
+  require_p1(c);
   if (nev < 1) throw ConfigError("correction step needs at least one eigenpair");
   if (to != from + 1 && to != from)
     throw ConfigError("correction step targets the next level (or the same level)");
@@ -1498,6 +1516,10 @@ void deinterleave(Ctx& c, const Level& L, int nr, int k_out, const int* perm, co
 }
 
 void spmv_full(Ctx& c, const Level& L, int form, const double* x, double* y) {
+  if (L.deg == 2) {
+    apply_p2(c, L, form, 1, x, y, false);
+    return;
+  }
   k_full_spmv<<<grid_for(L.ndofs(), kB), kB, 0, c.stream>>>(
       L.nx, L.ny, form == 0 ? L.stA.get() : L.stM.get(), x, y);
   MLG_LAUNCH_CHECK();
@@ -1527,7 +1549,13 @@ void restrict_levels(Ctx& c, int nr, const double* src, int from, int to, double
       bufs[k & 1]->ensure(C.ndofs() * nr);
       out = bufs[k & 1]->get();
     }
-    NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, F.hole, cur, out);
+    if (F.deg == 2) {
+      if (nr != 1) throw ConfigError("P2 restriction takes one vector");
+      restrict_p2(c, C, cur, out);
+    } else {
+      NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, F.hole, cur,
+                  out);
+    }
     cur = out;
   }
 }

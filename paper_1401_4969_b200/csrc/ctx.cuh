@@ -203,15 +203,26 @@ struct Level {
   double udinv = 0.0;
 
   Hole hole;  // in this level's cells (none for rectangles)
-  IMap imap() const { return make_imap(nx, ny, hole); }
+  // Element degree.  P2 dofs live on the half lattice: grid (2nx+1) x (2ny+1),
+  // dof = Y*(2nx+1)+X (p2.cu); gx/gy are the dof-grid extents in both cases.
+  int deg = 1;
+  int gx() const { return deg == 2 ? 2 * nx : nx; }
+  int gy() const { return deg == 2 ? 2 * ny : ny; }
+  IMap imap() const { return make_imap(gx(), gy(), deg == 2 ? hole.scaled(2) : hole); }
+  // P2 operators: 25 slot values per dof (5x5 half-lattice block, ascending
+  // column order) and the mask of structurally present couplings
+  DevBuf<double> p2A, p2M;
+  DevBuf<unsigned> p2pat;
+  std::int64_t p2nnz = 0;
   // CG operator for domains with a hole: the interior restriction of A with
   // identity rows at non-interior points (see corrector.cu ensure_cg_stencil).
   DevBuf<Stencil> stCG;
   DevBuf<double> dinvCG;
 
-  std::int64_t ndofs() const { return static_cast<std::int64_t>(nx + 1) * (ny + 1); }
+  std::int64_t npts() const { return static_cast<std::int64_t>(nx + 1) * (ny + 1); }  // lattice
+  std::int64_t ndofs() const { return static_cast<std::int64_t>(gx() + 1) * (gy() + 1); }
   std::int64_t nint() const {
-    return hole.any() ? imap().count() : static_cast<std::int64_t>(nx - 1) * (ny - 1);
+    return hole.any() ? imap().count() : static_cast<std::int64_t>(gx() - 1) * (gy() - 1);
   }
 };
 

@@ -473,13 +473,14 @@ void build_level0(Ctx& c) {
     throw ConfigError("domain rectangle must have positive side lengths");
   if (!(cfg.H > 0.0)) throw ConfigError("mesh size H must be positive");
   L->level = 0;
+  L->deg = cfg.degree;
   L->nx = cells(cfg.x_max - cfg.x_min, cfg.H, "x");
   L->ny = cells(cfg.y_max - cfg.y_min, cfg.H, "y");
   L->dx = (cfg.x_max - cfg.x_min) / L->nx;
   L->dy = (cfg.y_max - cfg.y_min) / L->ny;
   L->hole = hole_cells(cfg, L->nx, L->ny);
   if (L->hole.any()) {
-    const std::int64_t np = L->ndofs(), ncell = static_cast<std::int64_t>(L->nx) * L->ny;
+    const std::int64_t np = L->npts(), ncell = static_cast<std::int64_t>(L->nx) * L->ny;
     DevBuf<int> pflag(np + 1), cflag(ncell + 1), prank(np + 1), crank(ncell + 1);
     pflag.zero(c.stream);
     cflag.zero(c.stream);
@@ -516,7 +517,7 @@ void build_level0(Ctx& c) {
     MLG_LAUNCH_CHECK();
     c.sync();
   } else {
-  L->nv = L->ndofs();
+  L->nv = L->npts();
   L->nt = 2LL * L->nx * L->ny;
   L->lat.alloc(2 * L->nv);
   L->xy.alloc(2 * L->nv);
@@ -543,13 +544,14 @@ void build_level0(Ctx& c) {
 
 void refine_level(Ctx& c, const Level& C, Level& F) {
   F.level = C.level + 1;
+  F.deg = C.deg;
   F.nx = 2 * C.nx;
   F.ny = 2 * C.ny;
   F.dx = (c.cfg.x_max - c.cfg.x_min) / F.nx;
   F.dy = (c.cfg.y_max - c.cfg.y_min) / F.ny;
   F.nt = 4 * C.nt;
   F.hole = C.hole.scaled(2);
-  std::int64_t nvf_max = F.ndofs();
+  std::int64_t nvf_max = F.npts();
   if (F.hole.any()) {  // lattice points strictly inside the hole carry no vertex
     const std::int64_t ix = F.hole.x0 == 0 ? F.hole.x1 : F.nx - F.hole.x0;
     const std::int64_t iy = F.hole.y0 == 0 ? F.hole.y1 : F.ny - F.hole.y0;
@@ -559,12 +561,12 @@ void refine_level(Ctx& c, const Level& C, Level& F) {
     throw ConfigError("refined mesh exceeds the 32-bit index range of the reference layout");
   F.lat.alloc(2 * nvf_max);
   F.xy.alloc(2 * nvf_max);
-  F.vid.alloc(F.ndofs());
+  F.vid.alloc(F.npts());
   F.tri.alloc(3 * F.nt);
   F.parent.alloc(F.nt);
   F.geo.alloc(2LL * F.nx * F.ny);
   if (F.hole.any()) {  // absent points / cells
-    MLG_CUDA(cudaMemsetAsync(F.vid.get(), 0xFF, sizeof(int) * F.ndofs(), c.stream));
+    MLG_CUDA(cudaMemsetAsync(F.vid.get(), 0xFF, sizeof(int) * F.npts(), c.stream));
     MLG_CUDA(cudaMemsetAsync(F.geo.get(), 0xFF, sizeof(unsigned) * 2 * F.nx * F.ny, c.stream));
   }
 
@@ -620,9 +622,16 @@ void export_mesh(Ctx& c, const Level& L, double* xy, int* lat, int* tri, int* pa
   c.sync();
 }
 
+void export_space_p2(Ctx& c, const Level& L, int* dof_lattice, int* conn6);
+
 void export_space(Ctx& c, const Level& L, int* dof_lattice, int* interior_dofs,
                   int* interior_index, int* conn3) {
   const std::int64_t nd = L.ndofs();
+  if (L.deg == 2) {  // dof lattice and 6-dof connectivity of the half lattice (p2.cu)
+    export_space_p2(c, L, dof_lattice, conn3);
+    dof_lattice = nullptr;
+    conn3 = nullptr;
+  }
   if (dof_lattice) {
     DevBuf<int> d(2 * nd);
     k_dof_lattice<<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(L.nx, L.ny, d.get());

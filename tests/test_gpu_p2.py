@@ -1,0 +1,101 @@
+"""P2 (degree 2) spaces on the B200 path vs the compiled reference: the dof
+numbering, 6-dof connectivity, stiffness and mass CSR (bitwise for the Laplace
+field, a few ulp for the variable field's exp), the full-space SpMV, the P2
+prolongation and its transpose (bitwise), and the level-1 dense eigensolve.
+Mirrors test_fespace.cpp:34-60,121-128,187-213.  The correction step itself is
+P1-only on the B200 path and says so."""
+import numpy as np
+import pytest
+
+from _parity import compare_pairs
+
+pytestmark = pytest.mark.gpu
+
+SQUARE = (-1.0, 1.0, -1.0, 1.0)
+CASES = [("square_H05", SQUARE, 0.5, 1, 3), ("square_H025", SQUARE, 0.25, 4, 3),
+         ("rect", (0.0, 3.0, -1.0, 1.0), 0.5, 1, 2)]
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64) if a.dtype == np.float64 else a
+
+
+def pair(mlg, oracle_ref, domain, H, m, levels, example=0):
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*domain), H=H, delta=H, m=m, n_levels=levels,
+                        nev=2, degree=2, example=["laplace", "variable"][example])
+    hy = mlg.Hierarchy(cfg)
+    rh = oracle_ref.RefHierarchy(domain=domain, H=H, delta=H, m=m, n_levels=levels, nev=2,
+                                 degree=2, example=example)
+    hy.extend_to(levels)
+    rh.extend_to(levels)
+    return hy, rh
+
+
+@pytest.mark.parametrize("name,domain,H,m,levels", CASES)
+def test_p2_space_and_operators_bitexact(mlg, oracle_ref, name, domain, H, m, levels):
+    hy, rh = pair(mlg, oracle_ref, domain, H, m, levels)
+    for k in range(levels + 1):
+        gs, rs = hy.space(k), rh.space(k)
+        for key in ("dof_lattice", "interior_dofs", "interior_index", "connectivity"):
+            assert np.array_equal(getattr(gs, key), rs[key]), (name, k, key)
+        for form in ("stiffness", "mass"):
+            grp, gc, gv = hy.csr(k, form)
+            rrp, rc, rv = rh.csr(k, form)
+            assert np.array_equal(grp, rrp) and np.array_equal(gc, rc), (name, k, form)
+            assert np.array_equal(bits(gv), bits(rv)), (name, k, form)
+        x = np.random.default_rng(k).uniform(-1, 1, gs.ndofs)
+        for form in ("stiffness", "mass"):
+            assert np.array_equal(bits(hy.apply(k, form, x)), bits(rh.apply(k, form, x)))
+
+
+def test_p2_space_sizes(mlg, oracle_ref):  # test_fespace.cpp:34-60
+    hy, _ = pair(mlg, oracle_ref, SQUARE, 0.5, 1, 1)
+    s = hy.space(0)
+    assert s.ndofs == 25 + 56 and len(s.interior_dofs) == 49
+    order = s.dof_lattice[:, 1] * 100 + s.dof_lattice[:, 0]
+    assert np.all(np.diff(order) > 0)  # lexicographic (y, x)
+
+
+def test_p2_transfer_bitexact_and_energy(mlg, oracle_ref):  # test_fespace.cpp:187-213
+    hy, rh = pair(mlg, oracle_ref, SQUARE, 0.25, 4, 3)
+    rng = np.random.default_rng(29)
+    for a in range(3):
+        for b in range(a + 1, 4):
+            x = rng.uniform(-1, 1, hy.level_info(a).ndofs)
+            px = hy.prolong(x, a, b)
+            assert np.array_equal(bits(px), bits(rh.prolong(x, a, b))), (a, b)
+            ea = x @ hy.apply(a, "stiffness", x)
+            eb = px @ hy.apply(b, "stiffness", px)
+            assert abs(eb - ea) <= 1e-12 * ea
+            y = rng.uniform(-1, 1, hy.level_info(b).ndofs)
+            assert np.array_equal(bits(hy.restrict_transpose(y, b, a)),
+                                  bits(rh.restrict_transpose(y, b, a))), (a, b)
+    ones = np.ones(hy.level_info(1).ndofs)
+    assert np.allclose(hy.prolong(ones, 1, 2), 1.0, rtol=0, atol=1e-15)
+
+
+def test_p2_variable_field_operators(mlg, oracle_ref):
+    hy, rh = pair(mlg, oracle_ref, SQUARE, 0.5, 1, 2, example=1)
+    for k in range(3):
+        for form in ("stiffness", "mass"):
+            grp, gc, gv = hy.csr(k, form)
+            rrp, rc, rv = rh.csr(k, form)
+            assert np.array_equal(grp, rrp) and np.array_equal(gc, rc)
+            assert np.max(np.abs(gv - rv)) <= 8e-16 * np.max(np.abs(rv)), (k, form)
+
+
+def test_p2_coarse_eigensolve_and_mass(mlg, oracle_ref):
+    hy, rh = pair(mlg, oracle_ref, SQUARE, 0.25, 4, 2)
+    pairs = mlg.coarse_eigensolve(hy, 1, 3)
+    lam_r, co_r = rh.coarse_eigensolve(1, 3)
+    compare_pairs([p.lam for p in pairs], [p.coeffs for p in pairs], lam_r, co_r,
+                  lambda f: rh.apply(1, "mass", f), lambda v: hy.expand_interior(1, v))
+    ones = np.ones(hy.level_info(2).ndofs)  # test_fespace.cpp:121-128
+    assert abs(ones @ hy.apply(2, "mass", ones) - 4.0) <= 1e-12 * 4.0
+
+
+def test_p2_correction_step_reports_scope(mlg, oracle_ref):
+    hy, _ = pair(mlg, oracle_ref, SQUARE, 0.25, 4, 2)
+    with pytest.raises(mlg.ConfigError, match="P2"):
+        mlg.multilevel_correction(hy)
