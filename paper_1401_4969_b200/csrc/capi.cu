@@ -414,16 +414,16 @@ int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const dou
     mlg::residual(c, F, 1, ui.get(), &lambda, res.get());
     std::vector<mlg::SolveReport> rep;
     mlg::local_solves(c, F, 1, 1, res.get(), cg_tol, 0, &rep, j);
-    const mlg::CgBatch& b = mlg::local_batch(c);
-    const mlg::CgSys s = b.systems()[0];
+    const mlg::LocalView b = mlg::local_view(c);
+    const mlg::CgSys s = b.systems[0];
     std::vector<double> x(static_cast<std::size_t>(s.h) * s.pitch);  // window rows, pitched
-    MLG_CUDA(cudaMemcpyAsync(x.data(), b.x() + s.voff, sizeof(double) * x.size(),
+    MLG_CUDA(cudaMemcpyAsync(x.data(), b.x + s.voff, sizeof(double) * x.size(),
                              cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     std::fill(e_full, e_full + nd, 0.0);
     for (int ly = 0; ly < s.h; ++ly)
       for (int lx = 0; lx < s.w; ++lx)
-        e_full[static_cast<int64_t>(s.y0 + ly) * (F.nx + 1) + (s.x0 + lx)] =
+        e_full[static_cast<int64_t>(s.y0 + ly) * (F.gx() + 1) + (s.x0 + lx)] =
             x[static_cast<std::size_t>(ly) * s.pitch + lx];
     if (report) {
       report->iterations = rep[0].iterations;

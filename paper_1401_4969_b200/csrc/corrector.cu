@@ -18,6 +18,7 @@
 #include <cstring>
 #include <string>
 
+#include "cg_p2.cuh"
 #include "corrector.cuh"
 #include "p2.cuh"
 #include "vec_kernels.cuh"
@@ -648,7 +649,7 @@ PartDev part_dev(const Ctx& c, int level) {
   P.side = p.side;
   P.bw = p.nx0 / p.side;
   P.bh = p.ny0 / p.side;
-  P.scale = 1 << level;
+  P.scale = (c.cfg.degree == 2 ? 2 : 1) << level;  // dof-grid points per coarse cell
   P.m = p.m;
   if (p.m > 256) throw ConfigError("more than 256 subdomains are not supported on this path");
   for (int j = 0; j < p.m; ++j) {
@@ -802,6 +803,7 @@ static void build_partition(Ctx& c) {  // decomp.cpp:24-121 + corrector.cpp:117-
 
 struct Workspace {
   CgBatch local, strip;
+  CgBatchP2 local2, strip2;  // degree-2 batches (cg_p2.cu)
   DevBuf<double> corr;
   DevBuf<double> aug_ctmp, aug_uu_a, aug_uu_b, aug_cp, aug_c0;
   DevBuf<double> u, res, glued, au, bu, full, mfull, load, tmp_c0, tmp_c1, a_cu, b_cu;
@@ -926,8 +928,7 @@ void prolong_chain(Ctx& c, int nr, const double* src, int from, int to, double* 
       out = bufs[k & 1]->get();
     }
     if (F.deg == 2) {
-      if (nr != 1) throw ConfigError("P2 prolongation takes one vector");
-      prolong_p2(c, C, cur, out);
+      prolong_p2(c, C, nr, cur, out);
     } else {
       NR_DISPATCH(nr, k_prolong, grid_for(F.ndofs(), kB), C.nx, F.nx, F.ny, F.hole, cur, out);
     }
@@ -946,8 +947,11 @@ const double* restrict_chain(Ctx& c, int nr, const double* src, int from, int sl
     const Level& C = c.level(k - 1);
     DevBuf<double>& out = w.chain[2 * (k - 1) + slot];
     out.ensure(C.ndofs() * nr);
-    NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, F.hole, cur,
-                out.get());
+    if (F.deg == 2)
+      restrict_p2(c, C, nr, cur, out.get());
+    else
+      NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, F.hole, cur,
+                  out.get());
     cur = out.get();
   }
   return cur;
@@ -1100,10 +1104,25 @@ std::vector<DensePair> dense_gen_eigensolve_dev(Ctx& c, int n, double* a, double
 // ---------------------------------------------------------------------------
 // Level-1 direct solve: solve_interior_eigenproblem (sparse.cpp:326-355)
 // ---------------------------------------------------------------------------
-void require_p1(const Ctx& c) {
-  if (c.cfg.degree != 1)
-    throw ConfigError("the correction step on P2 spaces is not on the B200 path yet "
-                      "(P2 level build, operators, transfer and the coarse solve are)");
+// Degree dispatch of the operator kernels the step uses.
+static void residual_any(Ctx& c, const Level& F, int nr, const double* u, const double* w,
+                         const Lam& lam, double* out, const unsigned char* mask) {
+  if (F.deg == 2) {
+    residual_p2(c, F, nr, u, w, lam, out, mask);
+    return;
+  }
+  NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.imap(), F.stA.get(), F.stM.get(), u, w,
+              lam, out, mask);
+}
+
+static void dual_any(Ctx& c, const Level& F, int nr, const double* x, double* ya, double* ym) {
+  if (F.deg == 2) {
+    if (ya) apply_p2(c, F, 0, nr, x, ya, true);
+    if (ym) apply_p2(c, F, 1, nr, x, ym, true);
+    return;
+  }
+  NR_DISPATCH(nr, k_dual, grid_for(F.ndofs(), kB), F.imap(), F.stA.get(), F.stM.get(), x, ya,
+              ym);
 }
 
 std::vector<double> coarse_eigensolve(Ctx& c, int level, int nev, DevBuf<double>& u_out) {
@@ -1132,11 +1151,7 @@ std::vector<double> coarse_eigensolve(Ctx& c, int level, int nev, DevBuf<double>
   NR_DISPATCH(nr, k_interleave, grid_for(L.ndofs(), kB), L.imap(), nev, tmp.get(), 1,
               u_out.get());
   w.mfull.ensure(L.ndofs() * nr);
-  if (L.deg == 2)
-    apply_p2(c, L, 1, nr, u_out.get(), w.mfull.get(), true);
-  else
-    NR_DISPATCH(nr, k_dual, grid_for(L.ndofs(), kB), L.imap(), L.stA.get(), L.stM.get(),
-                u_out.get(), nullptr, w.mfull.get());
+  dual_any(c, L, nr, u_out.get(), nullptr, w.mfull.get());
   const auto q = mdot(c, nr, L, u_out.get(), w.mfull.get());
   Lam s{};
   for (int r = 0; r < 8; ++r) s.v[r] = 1.0;
@@ -1157,7 +1172,7 @@ std::vector<double> coarse_eigensolve(Ctx& c, int level, int nev, DevBuf<double>
 // Step 1: batched local residual solves (corrector.cpp:198-214, 361-369)
 // ---------------------------------------------------------------------------
 static std::vector<CgSys> local_systems(const Ctx& c, int level) {
-  const int S = 1 << level;
+  const int S = (c.cfg.degree == 2 ? 2 : 1) << level;  // dof-grid points per coarse cell
   std::vector<CgSys> sys;
   for (int j = 0; j < c.part.m; ++j) {
     const IRect& o = c.part.overlaps[j];
@@ -1181,7 +1196,6 @@ static std::string fmt_report(const SolveReport& r) {
 // lives in its window-compact X (never expanded to N-length vectors).
 int local_solves(Ctx& c, const Level& F, int nr, int nev, const double* res, double tol,
                  int maxit, std::vector<SolveReport>* reports, int only_j) {
-  require_p1(c);
   Workspace& w = W(c);
   const std::vector<CgSys> win = local_systems(c, F.level);
   std::vector<CgSys> sys;
@@ -1192,6 +1206,12 @@ int local_solves(Ctx& c, const Level& F, int nr, int nev, const double* res, dou
       s.rhs = i;
       sys.push_back(s);
     }
+  }
+  if (F.deg == 2) {
+    w.local2.setup(c, F, std::move(sys), nullptr, res, nr);
+    const CgResult r = w.local2.solve(c, tol);
+    if (reports) *reports = r.reports;
+    return r.iters_max;
   }
   w.local.setup(c, F, std::move(sys), nullptr, res, nr);
   const CgResult r = w.local.solve(c, tol, maxit);
@@ -1219,7 +1239,6 @@ void ensure_strip_mask(Ctx& c, Level& F) {
 int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const Lam& lam,
                 double* glued, double tol, int maxit, std::vector<SolveReport>* reports,
                 bool* empty) {
-  require_p1(c);
   Workspace& w = W(c);
   ensure_strip_mask(c, F);
   bool any_strip = false;
@@ -1230,19 +1249,26 @@ int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const Lam& l
   *empty = !any_strip;
   if (!any_strip) return 0;  // m = 1: G_1 is the whole domain, the strip is empty
   w.load.ensure(F.ndofs() * nr);
-  NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.imap(), F.stA.get(), F.stM.get(), u,
-              glued, lam, w.load.get(), F.strip_mask.get());
+  residual_any(c, F, nr, u, glued, lam, w.load.get(), F.strip_mask.get());
   std::vector<CgSys> sys;
   for (int i = 0; i < nev; ++i) {
     CgSys s{};
     s.x0 = 1;
     s.y0 = 1;
-    s.w = F.nx - 1;
-    s.h = F.ny - 1;
+    s.w = F.gx() - 1;
+    s.h = F.gy() - 1;
     s.rhs = i;
     sys.push_back(s);
   }
-  const long long rows = static_cast<long long>(F.nx - 1) * (F.ny - 1);
+  const long long rows = static_cast<long long>(F.gx() - 1) * (F.gy() - 1);
+  if (F.deg == 2) {
+    w.strip2.setup(c, F, std::move(sys), F.strip_mask.get(), w.load.get(), nr);
+    const CgResult r = w.strip2.solve(c, tol);
+    if (reports) *reports = r.reports;
+    NR_DISPATCH(nr, k_strip_scatter, grid_for(rows, kB), F.gx(), nev, w.strip2.sys_dev(),
+                F.strip_mask.get(), w.strip2.x(), glued);
+    return r.iters_max;
+  }
   w.strip.setup(c, F, std::move(sys), F.strip_mask.get(), w.load.get(), nr);
   const CgResult r = w.strip.solve(c, tol, maxit);
   if (reports) *reports = r.reports;
@@ -1273,8 +1299,7 @@ static std::vector<double> expand_augmented(Ctx& c, Level& F, int level, int nr,
   NR_DISPATCH(nr, k_candidates, grid_for(nd, kB), nd, k, w.keep.get(), w.coef.get(), glued,
               w.full.get());
   w.mfull.ensure(nd * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), w.full.get(),
-              nullptr, w.mfull.get());
+  dual_any(c, F, nr, w.full.get(), nullptr, w.mfull.get());
   const auto q = mdot(c, nr, F, w.full.get(), w.mfull.get());
   Lam s{};
   for (int r = 0; r < 8; ++r) s.v[r] = 1.0;
@@ -1310,7 +1335,6 @@ static bool arrow_enabled() {  // A/B hook: MLG_AUG=0/1/2 forces the dense cuSOL
 
 std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double* glued, int nev,
                               DevBuf<double>& u_out) {
-  require_p1(c);
   Level& F = c.level(level);
   const Level& L0 = c.level(0);
   c.ensure_coarse_dense();
@@ -1319,8 +1343,7 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
   const long long nd = F.ndofs();
   w.au.ensure(nd * nr);
   w.bu.ensure(nd * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), glued,
-              w.au.get(), w.bu.get());
+  dual_any(c, F, nr, glued, w.au.get(), w.bu.get());
   const double* a0 = restrict_chain(c, nr, w.au.get(), level, 0);
   const double* b0 = restrict_chain(c, nr, w.bu.get(), level, 1);
   w.a_cu.ensure(static_cast<std::size_t>(mc) * nr);
@@ -1422,7 +1445,6 @@ std::vector<double> augmented(Ctx& c, int level, int nr, int k_in, const double*
 // ---------------------------------------------------------------------------
 StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_in,
                            const double* u_in, DevBuf<double>& u_out) {
-  require_p1(c);
   if (nev < 1) throw ConfigError("correction step needs at least one eigenpair");
   if (to != from + 1 && to != from)
     throw ConfigError("correction step targets the next level (or the same level)");
@@ -1444,8 +1466,7 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
 
   Timer t0(c.stream);
   w.res.ensure(nd * nr);
-  NR_DISPATCH(nr, k_residual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), w.u.get(),
-              w.u.get(), lam, w.res.get(), nullptr);
+  residual_any(c, F, nr, w.u.get(), w.u.get(), lam, w.res.get(), nullptr);
   std::vector<SolveReport> lrep;
   out.times.local_iters_max =
       local_solves(c, F, nr, nev, w.res.get(), c.cfg.cg_tol, 0, &lrep);
@@ -1460,7 +1481,8 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
 
   w.glued.ensure(nd * nr);
   NR_DISPATCH(nr, k_glue_cg, grid_for(nd, kB), F.imap(), part_dev(c, to), nev,
-              w.local.sys_dev(), w.local.x(), w.u.get(), w.glued.get());
+              F.deg == 2 ? w.local2.sys_dev() : w.local.sys_dev(),
+              F.deg == 2 ? w.local2.x() : w.local.x(), w.u.get(), w.glued.get());
   std::vector<SolveReport> srep;
   bool empty = false;
   out.times.strip_iters_max =
@@ -1476,8 +1498,7 @@ StepResult correction_step(Ctx& c, int from, int to, int nev, const double* lam_
 
   // matching diagnostic (corrector.cpp:383-399)
   w.mfull.ensure(nd * nr);
-  NR_DISPATCH(nr, k_dual, grid_for(nd, kB), F.imap(), F.stA.get(), F.stM.get(), u_out.get(),
-              nullptr, w.mfull.get());
+  dual_any(c, F, nr, u_out.get(), nullptr, w.mfull.get());
   const auto m = mdot(c, nr, F, w.u.get(), w.mfull.get());
   out.matched = true;
   for (int i2 = 0; i2 < nev; ++i2) {
@@ -1550,8 +1571,7 @@ void restrict_levels(Ctx& c, int nr, const double* src, int from, int to, double
       out = bufs[k & 1]->get();
     }
     if (F.deg == 2) {
-      if (nr != 1) throw ConfigError("P2 restriction takes one vector");
-      restrict_p2(c, C, cur, out);
+      restrict_p2(c, C, nr, cur, out);
     } else {
       NR_DISPATCH(nr, k_restrict, grid_for(C.ndofs(), kB), F.nx, F.ny, C.nx, C.ny, F.hole, cur,
                   out);
@@ -1570,8 +1590,13 @@ void glue_full(Ctx& c, int level, const double* corr, const double* u, double* g
 void residual(Ctx& c, const Level& F, int nr, const double* u, const double* lam, double* out) {
   Lam l{};
   for (int r = 0; r < nr; ++r) l.v[r] = lam[r];
-  NR_DISPATCH(nr, k_residual, grid_for(F.ndofs(), kB), F.imap(), F.stA.get(), F.stM.get(), u,
-              u, l, out, nullptr);
+  residual_any(c, F, nr, u, u, l, out, nullptr);
+}
+
+LocalView local_view(Ctx& c) {
+  Workspace& w = W(c);
+  if (c.cfg.degree == 2) return {w.local2.systems(), w.local2.x(), w.local2.sys_dev()};
+  return {w.local.systems(), w.local.x(), w.local.sys_dev()};
 }
 
 }  // namespace mlg

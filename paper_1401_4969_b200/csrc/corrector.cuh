@@ -35,6 +35,13 @@ int local_solves(Ctx& c, const Level& F, int nr, int nev, const double* res, dou
                  int maxit, std::vector<SolveReport>* reports, int only_j = -1);
 // The batched local CG of the last local_solves call (X holds e_j per window).
 const CgBatch& local_batch(Ctx& c);
+// The last local_solves batch, whatever the degree: systems, pooled x, device systems.
+struct LocalView {
+  std::vector<CgSys> systems;
+  const double* x;
+  const CgSys* sys_dev;
+};
+LocalView local_view(Ctx& c);
 int strip_solve(Ctx& c, Level& F, int nr, int nev, const double* u, const struct Lam& lam,
                 double* glued, double tol, int maxit, std::vector<SolveReport>* reports,
                 bool* empty);

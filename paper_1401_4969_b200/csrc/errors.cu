@@ -66,6 +66,7 @@ struct ErrGeom {
   double x0, y0, dx, dy;
   const unsigned* geo;
   int example;  // field weight: 0 laplace (1), 1 variable ((1+x^2)(1+y^2))
+  int deg;      // 1: P1 lattice dofs; 2: P2 half-lattice dofs (p2.cu)
 };
 
 __device__ __forceinline__ void canon_vertex(int cx, int cy, int upper, int k, int* x, int* y) {
@@ -97,14 +98,27 @@ __global__ void __launch_bounds__(kEB) k_errors(ErrGeom G, ExactMode md, const d
     const int cx = static_cast<int>(cell % G.nx), cy = static_cast<int>(cell / G.nx);
     if (G.geo[t] == 0xFFFFFFFFu) continue;  // removed cell (domain with a hole)
     const int rot = static_cast<int>(G.geo[t] & 3u);
-    double vx[3], vy[3], c[3];
+    double vx[3], vy[3], c[6];
+    int hx[3], hy[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {  // element vertex order (mesh.triangles[e])
       int lx, ly;
       canon_vertex(cx, cy, upper, (rot + j) % 3, &lx, &ly);
       vx[j] = lattice_coord(G.x0, lx, G.dx);
       vy[j] = lattice_coord(G.y0, ly, G.dy);
-      c[j] = coeffs[(static_cast<long long>(ly) * (G.nx + 1) + lx) * stride + lane];
+      hx[j] = lx;
+      hy[j] = ly;
+    }
+    if (G.deg == 2) {  // connectivity v0, v1, v2, m01, m12, m20 on the half lattice
+      const long long sx = 2LL * G.nx + 1;
+      const int ea[3] = {0, 1, 2}, eb[3] = {1, 2, 0};
+      for (int j = 0; j < 3; ++j) {
+        c[j] = coeffs[(2LL * hy[j] * sx + 2LL * hx[j]) * stride + lane];
+        c[3 + j] = coeffs[((hy[ea[j]] + hy[eb[j]]) * sx + (hx[ea[j]] + hx[eb[j]])) * stride + lane];
+      }
+    } else {
+      for (int j = 0; j < 3; ++j)
+        c[j] = coeffs[(static_cast<long long>(hy[j]) * (G.nx + 1) + hx[j]) * stride + lane];
     }
     // element_geometry (fespace.cpp:169-183)
     const double area2 = (vx[1] - vx[0]) * (vy[2] - vy[0]) - (vx[2] - vx[0]) * (vy[1] - vy[0]);
@@ -113,14 +127,30 @@ __global__ void __launch_bounds__(kEB) k_errors(ErrGeom G, ExactMode md, const d
     const double g1x = (vy[2] - vy[0]) / area2, g1y = (vx[0] - vx[2]) / area2;
     const double g2x = (vy[0] - vy[1]) / area2, g2y = (vx[1] - vx[0]) / area2;
     // P1: the gradient of u_h is constant on the element
-    const double uhx = c[0] * g0x + c[1] * g1x + c[2] * g2x;
-    const double uhy = c[0] * g0y + c[1] * g1y + c[2] * g2y;
+    double uhx = c[0] * g0x + c[1] * g1x + c[2] * g2x;
+    double uhy = c[0] * g0y + c[1] * g1y + c[2] * g2y;
     for (int q = 0; q < kNQ; ++q) {
       const double l0 = kDuffy[q][0], l1 = kDuffy[q][1], l2 = kDuffy[q][2];
       const double w = kDuffy[q][3] * area;
       const double x = l0 * vx[0] + l1 * vx[1] + l2 * vx[2];
       const double y = l0 * vy[0] + l1 * vy[1] + l2 * vy[2];
-      const double uh = c[0] * l0 + c[1] * l1 + c[2] * l2;
+      double uh = c[0] * l0 + c[1] * l1 + c[2] * l2;
+      if (G.deg == 2) {  // shape_values / shape_gradients, degree 2 (fespace.cpp:128-161)
+        const double l[3] = {l0, l1, l2};
+        const double gl[3][2] = {{g0x, g0y}, {g1x, g1y}, {g2x, g2y}};
+        uh = 0.0;
+        uhx = 0.0;
+        uhy = 0.0;
+        for (int i = 0; i < 3; ++i) {
+          uh += c[i] * (l[i] * (2.0 * l[i] - 1.0));
+          uhx += c[i] * ((4.0 * l[i] - 1.0) * gl[i][0]);
+          uhy += c[i] * ((4.0 * l[i] - 1.0) * gl[i][1]);
+          const int a = i, b = (i + 1) % 3;
+          uh += c[3 + i] * (4.0 * l[a] * l[b]);
+          uhx += c[3 + i] * (4.0 * (l[a] * gl[b][0] + l[b] * gl[a][0]));
+          uhy += c[3 + i] * (4.0 * (l[a] * gl[b][1] + l[b] * gl[a][1]));
+        }
+      }
       double sx, cxx, sy, cyy;
       sincos(ax * (x - md.x0) / md.lx, &sx, &cxx);
       sincos(ay * (y - md.y0) / md.ly, &sy, &cyy);
@@ -184,7 +214,8 @@ ErrorReport compute_errors(Ctx& c, const Level& L, const double* d_coeffs, int s
   const long long nt = 2LL * L.nx * L.ny;
   const int nb = static_cast<int>(std::min<long long>(grid_for(nt, kEB), 8LL * sms));
   DevBuf<double> part(static_cast<std::size_t>(nb) * kNS), out(kNS);
-  ErrGeom G{L.nx, L.ny, c.cfg.x_min, c.cfg.y_min, L.dx, L.dy, L.geo.get(), c.cfg.example};
+  ErrGeom G{L.nx, L.ny, c.cfg.x_min, c.cfg.y_min, L.dx, L.dy, L.geo.get(), c.cfg.example,
+            L.deg};
   k_errors<<<nb, kEB, 0, c.stream>>>(G, *mode, d_coeffs, stride, lane, part.get());
   MLG_LAUNCH_CHECK();
   k_errors_final<<<1, 32, 0, c.stream>>>(nb, part.get(), out.get());

@@ -27,6 +27,7 @@
 
 #include "p2.cuh"
 #include "stencil.cuh"
+#include "vec_kernels.cuh"
 
 namespace mlg {
 namespace {
@@ -358,31 +359,83 @@ __device__ PRow p2_row(int nxc, int nyc, int FX, int FY) {
 }
 
 // y = P x (SparseMatrix::multiply, sparse.cpp:129-136: from 0.0, column order)
+template <int NR>
 __global__ void k_p2_prolong(int nxc, int nyc, const double* xc, double* xf) {
   const int gx = 4 * nxc, gy = 4 * nyc;
   const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (d >= static_cast<long long>(gx + 1) * (gy + 1)) return;
   const PRow r = p2_row(nxc, nyc, static_cast<int>(d % (gx + 1)), static_cast<int>(d / (gx + 1)));
-  double s = 0.0;
-  for (int k = 0; k < r.n; ++k) s = xadd(s, xmul(r.val[k], xc[r.col[k]]));
-  xf[d] = s;
+  double s[NR], t[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) s[q] = 0.0;
+  for (int k = 0; k < r.n; ++k) {
+    ldv<NR>(xc + r.col[k] * NR, t);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) s[q] = xadd(s[q], xmul(r.val[k], t[q]));
+  }
+  stv<NR>(xf + d * NR, s);
 }
 
 // y = P^T x (multiply_transpose, sparse.cpp:144-148: rows in ascending order):
 // coarse dof c gathers the fine rows around it (a 9x9 fine half-lattice block).
+template <int NR>
 __global__ void k_p2_restrict(int nxc, int nyc, const double* xf, double* xc) {
   const int gxc = 2 * nxc, gyc = 2 * nyc, gxf = 4 * nxc, gyf = 4 * nyc;
   const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (c >= static_cast<long long>(gxc + 1) * (gyc + 1)) return;
   const int CX = static_cast<int>(c % (gxc + 1)), CY = static_cast<int>(c / (gxc + 1));
-  double s = 0.0;
+  double s[NR], t[NR];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) s[q] = 0.0;
   for (int FY = max(2 * CY - 4, 0); FY <= min(2 * CY + 4, gyf); ++FY)
     for (int FX = max(2 * CX - 4, 0); FX <= min(2 * CX + 4, gxf); ++FX) {
       const PRow r = p2_row(nxc, nyc, FX, FY);
       for (int k = 0; k < r.n; ++k)
-        if (r.col[k] == c) s = xadd(s, xmul(r.val[k], xf[static_cast<long long>(FY) * (gxf + 1) + FX]));
+        if (r.col[k] == c) {
+          ldv<NR>(xf + (static_cast<long long>(FY) * (gxf + 1) + FX) * NR, t);
+#pragma unroll
+          for (int q = 0; q < NR; ++q) s[q] = xadd(s[q], xmul(r.val[k], t[q]));
+        }
     }
-  xc[c] = s;
+  stv<NR>(xc + c * NR, s);
+}
+
+// res = lam * (M u) - (A w) at interior dofs (corrector.cpp:201,237), 0 at
+// non-interior ones; with only_mask, masked-out interior dofs are not written.
+template <int NR>
+__global__ void k_p2_residual(IMap im, const double* stA, const double* stM, const unsigned* pat,
+                              const double* u, const double* w, Lam lam, double* out,
+                              const unsigned char* only_mask) {
+  const int gx = im.nx;
+  const long long nd = static_cast<long long>(gx + 1) * (im.ny + 1);
+  const long long d = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (d >= nd) return;
+  const int X = static_cast<int>(d % (gx + 1)), Y = static_cast<int>(d / (gx + 1));
+  double y[NR];
+  if (!im.interior(X, Y)) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) y[r] = 0.0;
+    stv<NR>(out + d * NR, y);
+    return;
+  }
+  if (only_mask && !only_mask[d]) return;
+  double mu[NR], aw[NR], t[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) mu[r] = aw[r] = 0.0;
+  const unsigned m = pat[d];
+  for (int s = 0; s < 25; ++s)
+    if (m >> s & 1u) {
+      const long long col = slot_col(d, s, gx);
+      ldv<NR>(u + col * NR, t);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) mu[r] = xadd(mu[r], xmul(stM[d * 25 + s], t[r]));
+      ldv<NR>(w + col * NR, t);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) aw[r] = xadd(aw[r], xmul(stA[d * 25 + s], t[r]));
+    }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) y[r] = xsub(xmul(lam.v[r], mu[r]), aw[r]);
+  stv<NR>(out + d * NR, y);
 }
 
 void upload_q6(Ctx& c) {
@@ -491,15 +544,31 @@ void export_space_p2(Ctx& c, const Level& L, int* dof_lattice, int* conn6) {
   c.sync();
 }
 
-void prolong_p2(Ctx& c, const Level& C, const double* xc, double* xf) {
+#define P2_NR(nr, kernel, grid, ...)                                              \
+  do {                                                                            \
+    switch (nr) {                                                                 \
+      case 1: kernel<1><<<grid, kBlock, 0, c.stream>>>(__VA_ARGS__); break;       \
+      case 2: kernel<2><<<grid, kBlock, 0, c.stream>>>(__VA_ARGS__); break;       \
+      case 4: kernel<4><<<grid, kBlock, 0, c.stream>>>(__VA_ARGS__); break;       \
+      case 8: kernel<8><<<grid, kBlock, 0, c.stream>>>(__VA_ARGS__); break;       \
+      default: throw ConfigError("unsupported right-hand-side batch width");      \
+    }                                                                             \
+    MLG_LAUNCH_CHECK();                                                           \
+  } while (0)
+
+void prolong_p2(Ctx& c, const Level& C, int nr, const double* xc, double* xf) {
   const long long nf = static_cast<long long>(4 * C.nx + 1) * (4 * C.ny + 1);
-  k_p2_prolong<<<grid_for(nf, kBlock), kBlock, 0, c.stream>>>(C.nx, C.ny, xc, xf);
-  MLG_LAUNCH_CHECK();
+  P2_NR(nr, k_p2_prolong, grid_for(nf, kBlock), C.nx, C.ny, xc, xf);
 }
 
-void restrict_p2(Ctx& c, const Level& C, const double* xf, double* xc) {
-  k_p2_restrict<<<grid_for(C.ndofs(), kBlock), kBlock, 0, c.stream>>>(C.nx, C.ny, xf, xc);
-  MLG_LAUNCH_CHECK();
+void restrict_p2(Ctx& c, const Level& C, int nr, const double* xf, double* xc) {
+  P2_NR(nr, k_p2_restrict, grid_for(C.ndofs(), kBlock), C.nx, C.ny, xf, xc);
+}
+
+void residual_p2(Ctx& c, const Level& L, int nr, const double* u, const double* w,
+                 const Lam& lam, double* out, const unsigned char* only_mask) {
+  P2_NR(nr, k_p2_residual, grid_for(L.ndofs(), kBlock), L.imap(), L.p2A.get(), L.p2M.get(),
+        L.p2pat.get(), u, w, lam, out, only_mask);
 }
 
 }  // namespace mlg

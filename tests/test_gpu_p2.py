@@ -2,8 +2,9 @@
 numbering, 6-dof connectivity, stiffness and mass CSR (bitwise for the Laplace
 field, a few ulp for the variable field's exp), the full-space SpMV, the P2
 prolongation and its transpose (bitwise), and the level-1 dense eigensolve.
-Mirrors test_fespace.cpp:34-60,121-128,187-213.  The correction step itself is
-P1-only on the B200 path and says so."""
+Mirrors test_fespace.cpp:34-60,121-128,187-213.  The correction step is
+run by the degree-2 batched CG (cg_p2.cu) and checked against the reference's
+multilevel run."""
 import numpy as np
 import pytest
 
@@ -95,7 +96,54 @@ def test_p2_coarse_eigensolve_and_mass(mlg, oracle_ref):
     assert abs(ones @ hy.apply(2, "mass", ones) - 4.0) <= 1e-12 * 4.0
 
 
-def test_p2_correction_step_reports_scope(mlg, oracle_ref):
-    hy, _ = pair(mlg, oracle_ref, SQUARE, 0.25, 4, 2)
-    with pytest.raises(mlg.ConfigError, match="P2"):
-        mlg.multilevel_correction(hy)
+@pytest.mark.parametrize("spec", [(SQUARE, 0.25, 4, 3, 2), (SQUARE, 0.5, 1, 3, 3),
+                                  ((0.0, 1.0, 0.0, 1.0), 1 / 8, 4, 3, 1)])
+def test_p2_multilevel_matches_reference(mlg, oracle_ref, spec):
+    """The whole degree-2 multilevel correction (P2 batched CG, strip, arrowhead /
+    dense augmented solve) vs the reference with degree 2."""
+    domain, H, m, levels, nev = spec
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*domain), H=H, delta=H, m=m, n_levels=levels,
+                        nev=nev, degree=2)
+    hy = mlg.Hierarchy(cfg)
+    rh = oracle_ref.RefHierarchy(domain=domain, H=H, delta=H, m=m, n_levels=levels, nev=nev,
+                                 degree=2)
+    lam_g, pairs, matched, _ = mlg.multilevel_correction(hy)
+    lam_r, co_r, matched_r, _ = rh.multilevel(levels, nev)
+    for k in range(levels):
+        assert np.max(np.abs(lam_g[k] - lam_r[k]) / lam_r[k]) <= 1e-10, (k, lam_g, lam_r)
+    rh.extend_to(levels)
+    compare_pairs(lam_g[-1], [p.coeffs for p in pairs], lam_r[-1], co_r,
+                  lambda f: rh.apply(levels, "mass", f), lambda v: hy.expand_interior(levels, v))
+    assert list(matched) == list(matched_r)
+
+
+def test_p2_local_solve_matches_reference(mlg, oracle_ref):
+    hy, rh = pair(mlg, oracle_ref, SQUARE, 0.25, 4, 2)
+    lam, co = rh.coarse_eigensolve(1, 1)
+    u = rh.prolong(hy.expand_interior(1, co[0]), 1, 2)
+    for j in range(4):
+        e_g, rep = mlg.local_bvp_solve(hy, 2, j, lam[0], u, 1e-12)
+        e_r, it_r, _ = rh.local_bvp_solve(2, j, lam[0], u, 1e-12)
+        assert rep.converged and abs(rep.iterations - it_r) <= 2
+        assert np.max(np.abs(e_g - e_r)) <= 1e-10 * max(1.0, np.max(np.abs(e_r)))
+
+
+def test_p2_errors_and_report_match_reference(mlg, oracle_ref, tmp_path):
+    """compute_errors with P2 shape functions and the degree-2 run_experiment vs the
+    reference's (harness.cpp:171-222 with degree 2)."""
+    from paper_1401_4969_b200 import harness as H
+    kw = dict(domain=SQUARE, H=0.5, delta=0.5, m=1, n_levels=3, nev=2, degree=2)
+    ref_csv = tmp_path / "ref.csv"
+    oracle_ref.run_experiment(ref_csv, **kw)
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*SQUARE), H=0.5, delta=0.5, m=1, n_levels=3,
+                        nev=2, degree=2)
+    H.run_experiment(cfg, str(tmp_path / "ours.csv"))
+    a = (tmp_path / "ours.csv").read_text().splitlines()
+    b = ref_csv.read_text().splitlines()
+    assert a[0] == b[0] and len(a) == len(b)
+    for la, lb in zip(a[1:], b[1:]):
+        fa, fb = la.split(","), lb.split(",")
+        assert fa[:4] == fb[:4]
+        assert abs(float(fa[4]) - float(fb[4])) <= 1e-10 * float(fb[4])
+        if fb[6]:
+            assert abs(float(fa[6]) - float(fb[6])) <= 1e-7 * float(fb[6]), (fa, fb)
