@@ -52,7 +52,7 @@ typedef struct mlg_config {
   double delta;                      /* requested overlap (rounded up to the lattice) */
   int m;                             /* subdomain count (perfect square) */
   int n_levels;
-  int degree; /* 1 (P2 is not on the B200 path: ConfigError) */
+  int degree; /* 1 (P1) or 2 (P2, fespace.cpp:230-312) */
   int nev;
   int example;
   int workers; /* accepted for parity; the GPU path has no worker threads */
@@ -124,7 +124,8 @@ int mlg_export_mesh(mlg_ctx* ctx, int level, double* vertices, int* vertex_latti
                     int* triangles, int* parent, int* boundary_edges);
 
 /* FeSpace (fespace.hpp:52-65): dof_lattice[ndofs][2] (half units),
- * interior_dofs[n_interior], interior_index[ndofs], connectivity[nt][3]. */
+ * interior_dofs[n_interior], interior_index[ndofs], connectivity[nt][3]
+ * (P1) or [nt][6] (P2: v0, v1, v2, m01, m12, m20). */
 int mlg_export_space(mlg_ctx* ctx, int level, int* dof_lattice, int* interior_dofs,
                      int* interior_index, int* connectivity3);
 
