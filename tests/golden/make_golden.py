@@ -121,6 +121,24 @@ def lshape_run(H, delta, m, levels, nev):
             "generator": "oracle/restate.py", "seconds": time.time() - t}
 
 
+def p2_fixtures():
+    h = ref.RefHierarchy(domain=SQUARE, H=0.25, delta=0.25, m=4, n_levels=3, nev=2, degree=2)
+    h.extend_to(3)
+    f = ref.fnv1a64
+    sp = h.space(3)
+    out = {"space": [f(sp["dof_lattice"]), f(sp["interior_dofs"]), f(sp["connectivity"])]}
+    for form in ("stiffness", "mass"):
+        rp, cols, v = h.csr(3, form)
+        out[form] = [f(rp), f(cols), f(v)]
+    lam, co, matched, _ = h.multilevel(3, 2)
+    out["multilevel"] = {"config": dict(domain=SQUARE, H=0.25, delta=0.25, m=4, n_levels=3,
+                                        nev=2, degree=2),
+                         "lambdas": lam.tolist(), "matched": matched.tolist(),
+                         "projections": projections(co)}
+    h.close()
+    return out
+
+
 def variable_values():
     """Variable-field operator values at (-1,1)^2, H=0.25, level 3: exact digests
     (for the record: exp() differs between libms, so consumers compare values to
@@ -212,6 +230,11 @@ def main():
             path.write_text(json.dumps(g, indent=1))
     if "variable_values" not in g:
         g["variable_values"] = variable_values()
+    # P2 (degree 2): the reference's own path -- digests of the level-3 space and
+    # operators and a multilevel run
+    if "p2" not in g:
+        g["p2"] = p2_fixtures()
+        path.write_text(json.dumps(g, indent=1))
     # Example "reaction" (BASELINE config 4): no reference code path, so these
     # fixtures come from the numpy restatement (oracle/restate.py) -- parity
     # unpinned against the reference, pinned against our own restatement.

@@ -147,3 +147,23 @@ def test_p2_errors_and_report_match_reference(mlg, oracle_ref, tmp_path):
         assert abs(float(fa[4]) - float(fb[4])) <= 1e-10 * float(fb[4])
         if fb[6]:
             assert abs(float(fa[6]) - float(fb[6])) <= 1e-7 * float(fb[6]), (fa, fb)
+
+
+def test_p2_golden_fixtures(mlg):
+    """Against the committed fixtures only (no reference at run time)."""
+    import json
+    from pathlib import Path
+    from oracle.ref import fnv1a64 as f
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "golden.json").read_text())["p2"]
+    c = g["multilevel"]["config"]
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*c["domain"]), H=c["H"], delta=c["delta"],
+                        m=c["m"], n_levels=c["n_levels"], nev=c["nev"], degree=2)
+    with mlg.Hierarchy(cfg) as hy:
+        hy.extend_to(3)
+        sp = hy.space(3)
+        assert [f(sp.dof_lattice), f(sp.interior_dofs), f(sp.connectivity)] == g["space"]
+        for form in ("stiffness", "mass"):
+            assert [f(a) for a in hy.csr(3, form)] == g[form]
+        lam, pairs, matched, _ = mlg.multilevel_correction(hy)
+        ref = np.array(g["multilevel"]["lambdas"])
+        assert np.max(np.abs(lam - ref) / ref) <= 1e-10
