@@ -74,6 +74,24 @@ __device__ __forceinline__ void tile_store(double (&acc)[K], double* out) {
   block_reduce_store<K, kT>(acc, out);
 }
 
+// Sum of a system's tile partials (2 per tile) by one block of kF threads:
+// thread t takes tiles t, t + kF, ...; then a fixed tree -- the same order on
+// every run.  The result is valid in thread 0.
+constexpr int kF = 256;
+__device__ __forceinline__ void sys_sum(const CgSys& S, const double* part, double* a0,
+                                        double* a1) {
+  double acc[2] = {0.0, 0.0};
+  for (int t = threadIdx.x; t < S.ntiles; t += kF) {
+    acc[0] += part[2LL * (S.toff + t)];
+    acc[1] += part[2LL * (S.toff + t) + 1];
+  }
+  __shared__ double red[2];
+  block_reduce_store<2, kF>(acc, red);
+  __syncthreads();
+  *a0 = red[0];
+  *a1 = red[1];
+}
+
 __global__ void __launch_bounds__(kT) k_p2cg_init(const CgSys* sys, const int* tile_sys,
                                                   const int* tile_t, P2Args A, double* X,
                                                   double* R, double* P, double* part) {
@@ -95,16 +113,14 @@ __global__ void __launch_bounds__(kT) k_p2cg_init(const CgSys* sys, const int* t
   tile_store<2>(acc, part + 2LL * blockIdx.x);
 }
 
-__global__ void k_p2cg_init_final(int nsys, const CgSys* sys, const double* part, double tol,
-                                  P2Ctl* ctl) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nsys) return;
+__global__ void __launch_bounds__(kF) k_p2cg_init_final(int nsys, const CgSys* sys,
+                                                         const double* part, double tol,
+                                                         P2Ctl* ctl) {
+  const int s = blockIdx.x;
   const CgSys S = sys[s];
-  double bb = 0.0, rz = 0.0;
-  for (int t = 0; t < S.ntiles; ++t) {
-    bb += part[2LL * (S.toff + t)];
-    rz += part[2LL * (S.toff + t) + 1];
-  }
+  double bb, rz;
+  sys_sum(S, part, &bb, &rz);
+  if (threadIdx.x) return;
   P2Ctl c{};
   c.bnorm = sqrt(bb);
   c.rho = rz;
@@ -142,18 +158,16 @@ __global__ void __launch_bounds__(kT) k_p2cg_a(const CgSys* sys, const int* tile
   tile_store<2>(acc, part + 2LL * blockIdx.x);
 }
 
-__global__ void k_p2cg_a_final(int nsys, const CgSys* sys, const double* part, double tol,
-                               P2Ctl* ctl) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nsys) return;
+__global__ void __launch_bounds__(kF) k_p2cg_a_final(int nsys, const CgSys* sys,
+                                                      const double* part, double tol,
+                                                      P2Ctl* ctl) {
+  const int s = blockIdx.x;
   const CgSys S = sys[s];
   P2Ctl c = ctl[s];
-  if (c.state != kNormal && c.state != kCheck && c.state != kFinal) return;
-  double a0 = 0.0, a1 = 0.0;
-  for (int t = 0; t < S.ntiles; ++t) {
-    a0 += part[2LL * (S.toff + t)];
-    a1 += part[2LL * (S.toff + t) + 1];
-  }
+  if (c.state != kNormal && c.state != kCheck && c.state != kFinal) return;  // block-uniform
+  double a0, a1;
+  sys_sum(S, part, &a0, &a1);
+  if (threadIdx.x) return;
   if (c.state == kNormal) {
     if (a0 <= 0.0) {
       c.indefinite = 1;
@@ -210,20 +224,23 @@ __global__ void __launch_bounds__(kT) k_p2cg_b(const CgSys* sys, const int* tile
   tile_store<2>(acc, part + 2LL * blockIdx.x);
 }
 
-__global__ void k_p2cg_b_final(int nsys, const CgSys* sys, const double* part, double tol,
-                               P2Ctl* ctl) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nsys) return;
+__global__ void __launch_bounds__(kF) k_p2cg_b_final(int nsys, const CgSys* sys,
+                                                      const double* part, double tol,
+                                                      P2Ctl* ctl) {
+  const int s = blockIdx.x;
   const CgSys S = sys[s];
   P2Ctl c = ctl[s];
   if (c.state == kRestart) {
-    c.state = kNormal;
-  } else if (c.state == kNormal) {
-    double rr = 0.0, rz = 0.0;
-    for (int t = 0; t < S.ntiles; ++t) {
-      rr += part[2LL * (S.toff + t)];
-      rz += part[2LL * (S.toff + t) + 1];
+    if (threadIdx.x == 0) {
+      c.state = kNormal;
+      ctl[s] = c;
     }
+    return;
+  }
+  if (c.state == kNormal) {  // block-uniform
+    double rr, rz;
+    sys_sum(S, part, &rr, &rz);
+    if (threadIdx.x) return;
     c.iters += 1;
     if (sqrt(rr) <= tol * c.bnorm) {
       c.state = kCheck;
@@ -234,8 +251,8 @@ __global__ void k_p2cg_b_final(int nsys, const CgSys* sys, const double* part, d
       c.rho = rz;
       c.state = kPupd;
     }
+    ctl[s] = c;
   }
-  ctl[s] = c;
 }
 
 // Sweep C: p = z + beta p.
@@ -317,10 +334,11 @@ CgResult CgBatchP2::solve(Ctx& c, double tol) {
   const int* ts = tsys_.get();
   const int* tt = tt_.get();
   const unsigned sb = static_cast<unsigned>((nsys + 127) / 128);
+  const unsigned nb = static_cast<unsigned>(nsys);  // one block per system (sys_sum)
   k_p2cg_init<<<ntiles_, kT, 0, c.stream>>>(sd, ts, tt, A, X_.get(), R_.get(), P_.get(),
                                            part_.get());
   MLG_LAUNCH_CHECK();
-  k_p2cg_init_final<<<sb, 128, 0, c.stream>>>(nsys, sd, part_.get(), tol, ctl);
+  k_p2cg_init_final<<<nb, kF, 0, c.stream>>>(nsys, sd, part_.get(), tol, ctl);
   MLG_LAUNCH_CHECK();
   long long max_maxit = 0;
   for (const CgSys& s : sys_h_) max_maxit = std::max<long long>(max_maxit, s.maxit);
@@ -329,10 +347,10 @@ CgResult CgBatchP2::solve(Ctx& c, double tol) {
     for (int k = 0; k < kChunk; ++k) {
       k_p2cg_a<<<ntiles_, kT, 0, c.stream>>>(sd, ts, tt, A, ctl, X_.get(), R_.get(), P_.get(),
                                             Q_.get(), part_.get());
-      k_p2cg_a_final<<<sb, 128, 0, c.stream>>>(nsys, sd, part_.get(), tol, ctl);
+      k_p2cg_a_final<<<nb, kF, 0, c.stream>>>(nsys, sd, part_.get(), tol, ctl);
       k_p2cg_b<<<ntiles_, kT, 0, c.stream>>>(sd, ts, tt, A, ctl, X_.get(), R_.get(), P_.get(),
                                             Q_.get(), part_.get());
-      k_p2cg_b_final<<<sb, 128, 0, c.stream>>>(nsys, sd, part_.get(), tol, ctl);
+      k_p2cg_b_final<<<nb, kF, 0, c.stream>>>(nsys, sd, part_.get(), tol, ctl);
       k_p2cg_c<<<ntiles_, kT, 0, c.stream>>>(sd, ts, tt, A, ctl, R_.get(), P_.get());
       running_.zero(c.stream);
       k_p2cg_c_final<<<sb, 128, 0, c.stream>>>(nsys, ctl, running_.get());
