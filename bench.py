@@ -57,14 +57,17 @@ WORKLOADS = {
 FALLBACK_HBM = 6650.0
 
 
-def cg_bytes_per_row(uniform=False):
+def cg_bytes_per_row(uniform=0):
     """Algorithmic HBM bytes per window row of one CG iteration launch (k_cg_iter,
     the fused one-reduction PCG sweep): update mode reads x, r, p and writes x, r,
     p (6 x 8 B = 48 B); true-residual mode reads x and b and writes r (24 B).
     Non-uniform levels add the stencil {C,E,N,NE} and D^-1 (40 B); on uniform
-    levels they are kernel parameters.  Stencil neighbours come from registers
-    and warp shuffles, so nothing else is re-read.  Returns (update, check)."""
-    return (48, 24) if uniform else (88, 64)
+    levels they are kernel parameters.  uniform == 2: x updates deferred in
+    pairs -- one launch moves r, p (32 B), the next r, p, x and the deferred
+    update's p (56 B): 44 B/row per launch of a sampled pair.  Stencil
+    neighbours come from registers and warp shuffles, so nothing else is
+    re-read.  Returns (update, check)."""
+    return {0: (88, 64), 1: (48, 24), 2: (44, 24)}[int(uniform)]
 
 
 # ----------------------------------------------------------------- helpers ---
@@ -317,7 +320,7 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
             "algorithmic_bytes_per_launch": ka_bytes / ka_n,
             "bytes_per_row": bpr, "bytes_per_check_row": bpc,
             "rows_per_launch": (ka_rows + ka_chk) / ka_n,
-            "uniform_stencil": bool(tims[-1].spmv_uniform_stencil),
+            "uniform_stencil": int(tims[-1].spmv_uniform_stencil),
             "avg_launch_ms": ka_ms / ka_n, "launches": int(ka_n),
             "share_of_step": ka_ms * 1e-3 / sum(step_s),
         }

@@ -99,7 +99,9 @@ typedef struct mlg_step_timings {
   double step_seconds;     /* CUDA events on the context stream around the whole call,
                               host<->device copies included for the host-array variant */
   int spmv_uniform_stencil; /* 1: stencil/D^-1 taken from kernel parameters (no
-                               coefficient stream: 48 B/row instead of 88) */
+                               coefficient stream: 48 B/row instead of 88); 2: the
+                               same with x updates deferred in pairs (44 B/row
+                               averaged over a launch pair); 0: general stencil */
   double spmv_check_rows;  /* rows the same launches swept in true-residual mode */
 } mlg_step_timings;
 

@@ -86,7 +86,7 @@ class StepTimings:  # corrector.hpp:97-101 (+ device evidence)
     spmv_rows: float = 0.0
     kernel_launches: int = 0
     step_seconds: float = 0.0
-    spmv_uniform_stencil: bool = False
+    spmv_uniform_stencil: int = 0  # 0 general, 1 uniform, 2 uniform + deferred x
     spmv_check_rows: float = 0.0
 
     @classmethod
@@ -94,7 +94,7 @@ class StepTimings:  # corrector.hpp:97-101 (+ device evidence)
         return cls(t.local_seconds, t.iface_seconds, t.aug_seconds, t.build_seconds,
                    t.local_iterations_max, t.strip_iterations_max, t.spmv_kernel_ms,
                    t.spmv_launches, t.spmv_rows, t.kernel_launches, t.step_seconds,
-                   bool(t.spmv_uniform_stencil), t.spmv_check_rows)
+                   int(t.spmv_uniform_stencil), t.spmv_check_rows)
 
 
 @dataclass

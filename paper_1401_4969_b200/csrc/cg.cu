@@ -600,14 +600,28 @@ __device__ __forceinline__ void sweep_edge(const CgSys& S, const SweepArgs& A, c
 #define MLG_CG_D 8
 #endif
 #ifndef MLG_CG_ASYNC_MINBLOCKS
-#define MLG_CG_ASYNC_MINBLOCKS 6
+#define MLG_CG_ASYNC_MINBLOCKS 5  // the 4-array ring (deferred x) with 5 CTAs/SM: no spills
 #endif
 constexpr int kD = MLG_CG_D;
 static_assert((kD & (kD - 1)) == 0 && kD >= 4, "ring depth must be a power of two >= 4");
 
+#ifndef MLG_CG_RINGA
+#define MLG_CG_RINGA 4
+#endif
 struct RowRing {
-  double v[kD][3][32];  // [slot][p, r, x][lane]
+  double v[kD][MLG_CG_RINGA][32];  // [slot][p, r, x, p of a deferred x update][lane]
 };
+
+// x and the deferred update's p are read once (no halo reuse): keep them out of L1.
+__device__ __forceinline__ void cp_async8_cg(double* sdst, const double* gsrc) {
+#ifdef MLG_CG_XCG
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+#else
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+#endif
+}
 
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
@@ -627,9 +641,14 @@ __device__ __forceinline__ void cp_async_wait() {
 // instead of copied) and their new p is forced to zero, which reproduces the
 // flagged product exactly (an absent neighbour contributes a literal 0 to the
 // same paired-FMA chain).
-template <bool RST, bool LAP, bool EDGE, bool SLOW, bool MASKED = true>
+// XM: 2 = x += al * p (the reference order), 0 = x untouched (update
+// deferred to the next launch), 1 = x += alp * p_prev + al * p (two updates:
+// the deferred one and this launch's).  Averaged over a 0/1 pair the x stream
+// costs 12 B/row per iteration instead of 16.
+template <bool RST, bool LAP, bool EDGE, bool SLOW, bool MASKED = true, int XM = 2>
 __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, const Task& k,
-                                            double al, double be, double* __restrict__ X,
+                                            double al, double be, double alp,
+                                            double* __restrict__ X,
                                             const double* __restrict__ Rc,
                                             double* __restrict__ Rn,
                                             const double* __restrict__ Pc,
@@ -651,7 +670,9 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
       const long long o = base + row * w;
       cp_async8(&ring.v[s][0][lane], Pc + o);
       cp_async8(&ring.v[s][1][lane], Rc + o);
-      cp_async8(&ring.v[s][2][lane], X + o);
+      if (XM != 0) cp_async8_cg(&ring.v[s][2][lane], X + o);
+      if constexpr (XM == 1 && MLG_CG_RINGA > 3)
+        cp_async8_cg(&ring.v[s][MLG_CG_RINGA - 1][lane], Pn + o);  // p of the deferred update
     }
     cp_async_commit();
   };
@@ -669,14 +690,15 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     const int sc = n & (kD - 1);
     const double pc = ring.v[(n + 1) & (kD - 1)][0][lane];
     const double rb = ring.v[sc][1][lane];
-    const double xb = ring.v[sc][2][lane];
+    const double xb = XM != 0 ? ring.v[sc][2][lane] : 0.0;
     bool b_in = true;
     if constexpr (EDGE) b_in = rm.template in<SLOW, MASKED>(n, f, A.sg);
     double rn = rb, xn = xb;
     if constexpr (!RST) {
       const double qo = product_lat<LAP, false>(pa, pb, pc, u, lat1);
       rn = fma(-al, qo, rb);
-      xn = fma(al, pb, xb);
+      if constexpr (XM == 1) xn = fma(al, pb, fma(alp, ring.v[sc][MLG_CG_RINGA - 1][lane], xb));
+      else if constexpr (XM == 2) xn = fma(al, pb, xb);
     }
     if constexpr (EDGE) rn = b_in ? rn : 0.0;
     const double tz = xmul(dv, rn);
@@ -685,7 +707,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     if constexpr (decltype(store)::value) {
       if (own && b_in) {
         const long long o = base + n * w;
-        X[o] = xn;
+        if (XM != 0) X[o] = xn;
         Rn[o] = rn;
         Pn[o] = tp;
       }
@@ -726,11 +748,13 @@ enum Phase { kPhaseInit = 0, kPhaseIter = 1 };
 // Scalar recurrences of cg_solve for one system after a launch's reduction.
 template <int PH>
 __device__ __forceinline__ void update_ctl(CgCtl& c, const double (&a)[kCgDots], double tol,
-                                           int maxit) {
+                                           int maxit, int xdefer = 0) {
   if (PH == kPhaseInit) {
     c.bnorm = sqrt(a[0]);
     c.iters = 0;
     c.alpha = c.beta = c.rho = 0.0;
+    c.alpha_prev = 0.0;
+    c.xphase = 0;
     c.restart = 1;
     if (c.bnorm == 0.0) {  // sparse.cpp:208-212
       c.status = kConverged;
@@ -742,11 +766,25 @@ __device__ __forceinline__ void update_ctl(CgCtl& c, const double (&a)[kCgDots],
     }
     return;
   }
+  if (c.mode == kModeFlush) {  // the deferred x update is applied: x is current
+    c.xphase = 0;
+    c.mode = kModeCheck;
+    return;
+  }
   if (c.mode == kModeNormal) {
     const bool updated = !c.restart;
     if (updated) c.iters += 1;
+    if (updated && xdefer) {  // this launch deferred (phase 0) or caught up (phase 1)
+      if (c.xphase == 0) {
+        c.alpha_prev = c.alpha;
+        c.xphase = 1;
+      } else {
+        c.xphase = 0;
+      }
+    }
     if (updated && (sqrt(a[0]) <= tol * c.bnorm || c.iters >= maxit)) {
-      c.mode = kModeCheck;  // confirm with the true residual (sparse.cpp:232-246)
+      // confirm with the true residual (sparse.cpp:232-246), once x is current
+      c.mode = c.xphase ? kModeFlush : kModeCheck;
       return;
     }
     const double pq = a[2];
@@ -775,6 +813,7 @@ __device__ __forceinline__ void update_ctl(CgCtl& c, const double (&a)[kCgDots],
     } else {  // restart from the true residual: p = z, no pending update
       c.restart = 1;
       c.alpha = c.beta = 0.0;
+      c.xphase = 0;
       c.mode = kModeNormal;
     }
   }
@@ -787,6 +826,7 @@ struct Finish {
   double tol;
   unsigned long long* rows;  // sampled launches: [update-mode rows, check-mode rows]
   int* active;               // systems still running (decremented when one stops)
+  int xdefer;                // 1: x updates are deferred in pairs (async batches)
 };
 
 // Scalars of a system as last written by any CTA (L2, not a stale L1 line).
@@ -801,6 +841,8 @@ __device__ __forceinline__ CgCtl load_ctl(const CgCtl* p) {
   c.restart = __ldcg(&p->restart);
   c.iters = __ldcg(&p->iters);
   c.status = __ldcg(&p->status);
+  c.alpha_prev = __ldcg(&p->alpha_prev);
+  c.xphase = __ldcg(&p->xphase);
   return c;
 }
 
@@ -853,7 +895,7 @@ __device__ __forceinline__ void finish_tile(const CgSys& S, int sys, int t,
       }
       CgCtl c = load_ctl(F.ctl + sys);
       const bool was_running = PH == kPhaseInit || c.status == kRunning;
-      update_ctl<PH>(c, a, F.tol, S.maxit);
+      update_ctl<PH>(c, a, F.tol, S.maxit, F.xdefer);
       F.ctl[sys] = c;
       F.counter[sys] = 0u;
       if (was_running && c.status != kRunning) atomicSub(F.active, 1);
@@ -893,6 +935,35 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
 // One tile (kCgWarps warp tasks of one system) of one CG iteration.  PERSIST:
 // called from the persistent kernel (L1-bypassing iterate loads, rows counted
 // in `rows_acc` instead of per-launch atomics).
+// Async sweep with the x-update mode of this launch (see sweep_async): with
+// deferral on, a restart launch leaves x alone, xphase 0 defers, xphase 1
+// applies the deferred update and this launch's.
+template <bool LAP, bool EDGE, bool SLOW, bool MASKED>
+__device__ __forceinline__ void sweep_async_x(bool rst, int xdefer, int xph, const CgSys& S,
+                                              const SweepArgs& A, const Task& k, double al,
+                                              double be, double alp, double* X,
+                                              const double* Rc, double* Rn, const double* Pc,
+                                              double* Pn, double (&acc)[kCgDots], RowRing& ring,
+                                              Xchg& xch) {
+  if (rst) {
+    if (xdefer)
+      sweep_async<true, LAP, EDGE, SLOW, MASKED, 0>(S, A, k, al, be, alp, X, Rc, Rn, Pc, Pn, acc,
+                                                    ring, xch);
+    else
+      sweep_async<true, LAP, EDGE, SLOW, MASKED, 2>(S, A, k, al, be, alp, X, Rc, Rn, Pc, Pn, acc,
+                                                    ring, xch);
+  } else if (!xdefer) {
+    sweep_async<false, LAP, EDGE, SLOW, MASKED, 2>(S, A, k, al, be, alp, X, Rc, Rn, Pc, Pn, acc,
+                                                   ring, xch);
+  } else if (xph) {
+    sweep_async<false, LAP, EDGE, SLOW, MASKED, 1>(S, A, k, al, be, alp, X, Rc, Rn, Pc, Pn, acc,
+                                                   ring, xch);
+  } else {
+    sweep_async<false, LAP, EDGE, SLOW, MASKED, 0>(S, A, k, al, be, alp, X, Rc, Rn, Pc, Pn, acc,
+                                                   ring, xch);
+  }
+}
+
 template <bool UNI, bool ASYNC, bool PERSIST, bool LAP>
 __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mode, double al,
                                         double be, bool rst, const SweepArgs& A,
@@ -900,8 +971,20 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
                                         const double* __restrict__ Rc, double* __restrict__ Rn,
                                         const double* __restrict__ Pc, double* __restrict__ Pn,
                                         const Finish& F, RowRing* s_ring,
-                                        unsigned long long& rows_acc) {
+                                        unsigned long long& rows_acc, double alp = 0.0,
+                                        int xph = 0) {
   if (mode == kModeSkip) return;  // uniform across the system's tiles
+  if (mode == kModeFlush) {  // apply the deferred x update at owned rows (no neighbours)
+    const Task k = task_of(S, tl.t, A.task_map);
+    if (out_lane(S, k))
+      for (int ly = k.ly0; ly < k.ly1; ++ly) {
+        const long long v = cg_index(S, ly, k.col);
+        X[v] = fma(alp, Pn[v], X[v]);  // points outside the system hold p = 0
+      }
+    double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
+    return;
+  }
   __shared__ Xchg s_xch[kCgWarps];
   Xchg& xch = s_xch[threadIdx.x >> 5];
   const Task k = task_of(S, tl.t, A.task_map);
@@ -923,10 +1006,8 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
   if (fast) {
     if constexpr (ASYNC) {
       RowRing& ring = s_ring[threadIdx.x >> 5];
-      if (rst)
-        sweep_async<true, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
-      else
-        sweep_async<false, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
+      sweep_async_x<LAP, false, false, true>(rst, F.xdefer, xph, S, A, k, al, be, alp, X, Rc, Rn,
+                                             Pc, Pn, acc, ring, xch);
     } else {
       if (rst)
         sweep_reg<true, PERSIST, LAP, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
@@ -938,22 +1019,15 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
     const int bhs = A.sg.bh * A.sg.scale;  // see sweep_edge
     const bool slow = A.mask && (S.y0 + min(k.ly1 + 4, S.h - 1)) / bhs -
                                         (S.y0 + max(k.ly0 - 2, 0)) / bhs > 2;
-    if (slow) {
-      if (rst)
-        sweep_async<true, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
-      else
-        sweep_async<false, LAP, true, true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
-    } else if (A.mask) {
-      if (rst)
-        sweep_async<true, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
-      else
-        sweep_async<false, LAP, true, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
-    } else {
-      if (rst)
-        sweep_async<true, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
-      else
-        sweep_async<false, LAP, true, false, false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, ring, xch);
-    }
+    if (slow)
+      sweep_async_x<LAP, true, true, true>(rst, F.xdefer, xph, S, A, k, al, be, alp, X, Rc, Rn,
+                                           Pc, Pn, acc, ring, xch);
+    else if (A.mask)
+      sweep_async_x<LAP, true, false, true>(rst, F.xdefer, xph, S, A, k, al, be, alp, X, Rc, Rn,
+                                            Pc, Pn, acc, ring, xch);
+    else
+      sweep_async_x<LAP, true, false, false>(rst, F.xdefer, xph, S, A, k, al, be, alp, X, Rc,
+                                             Rn, Pc, Pn, acc, ring, xch);
   } else if (flagged) {
     if (rst)
       sweep_edge<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
@@ -1057,7 +1131,8 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
   __syncthreads();
   unsigned long long rows_acc = 0;
   cg_tile<UNI, ASYNC, false, LAP>(S, tl, s_c.mode, s_c.alpha, s_c.beta, s_c.restart != 0, A, bsrc,
-                             bstride, X, Rc, Rn, Pc, Pn, F, s_ring, rows_acc);
+                             bstride, X, Rc, Rn, Pc, Pn, F, s_ring, rows_acc, s_c.alpha_prev,
+                             s_c.xphase);
 }
 
 // ---- persistent variant: all iterations of a batch in one launch -----------
@@ -1193,7 +1268,7 @@ __global__ void __launch_bounds__(kBlock, MLG_CG_PERSIST_MINBLOCKS * 4 / kCgWarp
           a[q] = v;
         }
         CgCtl c = s_ctl[i];
-        if (c.mode != kModeSkip) update_ctl<kPhaseIter>(c, a, F.tol, S.maxit);
+        if (c.mode != kModeSkip) update_ctl<kPhaseIter>(c, a, F.tol, S.maxit, F.xdefer);
         s_ctl[i] = c;
         if (s_tl[i].t == 0 && c.status == kRunning) atomicAdd(G.running + it % 3, 1u);
       }
@@ -1561,8 +1636,16 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
   gsync.zero(st);
   active_d.ensure(1);
   active_d.upload(&nsys, 1, st);
-  const Finish F{part.get(), counters.get(), ctl_d.get(), tol, nullptr, active_d.get()};
-  const Finish Fp{part.get(), counters.get(), ctl_d.get(), tol, prof_rows.get(), active_d.get()};
+  // Deferred x updates in pairs for the HBM-streaming (async) batches: 44 B/row
+  // per iteration on average instead of 48 (MLG_CG_XDEFER=0 turns it off).
+  static const int xdefer_env = [] {
+    const char* e = std::getenv("MLG_CG_XDEFER");
+    return e ? std::atoi(e) : 1;
+  }();
+  const int xdefer = use_async && xdefer_env && MLG_CG_RINGA > 3 ? 1 : 0;
+  const Finish F{part.get(), counters.get(), ctl_d.get(), tol, nullptr, active_d.get(), xdefer};
+  const Finish Fp{part.get(), counters.get(), ctl_d.get(), tol, prof_rows.get(), active_d.get(),
+                  xdefer};
   double *rc = R0.get(), *rn = R1.get(), *pc = P0.get(), *pn = P1.get();
 
   if (uni)
@@ -1691,7 +1774,9 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       const unsigned nt = static_cast<unsigned>(tiles.size());
       // Kernel timing evidence: every 4th launch of the local solves is
       // bracketed by pooled CUDA events (cheap enough not to starve the stream).
-      const bool prof = profiling && (iter_count++ % 4 == 0);
+      // (pairs of consecutive launches: with deferred x updates the two phases
+      // move 32 and 56 B/row, so a pair is the unit the 44 B/row average holds for)
+      const bool prof = profiling && (iter_count++ % 4 < 2);
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (prof) {
         ev0 = c.event(2 * evs.size());
@@ -1754,7 +1839,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     c.times.ka_rows += static_cast<double>(rows[0]);
     c.times.ka_check_rows += static_cast<double>(rows[1]);
   }
-  c.times.ka_uniform = uni ? 1 : 0;
+  c.times.ka_uniform = uni ? (use_async && xdefer_env && MLG_CG_RINGA > 3 ? 2 : 1) : 0;
   CgResult res;
   res.reports.resize(ctl.size());
   for (std::size_t k = 0; k < ctl.size(); ++k) {

@@ -52,9 +52,14 @@ struct CgTile {
 struct CgCtl {
   double alpha, beta, rho, bnorm, final_res;
   int mode, restart, iters, status;
+  // Deferred x updates (HBM-streaming batches): xphase 1 = the last launch
+  // left x += alpha_prev * p_prev pending (p_prev is in the "new" p buffer of
+  // the following launch); the next launch applies both updates at once.
+  double alpha_prev;
+  int xphase;
 };
 
-enum : int { kModeSkip = 0, kModeNormal = 1, kModeCheck = 2 };
+enum : int { kModeSkip = 0, kModeNormal = 1, kModeCheck = 2, kModeFlush = 3 };
 enum : int { kRunning = 0, kConverged = 1, kNotConverged = 2, kIndefinite = 3 };
 
 #ifndef MLG_CG_WARPS
