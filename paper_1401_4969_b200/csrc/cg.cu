@@ -974,16 +974,18 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
                                         unsigned long long& rows_acc, double alp = 0.0,
                                         int xph = 0) {
   if (mode == kModeSkip) return;  // uniform across the system's tiles
-  if (mode == kModeFlush) {  // apply the deferred x update at owned rows (no neighbours)
-    const Task k = task_of(S, tl.t, A.task_map);
-    if (out_lane(S, k))
-      for (int ly = k.ly0; ly < k.ly1; ++ly) {
-        const long long v = cg_index(S, ly, k.col);
-        X[v] = fma(alp, Pn[v], X[v]);  // points outside the system hold p = 0
-      }
-    double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
-    return;
+  if constexpr (ASYNC) {  // the only batches with deferred x updates
+    if (mode == kModeFlush) {  // apply the deferred x update at owned rows (no neighbours)
+      const Task k = task_of(S, tl.t, A.task_map);
+      if (out_lane(S, k))
+        for (int ly = k.ly0; ly < k.ly1; ++ly) {
+          const long long v = cg_index(S, ly, k.col);
+          X[v] = fma(alp, Pn[v], X[v]);  // points outside the system hold p = 0
+        }
+      double acc[kCgDots] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      finish_tile<kPhaseIter>(S, tl.sys, tl.t, acc, F);
+      return;
+    }
   }
   __shared__ Xchg s_xch[kCgWarps];
   Xchg& xch = s_xch[threadIdx.x >> 5];
@@ -1776,7 +1778,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       // bracketed by pooled CUDA events (cheap enough not to starve the stream).
       // (pairs of consecutive launches: with deferred x updates the two phases
       // move 32 and 56 B/row, so a pair is the unit the 44 B/row average holds for)
-      const bool prof = profiling && (iter_count++ % 4 < 2);
+      const bool prof = profiling && (iter_count++ % 8 < 2);
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (prof) {
         ev0 = c.event(2 * evs.size());
