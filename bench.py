@@ -313,7 +313,9 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
         peak, peak_src = measured_peak()
         tr = ncu_traffic(workload)
         out["roofline"] = {
-            "kernel": "k_cg_iter (local solves: fused PCG sweep, one launch per iteration)",
+            "kernel": ("k_cg_persist (local solves: the fused PCG sweep, all iterations in one "
+                       "cooperative launch, cp.async row ring)" if workload == "c2" else
+                       "k_cg_iter (local solves: fused PCG sweep, one launch per iteration)"),
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
             "traffic": None if tr is None else tr * (ka_rows + ka_chk) / ka_n,
