@@ -1671,7 +1671,15 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     const char* e = std::getenv("MLG_CG_XDEFER");
     return e ? std::atoi(e) : 1;
   }();
-  const int xdefer = use_async && xdefer_env && MLG_CG_RINGA > 3 ? 1 : 0;
+  static const int xdefer_p_env = [] {  // persistent batches on the ring (A/B hook)
+    const char* e = std::getenv("MLG_CG_XDEFER_P");
+    return e ? std::atoi(e) : 1;  // config 2: 31.1 -> 31.4 M DOF/s
+  }();
+  const int xdefer = ((use_async && xdefer_env) ||
+                      (use_persist && persist_async_on() && xdefer_p_env)) &&
+                             MLG_CG_RINGA > 3
+                         ? 1
+                         : 0;
   const Finish F{part.get(), counters.get(), ctl_d.get(), tol, nullptr, active_d.get(), xdefer};
   const Finish Fp{part.get(), counters.get(), ctl_d.get(), tol, prof_rows.get(), active_d.get(),
                   xdefer};
@@ -1873,7 +1881,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     c.times.ka_rows += static_cast<double>(rows[0]);
     c.times.ka_check_rows += static_cast<double>(rows[1]);
   }
-  c.times.ka_uniform = uni ? (use_async && xdefer_env && MLG_CG_RINGA > 3 ? 2 : 1) : 0;
+  c.times.ka_uniform = uni ? (xdefer ? 2 : 1) : 0;
   CgResult res;
   res.reports.resize(ctl.size());
   for (std::size_t k = 0; k < ctl.size(); ++k) {
