@@ -103,6 +103,9 @@ typedef struct mlg_step_timings {
                                same with x updates deferred in pairs (44 B/row
                                averaged over a launch pair); 0: general stencil */
   double spmv_check_rows;  /* rows the same launches swept in true-residual mode */
+  int64_t spmv_launches_all; /* all launches of that kernel in the step (sampled or not):
+                                the kernel's share of the step is
+                                spmv_kernel_ms / spmv_launches * spmv_launches_all */
 } mlg_step_timings;
 
 const char* mlg_last_error(void);

@@ -76,7 +76,7 @@ class MlgStepTimings(C.Structure):
         ("spmv_kernel_ms", C.c_double), ("spmv_launches", C.c_int64),
         ("spmv_rows", C.c_double), ("kernel_launches", C.c_int64),
         ("step_seconds", C.c_double), ("spmv_uniform_stencil", C.c_int),
-        ("spmv_check_rows", C.c_double),
+        ("spmv_check_rows", C.c_double), ("spmv_launches_all", C.c_int64),
     ]
 
 

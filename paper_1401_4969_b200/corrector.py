@@ -88,13 +88,14 @@ class StepTimings:  # corrector.hpp:97-101 (+ device evidence)
     step_seconds: float = 0.0
     spmv_uniform_stencil: int = 0  # 0 general, 1 uniform, 2 uniform + deferred x
     spmv_check_rows: float = 0.0
+    spmv_launches_all: int = 0  # every launch of the sampled kernel in the step
 
     @classmethod
     def from_c(cls, t: MlgStepTimings) -> "StepTimings":
         return cls(t.local_seconds, t.iface_seconds, t.aug_seconds, t.build_seconds,
                    t.local_iterations_max, t.strip_iterations_max, t.spmv_kernel_ms,
                    t.spmv_launches, t.spmv_rows, t.kernel_launches, t.step_seconds,
-                   int(t.spmv_uniform_stencil), t.spmv_check_rows)
+                   int(t.spmv_uniform_stencil), t.spmv_check_rows, t.spmv_launches_all)
 
 
 @dataclass

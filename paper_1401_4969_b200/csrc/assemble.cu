@@ -471,14 +471,15 @@ __global__ void k_cg_stencil(IMap im, const Stencil* st, const double* dinv, Ste
   dinv_out[d] = dinv[d];
 }
 
-// Clears *flag if any interior row of st / dinv differs bitwise from row (1,1).
-__global__ void k_uniform_check(int nx, int ny, const Stencil* st, const double* dinv,
-                                int* flag) {
+// Clears *flag if any interior row of st / dinv differs bitwise from the first one.
+__global__ void k_uniform_check(IMap im, const Stencil* st, const double* dinv, int* flag) {
   const std::int64_t k = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-  const int w = nx - 1;
-  if (k >= static_cast<std::int64_t>(w) * (ny - 1)) return;
-  const std::int64_t d = (k / w + 1) * (nx + 1) + (k % w + 1);
-  const std::int64_t d0 = (nx + 1) + 1;
+  if (k >= im.count()) return;
+  int ix, iy, ix0, iy0;
+  im.point(k, &ix, &iy);
+  im.point(0, &ix0, &iy0);
+  const std::int64_t d = static_cast<std::int64_t>(iy) * (im.nx + 1) + ix;
+  const std::int64_t d0 = static_cast<std::int64_t>(iy0) * (im.nx + 1) + ix0;
   const Stencil a = st[d], b = st[d0];
   const bool same = __double_as_longlong(a.c) == __double_as_longlong(b.c) &&
                     __double_as_longlong(a.e) == __double_as_longlong(b.e) &&
@@ -544,20 +545,27 @@ void assemble_level(Ctx& c, Level& L) {
                                                                 L.dinv.get(), L.stCG.get(),
                                                                 L.dinvCG.get());
     MLG_LAUNCH_CHECK();
-    c.sync();
-    return;
+    // the CG sweeps exclude the closed hole (its points and the re-entrant
+    // edges) by geometry, so the fast path applies when the interior rows agree
+    L.strip_geom.hx0 = L.hole.x0;
+    L.strip_geom.hx1 = L.hole.x1;
+    L.strip_geom.hy0 = L.hole.y0;
+    L.strip_geom.hy1 = L.hole.y1;
   }
   const char* env = std::getenv("MLG_GENERAL_STENCIL");
-  if (L.nx >= 2 && L.ny >= 2 && !(env && env[0] == '1')) {
+  const IMap im = L.imap();
+  if (L.nx >= 2 && L.ny >= 2 && im.count() > 0 && !(env && env[0] == '1')) {
     DevBuf<int> flag(1);
     const int one = 1;
     flag.upload(&one, 1, c.stream);
-    k_uniform_check<<<grid_for(L.nint(), kBlock), kBlock, 0, c.stream>>>(
-        L.nx, L.ny, L.stA.get(), L.dinv.get(), flag.get());
+    k_uniform_check<<<grid_for(im.count(), kBlock), kBlock, 0, c.stream>>>(
+        im, L.stA.get(), L.dinv.get(), flag.get());
     MLG_LAUNCH_CHECK();
     int f = 0;
     flag.download(&f, 1, c.stream);
-    const std::int64_t d0 = (L.nx + 1) + 1;
+    int ix0, iy0;
+    im.point(0, &ix0, &iy0);
+    const std::int64_t d0 = static_cast<std::int64_t>(iy0) * (L.nx + 1) + ix0;
     MLG_CUDA(cudaMemcpyAsync(&L.ust, L.stA.get() + d0, sizeof(Stencil), cudaMemcpyDeviceToHost,
                              c.stream));
     MLG_CUDA(cudaMemcpyAsync(&L.udinv, L.dinv.get() + d0, sizeof(double),

@@ -72,11 +72,13 @@ void fill_timings(mlg_step_timings* t, const mlg::StepTimes& s, const mlg::Ctx& 
   t->spmv_check_rows = c.times.ka_check_rows;
   t->kernel_launches = mlg::launch_counter().load() - c.times.launch_base;
   t->spmv_uniform_stencil = c.times.ka_uniform;
+  t->spmv_launches_all = c.times.ka_launches_all;
 }
 
 void reset_kernel_stats(mlg::Ctx& c) {
   c.times.ka_ms_sum = 0;
   c.times.ka_launches = 0;
+  c.times.ka_launches_all = 0;
   c.times.ka_rows = 0;
   c.times.ka_check_rows = 0;
   c.times.kernel_launches = 0;

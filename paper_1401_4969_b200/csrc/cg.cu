@@ -91,7 +91,7 @@ __device__ __forceinline__ bool in_strip(const StripGeom& g, int ix, int iy) {
   const int x1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
   const int y0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
   const int y1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
-  return !(ix >= x0 && ix <= x1 && iy >= y0 && iy <= y1);
+  return !(ix >= x0 && ix <= x1 && iy >= y0 && iy <= y1) && !g.in_hole(ix, iy);
 }
 
 // Old iterate at one row of the lane's column.
@@ -143,7 +143,8 @@ __device__ __forceinline__ void load_old(const CgSys& S, const SweepArgs& A, int
   }
   if (col < 0 || col >= S.w || ly < 0 || ly >= S.h) return;
   const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + col);
-  if (A.mask && !in_strip(A.sg, S.x0 + col, S.y0 + ly)) return;
+  if (A.mask ? !in_strip(A.sg, S.x0 + col, S.y0 + ly) : A.sg.in_hole(S.x0 + col, S.y0 + ly))
+    return;
   o.in = 1;
   if constexpr (!UNI) {
     o.st = A.st[g];
@@ -195,6 +196,7 @@ __device__ __forceinline__ double product(double sv, const Stencil& sst, int sin
 // Closed rectangle [xa,xb] x [ya,yb] (fine lattice) entirely inside the strip.
 __device__ __forceinline__ bool rect_in_strip(const StripGeom& g, int xa, int xb, int ya,
                                               int yb) {
+  if (g.rect_meets_hole(xa, xb, ya, yb)) return false;
   const int bxa = min(xa / (g.bw * g.scale), g.side - 1);
   const int bxb = min(xb / (g.bw * g.scale), g.side - 1);
   const int bya = min(ya / (g.bh * g.scale), g.side - 1);
@@ -214,6 +216,8 @@ __device__ __forceinline__ bool task_interior(const CgSys& S, const SweepArgs& A
   const int lane = threadIdx.x & 31;
   const int c0 = k.col - lane;  // column of lane 0 (warp-uniform)
   if (c0 < 0 || c0 + 31 >= S.w || k.ly0 - 2 < 0 || k.ly1 + 1 >= S.h) return false;
+  if (A.sg.rect_meets_hole(S.x0 + c0, S.x0 + c0 + 31, S.y0 + k.ly0 - 2, S.y0 + k.ly1 + 1))
+    return false;
   if (A.mask)
     return rect_in_strip(A.sg, S.x0 + c0, S.x0 + c0 + 31, S.y0 + k.ly0 - 2, S.y0 + k.ly1 + 1);
   return true;
@@ -256,14 +260,16 @@ __device__ __forceinline__ double product_flags(double sv, int sin_, double cv, 
 struct Flags {
   int cin;   // this lane's column is in the window
   int gx;    // ... and inside its block's G x-range (masked systems)
+  int hx;    // ... and inside the hole's x-range (domains with a hole)
   int masked;
   int h;
   int y0;    // window origin (fine lattice row of window row 0)
   // g: the kernel parameter's StripGeom (read in place, not copied)
   __device__ __forceinline__ int row_in(int ly, const StripGeom& g) const {
     if (!cin || ly < 0 || ly >= h) return 0;
-    if (!masked || !gx) return 1;
     const int iy = y0 + ly;
+    if (hx && iy >= g.hy0 && iy <= g.hy1) return 0;
+    if (!masked || !gx) return 1;
     const int by = min(iy / (g.bh * g.scale), g.side - 1);
     const int ya = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
     const int yb = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
@@ -278,6 +284,10 @@ __device__ __forceinline__ Flags make_flags(const CgSys& S, const SweepArgs& A, 
   f.h = S.h;
   f.y0 = S.y0;
   f.gx = 0;
+  {
+    const int ix = S.x0 + k.col;
+    f.hx = f.cin && ix >= A.sg.hx0 && ix <= A.sg.hx1;
+  }
   if (f.masked && f.cin) {
     const StripGeom& g = A.sg;
     const int ix = S.x0 + k.col;
@@ -401,16 +411,18 @@ __device__ __forceinline__ double product_int(double sv, double cv, double nv, c
 // task's rows fall in are precomputed; tasks spanning more blocks (tiny
 // levels) fall back to Flags::row_in.
 struct RowMask {
-  int h, cin, gx, slow;
+  int h, cin, gx, slow, hx;
   int ya0, yb0, ya1, yb1, ya2, yb2;  // window-row intervals of G (closed; empty = (1, 0))
+  int yh0, yh1;                      // window-row interval of the hole (closed; empty = (1, 0))
   // SLOW: tasks spanning > 3 blocks (tiny levels only); MASKED: strip systems
   template <bool SLOW, bool MASKED = true>
   __device__ __forceinline__ bool in(int r, const Flags& f, const StripGeom& g) const {
     if (SLOW) return f.row_in(r, g) != 0;
     const bool rowok = static_cast<unsigned>(r) < static_cast<unsigned>(h);
-    if (!MASKED) return cin & rowok;
+    const bool inh = hx & (r >= yh0) & (r <= yh1);
+    if (!MASKED) return cin & rowok & !inh;
     const bool ing = (r >= ya0 & r <= yb0) | (r >= ya1 & r <= yb1) | (r >= ya2 & r <= yb2);
-    return cin & rowok & !(gx & ing);
+    return cin & rowok & !(gx & ing) & !inh;
   }
 };
 
@@ -423,6 +435,9 @@ __device__ __forceinline__ RowMask make_rowmask(const CgSys& S, const SweepArgs&
   m.slow = 0;
   m.ya0 = m.ya1 = m.ya2 = 1;
   m.yb0 = m.yb1 = m.yb2 = 0;
+  m.hx = f.hx;
+  m.yh0 = A.sg.hy0 - S.y0;
+  m.yh1 = A.sg.hy1 - S.y0;
   if (f.masked) {
     const StripGeom& g = A.sg;
     const int bhs = g.bh * g.scale;
@@ -917,7 +932,8 @@ __global__ void __launch_bounds__(kBlock) k_cg_init(const CgSys* sys, const CgTi
       const long long g = static_cast<long long>(S.y0 + ly) * A.nxp1 + (S.x0 + k.col);
       const long long v = cg_index(S, ly, k.col);
       X[v] = 0.0;
-      if (A.mask && !in_strip(A.sg, S.x0 + k.col, S.y0 + ly)) {
+      if (A.mask ? !in_strip(A.sg, S.x0 + k.col, S.y0 + ly)
+                 : A.sg.in_hole(S.x0 + k.col, S.y0 + ly)) {
         R[v] = 0.0;
         continue;
       }
@@ -1521,7 +1537,7 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
       const int rb = t / s.nstrips, strip = t % s.nstrips;
       const int ca = s.x0 + strip * kCgCols, cb = s.x0 + std::min(strip * kCgCols + kCgCols, s.w) - 1;
       const int ra = s.y0 + rb * s.krows, rbb = s.y0 + std::min(rb * s.krows + s.krows, s.h) - 1;
-      if (!inside_g(ca, cb, ra, rbb)) tmap.push_back(t);
+      if (!inside_g(ca, cb, ra, rbb) && !g.rect_inside_hole(ca, cb, ra, rbb)) tmap.push_back(t);
     }
     for (CgSys& q : systems) {
       q.tmap_off = 0;
@@ -1568,6 +1584,7 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
 
 namespace {
 bool host_rect_in_strip(const StripGeom& g, int xa, int xb, int ya, int yb) {
+  if (g.rect_meets_hole(xa, xb, ya, yb)) return false;
   const int bxa = std::min(xa / (g.bw * g.scale), g.side - 1);
   const int bxb = std::min(xb / (g.bw * g.scale), g.side - 1);
   const int bya = std::min(ya / (g.bh * g.scale), g.side - 1);
@@ -1596,6 +1613,9 @@ double CgBatch::tile_cost(const CgTile& t, const std::vector<int>& tmap) const {
     const int rb = task / S.nstrips, strip = task % S.nstrips;
     const int c0 = strip * kCgCols - 2, ly0 = rb * S.krows, ly1 = std::min(ly0 + S.krows, S.h);
     bool interior = c0 >= 0 && c0 + 31 < S.w && ly0 - 2 >= 0 && ly1 + 1 < S.h;
+    if (interior && L->strip_geom.rect_meets_hole(S.x0 + c0, S.x0 + c0 + 31, S.y0 + ly0 - 2,
+                                                  S.y0 + ly1 + 1))
+      interior = false;
     if (interior && mask)
       interior = host_rect_in_strip(L->strip_geom, S.x0 + c0, S.x0 + c0 + 31, S.y0 + ly0 - 2,
                                     S.y0 + ly1 + 1);
@@ -1754,6 +1774,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       if (profiling) {
         MLG_CUDA(cudaEventRecord(ev1, st));
         evs.emplace_back(ev0, ev1);
+        ++c.times.ka_launches_all;
       }
       ctl_d.download(ctl.data(), ctl.size(), st);
       c.sync();
@@ -1819,6 +1840,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       // (pairs of consecutive launches: with deferred x updates the two phases
       // move 32 and 56 B/row, so a pair is the unit the 44 B/row average holds for)
       const bool prof = profiling && (iter_count++ % 8 < 2);
+      if (profiling) ++c.times.ka_launches_all;
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (prof) {
         ev0 = c.event(2 * evs.size());

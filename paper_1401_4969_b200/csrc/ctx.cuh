@@ -36,6 +36,18 @@ struct alignas(32) Stencil {
 // level: block grid, overlap cells and the fine/coarse scale 2^level.
 struct StripGeom {
   int side = 1, bw = 1, bh = 1, dc = 0, nx0 = 1, ny0 = 1, scale = 1;
+  // closed hole of a domain with a corner hole, fine lattice points of the
+  // level (hx1 < hx0: none): its points are outside every CG system
+  int hx0 = 1, hx1 = 0, hy0 = 1, hy1 = 0;
+  __host__ __device__ bool in_hole(int ix, int iy) const {
+    return ix >= hx0 && ix <= hx1 && iy >= hy0 && iy <= hy1;
+  }
+  __host__ __device__ bool rect_inside_hole(int xa, int xb, int ya, int yb) const {
+    return xa >= hx0 && xb <= hx1 && ya >= hy0 && yb <= hy1;
+  }
+  __host__ __device__ bool rect_meets_hole(int xa, int xb, int ya, int yb) const {
+    return xa <= hx1 && xb >= hx0 && ya <= hy1 && yb >= hy0;
+  }
 };
 
 // A rectangular hole [x0, x1) x [y0, y1) (lattice cells of one level) cut at
@@ -231,6 +243,7 @@ struct StepTimes {
   int local_iters_max = 0, strip_iters_max = 0;
   double ka_ms_sum = 0;  // summed device time of the local-solve SpMV kernel
   int ka_launches = 0;
+  long long ka_launches_all = 0;  // every launch of that kernel, sampled or not
   double ka_rows = 0;    // rows swept in CG-update mode by those launches (device count)
   double ka_check_rows = 0;  // ... in true-residual mode
   long long kernel_launches = 0;
