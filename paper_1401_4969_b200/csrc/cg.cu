@@ -1171,16 +1171,33 @@ struct GridSync {
 // Barrier number k (k = 1, 2, ... within the launch): arrive on a monotonic
 // counter and wait until it reaches k * gridDim.x -- one atomic round trip per
 // CTA, no reset/generation step on the critical path.
+// The wait polls with relaxed loads and acquires once: an acquire load also
+// invalidates the SM's L1 (CCTL.IVALL), which inside the poll loop would flush
+// the lines the other CTAs of the SM are still streaming through.
+#ifndef MLG_CG_BARPOLL
+#define MLG_CG_BARPOLL 1  // 0: acquire on every poll; 1: relaxed polls + one acquire
+#endif
 __device__ __forceinline__ void grid_sync(const GridSync& G, unsigned k) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(G.count, 1u);
     const unsigned target = k * gridDim.x;
     unsigned v;
+#if MLG_CG_BARPOLL >= 2
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(G.count) : "memory");
+#else
+    __threadfence();
+    atomicAdd(G.count, 1u);
+#endif
+#if MLG_CG_BARPOLL >= 1
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(G.count) : "memory");
+    } while (v < target);
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(G.count) : "memory");
+#else
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(G.count) : "memory");
     } while (v < target);
+#endif
   }
   __syncthreads();
 }
