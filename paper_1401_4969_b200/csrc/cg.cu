@@ -623,6 +623,10 @@ static_assert((kD & (kD - 1)) == 0 && kD >= 4, "ring depth must be a power of tw
 #ifndef MLG_CG_RINGA
 #define MLG_CG_RINGA 4
 #endif
+#ifndef MLG_CG_AUNR
+#define MLG_CG_AUNR 2  // unroll of the interior row loop (register rotation by renaming; A/B: 1 -> 2 +1.5 % at config 2)
+#endif
+constexpr int kAUnr = MLG_CG_AUNR;
 struct RowRing {
   double v[kD][MLG_CG_RINGA][32];  // [slot][p, r, x, p of a deferred x update][lane]
 };
@@ -748,6 +752,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
   using F = std::false_type;
   step(k.ly0 - 1, F{}, F{});
   step(k.ly0, T{}, F{});
+#pragma unroll kAUnr
   for (int n = k.ly0 + 1; n < k.ly1; ++n) step(n, T{}, T{});
   step(k.ly1, F{}, T{});
   cp_async_wait<0>();
