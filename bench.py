@@ -307,6 +307,8 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
     ka_rows = sum(t.spmv_rows for t in tims)
     ka_chk = sum(t.spmv_check_rows for t in tims)
     ka_all = sum(t.spmv_launches_all for t in tims)
+    # one cooperative launch per solve vs one launch per CG iteration
+    persistent = ka_all < 0.5 * sum(t.local_iterations_max for t in tims)
     if ka_n:
         bpr, bpc = cg_bytes_per_row(tims[-1].spmv_uniform_stencil)
         ka_bytes = ka_rows * bpr + ka_chk * bpc
@@ -315,7 +317,7 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
         tr = ncu_traffic(workload)
         out["roofline"] = {
             "kernel": ("k_cg_persist (local solves: the fused PCG sweep, all iterations in one "
-                       "cooperative launch, cp.async row ring)" if workload == "c2" else
+                       "cooperative launch, cp.async row ring)" if persistent else
                        "k_cg_iter (local solves: fused PCG sweep, one launch per iteration)"),
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,

@@ -1426,14 +1426,20 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
     const char* e = std::getenv("MLG_CG_ASYNC");  // A/B hook: 0 / 1
     return e ? std::atoi(e) : -1;
   }();
-  use_async = lev.uniform != 0 &&
-              (async_env >= 0 ? async_env != 0 : all_rows * 48 > (128LL << 20));
-  // L2-resident constant-coefficient batches: one persistent launch per solve.
+  const bool streaming_async =
+      lev.uniform != 0 && (async_env >= 0 ? async_env != 0 : all_rows * 48 > (128LL << 20));
+  // Constant-coefficient batches whose tiles fit the resident CTAs: one
+  // persistent launch per solve (measured: L2-resident config 2 and the
+  // streaming config 3 both gain; config 5's batches do not fit and fall back
+  // to one launch per iteration below).  MLG_CG_ASYNC=1 forces the latter.
   static const int persist_env = [] {
     const char* e = std::getenv("MLG_CG_PERSIST");  // A/B hook: 0 / 1
     return e ? std::atoi(e) : 1;
   }();
-  use_persist = lev.uniform != 0 && !use_async && persist_env != 0;
+  use_persist = lev.uniform != 0 && persist_env != 0 && async_env != 1;
+  use_async = use_persist ? false : streaming_async;
+  int s_krows = 0;
+  for (int pass = 0; pass < 2; ++pass) {
   // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
   // must still offer >= ~8k warps (148 SMs x ~56 resident) to hide latency.
   static const long long target_tasks = [] {
@@ -1529,9 +1535,16 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
       while (kr > 4 && tiles_for(kr) < static_cast<long long>(tpc) * resident) --kr;
       krows = kr;
     }
-    if (use_persist && (tiles_for(krows) + resident - 1) / resident > kPersistTiles)
-      use_persist = false;  // too many tiles per CTA: multi-launch path
+    if (use_persist && (tiles_for(krows) + resident - 1) / resident > kPersistTiles) {
+      use_persist = false;  // too many tiles per CTA: multi-launch path, retiled
+      use_async = streaming_async;
+      continue;
+    }
   }
+  s_krows = krows;
+  break;
+  }
+  const int krows = s_krows;
   for (CgSys& s : systems) {
     s.nrows = s.w * s.h;
     s.krows = krows;
