@@ -5,7 +5,8 @@ The path is chosen per batch at run time (persistent cooperative kernel for
 L2-resident batches, multi-launch register pipeline, cp.async row pipeline for
 HBM-streaming batches, general per-row stencil, generic uniform stencil); the
 selection hooks are read once per process, so each variant runs in its own
-subprocess."""
+subprocess.  The L-shaped cases (config 3's domain, golden vectors of the
+restatement) cover the hole exclusion of every path."""
 import json
 import os
 import subprocess
@@ -35,8 +36,9 @@ sys.path.insert(0, sys.argv[1])
 import paper_1401_4969_b200 as mlg
 out = {}
 for name, c in json.loads(sys.argv[2]).items():
+    hole = mlg.DomainRect(*c["hole"]) if "hole" in c else None
     cfg = mlg.RunConfig(domain=mlg.DomainRect(*c["domain"]), H=c["H"], delta=c["delta"], m=c["m"],
-                        n_levels=c["n_levels"], nev=c["nev"])
+                        n_levels=c["n_levels"], nev=c["nev"], hole=hole)
     with mlg.Hierarchy(cfg) as hy:
         lam, pairs, matched, times = mlg.multilevel_correction(hy)
     out[name] = [list(map(float, l)) for l in lam]
@@ -44,8 +46,24 @@ print(json.dumps(out))
 """
 
 
+LSHAPE = ["H8_L3_m16_nev3", "H8_L4_m16_nev1"]
+
+
+def _lshape_config(name):
+    c = GOLDEN["lshape"][name]["config"]
+    return {"domain": [-1.0, 1.0, -1.0, 1.0], "hole": [0.0, 1.0, -1.0, 0.0], "H": c["H"],
+            "delta": c["H"], "m": c["m"], "n_levels": c["n_levels"], "nev": c["nev"]}
+
+
+def _golden(name):
+    if name.startswith("lshape:"):
+        return GOLDEN["lshape"][name[7:]]["lambdas"]
+    return GOLDEN["multilevel"][name]["lambdas"]
+
+
 def _run(env_extra):
     cfgs = {n: GOLDEN["multilevel"][n]["config"] for n in CASES if n in GOLDEN["multilevel"]}
+    cfgs.update({"lshape:" + n: _lshape_config(n) for n in LSHAPE})
     env = dict(os.environ, **env_extra)
     r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), json.dumps(cfgs)],
                        capture_output=True, text=True, env=env, timeout=600)
@@ -57,7 +75,7 @@ def _run(env_extra):
 def test_cg_path_matches_golden_eigenvalues(variant):
     got = _run(VARIANTS[variant])
     for name, lams in got.items():
-        ref = GOLDEN["multilevel"][name]["lambdas"]
+        ref = _golden(name)
         assert len(lams) == len(ref), name
         for k, (a, b) in enumerate(zip(lams, ref)):
             a, b = np.asarray(a), np.asarray(b)
