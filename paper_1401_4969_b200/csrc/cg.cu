@@ -627,6 +627,9 @@ static_assert((kD & (kD - 1)) == 0 && kD >= 4, "ring depth must be a power of tw
 #define MLG_CG_AUNR 2  // unroll of the interior row loop (register rotation by renaming; A/B: 1 -> 2 +1.5 % at config 2)
 #endif
 constexpr int kAUnr = MLG_CG_AUNR;
+#ifndef MLG_CG_OFF32
+#define MLG_CG_OFF32 1
+#endif
 struct RowRing {
   double v[kD][MLG_CG_RINGA][32];  // [slot][p, r, x, p of a deferred x update][lane]
 };
@@ -678,15 +681,22 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
   const Flags f = make_flags(S, A, k);          // EDGE only
   const RowMask rm = make_rowmask(S, A, k, f);  // EDGE only
   const bool own = lane >= 2 && lane < 2 + kCgCols && (!EDGE || f.cin);
-  const long long w = S.pitch;
-  const long long base = cg_index(S, 0, k.col);
+#if MLG_CG_OFF32
+  // 32-bit element offsets (pools hold < 2^32 elements, checked at setup): one
+  // IMAD.WIDE.U32 per address instead of 64-bit offset arithmetic per array
+  using Off = unsigned;
+#else
+  using Off = long long;
+#endif
+  const Off w = static_cast<Off>(S.pitch);
+  const Off base = static_cast<Off>(cg_index(S, 0, k.col));
   const Stencil u = A.ust;
   const double dv = LAP ? 0.25 : A.udinv;
   const int last = k.ly1 + 1;  // last old row needed (the zero frame makes it readable)
   auto issue = [&](int row) {  // one commit group per row, empty past the end
     if (row <= last) {
       const int s = row & (kD - 1);
-      const long long o = base + row * w;
+      const Off o = base + static_cast<Off>(row) * w;
       cp_async8(&ring.v[s][0][lane], Pc + o);
       cp_async8(&ring.v[s][1][lane], Rc + o);
       if (XM != 0) cp_async8_cg(&ring.v[s][2][lane], X + o);
@@ -725,7 +735,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     if constexpr (EDGE) tp = b_in ? tp : 0.0;
     if constexpr (decltype(store)::value) {
       if (own && b_in) {
-        const long long o = base + n * w;
+        const Off o = base + static_cast<Off>(n) * w;
         if (XM != 0) X[o] = xn;
         Rn[o] = rn;
         Pn[o] = tp;
@@ -1596,6 +1606,8 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
     total_tiles += s.ntiles;
   }
   total_rows = cursor + static_cast<long long>(kCgPadRows) * max_pitch + 64;
+  if (total_rows >= (1LL << 32))  // sweep_async indexes the pool with 32-bit offsets
+    throw std::runtime_error("cg batch: pooled vectors exceed 2^32 elements");
   tmap_h = tmap;
   task_map.ensure(std::max<std::size_t>(tmap.size(), 1));
   if (!tmap.empty()) task_map.upload(tmap.data(), tmap.size(), c.stream);
