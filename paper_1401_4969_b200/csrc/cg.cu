@@ -582,6 +582,135 @@ __device__ __forceinline__ void sweep_reg(const CgSys& S, const SweepArgs& A, co
   }
 }
 
+// ---- general-stencil interior fast path -------------------------------------
+// Variable-coefficient levels, tasks whose 32 columns and rows ly0-2 .. ly1+1
+// lie inside the system (task_interior: every neighbour present, no flags).
+// Same terms, order and rounding as the flagged general sweep (product<false>,
+// xsub/xmul updates), but with a kWG-row register window of the old rows
+// (p, r, x, stencil, D^-1), i.e. kWG - 2 rows in flight instead of one.
+#ifndef MLG_CG_WG
+#define MLG_CG_WG 3  // A/B at config 4: 3 rows +4.5 %, 4 rows +2 % (spills), 5 rows -4 %
+#endif
+constexpr int kWG = MLG_CG_WG;
+#ifndef MLG_CG_GENFAST
+#define MLG_CG_GENFAST 1  // 0: every general-stencil task takes the flagged sweep
+#endif
+
+// product<false> with every presence flag set (sparse.cpp:69-76 column order)
+__device__ __forceinline__ double product_gen(double sv, double s_n, double s_ne, double cv,
+                                              const Stencil& c, double nv) {
+  const double wa = __shfl_up_sync(kFull, c.e, 1);
+  const double swa = __shfl_up_sync(kFull, s_ne, 1);
+  const double wv = __shfl_up_sync(kFull, cv, 1);
+  const double ev = __shfl_down_sync(kFull, cv, 1);
+  const double swv = __shfl_up_sync(kFull, sv, 1);
+  const double nev = __shfl_down_sync(kFull, nv, 1);
+  double a = 0.0;
+  a = xadd(a, xmul(swa, swv));
+  a = xadd(a, xmul(s_n, sv));
+  a = xadd(a, xmul(wa, wv));
+  a = xadd(a, xmul(c.c, cv));
+  a = xadd(a, xmul(c.e, ev));
+  a = xadd(a, xmul(c.n, nv));
+  a = xadd(a, xmul(c.ne, nev));
+  return a;
+}
+
+template <bool RST>
+__device__ __forceinline__ void sweep_gen(const CgSys& S, const SweepArgs& A, const Task& k,
+                                          double al, double be, double* __restrict__ X,
+                                          const double* __restrict__ Rc,
+                                          double* __restrict__ Rn,
+                                          const double* __restrict__ Pc,
+                                          double* __restrict__ Pn, double (&acc)[kCgDots]) {
+  const int lane = threadIdx.x & 31;
+  const bool own = lane >= 2 && lane < 2 + kCgCols;
+  const unsigned w = static_cast<unsigned>(S.pitch);
+  const unsigned gw = static_cast<unsigned>(A.nxp1);
+  const unsigned v0 = static_cast<unsigned>(cg_index(S, 0, k.col));
+  const unsigned g0 = static_cast<unsigned>(S.y0) * gw + static_cast<unsigned>(S.x0 + k.col);
+  const int last = k.ly1 + 1;  // last old row needed (inside the system)
+  double P[kWG], Rr[kWG], Xr[kWG], D[kWG];
+  Stencil St[kWG];
+  auto load = [&](int j, int row) {  // rows past `last` re-read `last` (unused)
+    const unsigned rr = static_cast<unsigned>(min(row, last));
+    const unsigned v = v0 + rr * w, g = g0 + rr * gw;
+    P[j] = Pc[v];
+    Rr[j] = Rc[v];
+    Xr[j] = X[v];
+    St[j] = A.st[g];
+    D[j] = A.dinv[g];
+  };
+#pragma unroll
+  for (int j = 0; j < kWG; ++j) load(j, k.ly0 - 2 + j);
+  int next = k.ly0 - 2 + kWG;  // next row to request
+  // new p at rows n-2 (s) and n-1 (m); z, D^-1 and stencil of row n-1
+  double sp = 0.0, mp = 0.0, mz = 0.0, mdv = 0.0;
+  double s_n = 0.0, s_ne = 0.0;
+  Stencil mst{0.0, 0.0, 0.0, 0.0};
+  auto step = [&](auto J, auto store, auto stage2, int n) {
+    constexpr int j0 = decltype(J)::value % kWG, j1 = (j0 + 1) % kWG, j2 = (j0 + 2) % kWG;
+    double rn = Rr[j1], xn = Xr[j1];
+    if constexpr (!RST) {
+      const double qo = product_gen(P[j0], St[j0].n, St[j0].ne, P[j1], St[j1], P[j2]);
+      rn = xsub(Rr[j1], xmul(al, qo));
+      xn = xadd(Xr[j1], xmul(al, P[j1]));
+    }
+    const double dv = D[j1];
+    const double tz = xmul(dv, rn);
+    const double tp = RST ? tz : xadd(tz, xmul(be, P[j1]));
+    const Stencil tst = St[j1];
+    load(j0, next);  // slot of row n-1 is free
+    ++next;
+    if constexpr (decltype(store)::value) {
+      if (own) {
+        const unsigned v = v0 + static_cast<unsigned>(n) * w;
+        X[v] = xn;
+        Rn[v] = rn;
+        Pn[v] = tp;
+        acc[0] += rn * rn;
+        acc[1] += rn * tz;
+      }
+    }
+    if constexpr (decltype(stage2)::value) {  // q = A p_new at row n-1
+      const double q = product_gen(sp, s_n, s_ne, mp, mst, tp);
+      if (own) {
+        acc[2] += mp * q;
+        acc[3] += q * mz;
+        acc[4] += q * xmul(mdv, q);
+      }
+    }
+    sp = mp;
+    s_n = mst.n;
+    s_ne = mst.ne;
+    mp = tp;
+    mz = tz;
+    mdv = dv;
+    mst = tst;
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  step(std::integral_constant<int, 0>{}, F{}, F{}, k.ly0 - 1);  // stage 1 only
+  step(std::integral_constant<int, 1>{}, T{}, F{}, k.ly0);
+  int n = k.ly0 + 1;  // slot phase 2
+  using Seq = std::make_integer_sequence<int, kWG>;
+#pragma unroll 1
+  for (; n + kWG - 1 < k.ly1; n += kWG)
+    static_for(Seq{}, [&](auto i) {
+      constexpr int ii = decltype(i)::value;
+      step(std::integral_constant<int, (2 + ii) % kWG>{}, T{}, T{}, n + ii);
+    });
+  const int rem = k.ly1 - n;  // 0..kWG-1 rows left, then row ly1 (stage 2 only)
+  static_for(std::make_integer_sequence<int, kWG - 1>{}, [&](auto i) {
+    constexpr int ii = decltype(i)::value;
+    if (ii < rem) step(std::integral_constant<int, (2 + ii) % kWG>{}, T{}, T{}, n + ii);
+  });
+  static_for(Seq{}, [&](auto r) {
+    constexpr int rr = decltype(r)::value;
+    if (rr == rem) step(std::integral_constant<int, (2 + rr) % kWG>{}, F{}, T{}, k.ly1);
+  });
+}
+
 template <bool RST, bool CG, bool LAP>
 __device__ __forceinline__ void sweep_edge(const CgSys& S, const SweepArgs& A, const Task& k,
                                            double al, double be, double* __restrict__ X,
@@ -771,6 +900,7 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
     for (int q = 0; q < kCgDots; ++q) acc[q] = 0.0;
   }
 }
+
 
 
 enum Phase { kPhaseInit = 0, kPhaseIter = 1 };
@@ -1066,6 +1196,12 @@ __device__ __forceinline__ void cg_tile(const CgSys& S, const CgTile tl, int mod
       sweep_edge<true, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
     else
       sweep_edge<false, PERSIST, LAP>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc, xch);
+  } else if (!UNI && MLG_CG_GENFAST && k.valid && mode == kModeNormal &&
+             task_interior(S, A, k)) {
+    if (rst)
+      sweep_gen<true>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
+    else
+      sweep_gen<false>(S, A, k, al, be, X, Rc, Rn, Pc, Pn, acc);
   } else if (!UNI && k.valid && mode == kModeNormal) {
     ORow a, b, c, d;  // old iterate at rows n-1, n, n+1 (and n+2 in flight)
     NRow s, m;        // new p at rows n-2, n-1
