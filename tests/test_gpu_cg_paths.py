@@ -26,6 +26,9 @@ VARIANTS = {
     "multi_launch_registers": {"MLG_CG_PERSIST": "0"},
     "cp_async_pipeline": {"MLG_CG_ASYNC": "1"},
     "general_stencil": {"MLG_GENERAL_STENCIL": "1"},
+    "general_stencil_multi_launch": {"MLG_GENERAL_STENCIL": "1", "MLG_CG_PERSIST": "0"},
+    "general_stencil_flagged_only": {"MLG_GENERAL_STENCIL": "1", "MLG_CG_MINROWS": "4",
+                                     "MLG_CG_MAXROWS": "8"},
     "generic_uniform_stencil": {"MLG_CG_NOLAP": "1"},
     "short_tasks": {"MLG_CG_MINROWS": "4", "MLG_CG_MAXROWS": "8"},
 }
