@@ -1586,109 +1586,109 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   use_async = use_persist ? false : streaming_async;
   int s_krows = 0;
   for (int pass = 0; pass < 2; ++pass) {
-  // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
-  // must still offer >= ~8k warps (148 SMs x ~56 resident) to hide latency.
-  static const long long target_tasks = [] {
-    const char* e = std::getenv("MLG_CG_TASKS");  // tuning hook
-    return e ? std::atoll(e) : 8192LL;
-  }();
-  static const int min_rows = [] {
-    const char* e = std::getenv("MLG_CG_MINROWS");  // tuning hook
-    return e ? std::atoi(e) : 16;
-  }();
-  static const int max_rows_async = [] {
-    const char* e = std::getenv("MLG_CG_MAXROWS");  // tuning hook
-    return e ? std::atoi(e) : kCgRowsAsync;
-  }();
-  const int max_rows = use_async ? max_rows_async : kCgRows;
-  int krows = static_cast<int>(std::min<long long>(
-      max_rows, std::max<long long>(min_rows, all_rows / (kCgCols * target_tasks))));
-  // Wave quantisation: every tile costs ~(krows + c0) row steps and the grid
-  // runs in waves of `resident` tiles, so pick the row count that minimises
-  // waves x (krows + c0) from half the first choice up to the cap.
-  {
-    const int resident = use_persist ? resident_persist() : resident_tiles(use_async);
-    // Strip systems drop the tasks whose output cells lie inside one G_j
-    // (setup below); count them per block in closed form.
-    auto inside_tasks = [&](const CgSys& s, int kr) {
-      if (!mask_) return 0LL;
-      const StripGeom& g = lev.strip_geom;
-      long long n = 0;
-      for (int bx = 0; bx < g.side; ++bx)
-        for (int by = 0; by < g.side; ++by) {
-          const int gx0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
-          const int gx1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
-          const int gy0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
-          const int gy1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
-          long long cs = 0, cr = 0;
-          for (int c = 0; c * kCgCols < s.w; ++c) {
-            const int ca = s.x0 + c * kCgCols, cb = s.x0 + std::min(c * kCgCols + kCgCols, s.w) - 1;
-            cs += ca >= gx0 && cb <= gx1;
+    // Rows per warp task: long sweeps amortise the 2-row halo, but the batch
+    // must still offer >= ~8k warps (148 SMs x ~56 resident) to hide latency.
+    static const long long target_tasks = [] {
+      const char* e = std::getenv("MLG_CG_TASKS");  // tuning hook
+      return e ? std::atoll(e) : 8192LL;
+    }();
+    static const int min_rows = [] {
+      const char* e = std::getenv("MLG_CG_MINROWS");  // tuning hook
+      return e ? std::atoi(e) : 16;
+    }();
+    static const int max_rows_async = [] {
+      const char* e = std::getenv("MLG_CG_MAXROWS");  // tuning hook
+      return e ? std::atoi(e) : kCgRowsAsync;
+    }();
+    const int max_rows = use_async ? max_rows_async : kCgRows;
+    int krows = static_cast<int>(std::min<long long>(
+        max_rows, std::max<long long>(min_rows, all_rows / (kCgCols * target_tasks))));
+    // Wave quantisation: every tile costs ~(krows + c0) row steps and the grid
+    // runs in waves of `resident` tiles, so pick the row count that minimises
+    // waves x (krows + c0) from half the first choice up to the cap.
+    {
+      const int resident = use_persist ? resident_persist() : resident_tiles(use_async);
+      // Strip systems drop the tasks whose output cells lie inside one G_j
+      // (setup below); count them per block in closed form.
+      auto inside_tasks = [&](const CgSys& s, int kr) {
+        if (!mask_) return 0LL;
+        const StripGeom& g = lev.strip_geom;
+        long long n = 0;
+        for (int bx = 0; bx < g.side; ++bx)
+          for (int by = 0; by < g.side; ++by) {
+            const int gx0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+            const int gx1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+            const int gy0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+            const int gy1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+            long long cs = 0, cr = 0;
+            for (int c = 0; c * kCgCols < s.w; ++c) {
+              const int ca = s.x0 + c * kCgCols, cb = s.x0 + std::min(c * kCgCols + kCgCols, s.w) - 1;
+              cs += ca >= gx0 && cb <= gx1;
+            }
+            for (int r = 0; r * kr < s.h; ++r) {
+              const int ra = s.y0 + r * kr, rb = s.y0 + std::min(r * kr + kr, s.h) - 1;
+              cr += ra >= gy0 && rb <= gy1;
+            }
+            n += cs * cr;
           }
-          for (int r = 0; r * kr < s.h; ++r) {
-            const int ra = s.y0 + r * kr, rb = s.y0 + std::min(r * kr + kr, s.h) - 1;
-            cr += ra >= gy0 && rb <= gy1;
-          }
-          n += cs * cr;
+        return n;
+      };
+      auto tiles_for = [&](int kr) {
+        // strip systems (mask) all share one window: count its dropped tasks once.
+        // (Persistent batches keep the uncompacted count: there the per-tile
+        // fixed cost favours fewer, taller tiles -- measured at config 2.)
+        const long long drop =
+            mask_ && !use_persist && !systems.empty() ? inside_tasks(systems[0], kr) : 0;
+        long long t = 0;
+        for (const CgSys& s : systems) {
+          const long long ns = std::max(1, (s.w + kCgCols - 1) / kCgCols);
+          const long long nb = std::max(1, (s.h + kr - 1) / kr);
+          const long long nt = std::max(1LL, ns * nb - drop);
+          t += (nt + kCgWarps - 1) / kCgWarps;
         }
-      return n;
-    };
-    auto tiles_for = [&](int kr) {
-      // strip systems (mask) all share one window: count its dropped tasks once.
-      // (Persistent batches keep the uncompacted count: there the per-tile
-      // fixed cost favours fewer, taller tiles -- measured at config 2.)
-      const long long drop =
-          mask_ && !use_persist && !systems.empty() ? inside_tasks(systems[0], kr) : 0;
-      long long t = 0;
-      for (const CgSys& s : systems) {
-        const long long ns = std::max(1, (s.w + kCgCols - 1) / kCgCols);
-        const long long nb = std::max(1, (s.h + kr - 1) / kr);
-        const long long nt = std::max(1LL, ns * nb - drop);
-        t += (nt + kCgWarps - 1) / kCgWarps;
+        return t;
+      };
+      // (c0: a task's prologue/epilogue in row steps)
+      static const int c0 = [] {
+        const char* e = std::getenv("MLG_CG_C0");  // tuning hook
+        return e ? std::atoi(e) : 6;
+      }();
+      double best = 1e300;
+      int best_k = krows;
+      for (int kr = std::max(4, krows / 2); kr <= max_rows; ++kr) {
+        const long long waves = (tiles_for(kr) + resident - 1) / resident;
+        const double cost = static_cast<double>(waves) * (kr + c0);
+        if (cost < best - 1e-9) {
+          best = cost;
+          best_k = kr;
+        }
       }
-      return t;
-    };
-    // (c0: a task's prologue/epilogue in row steps)
-    static const int c0 = [] {
-      const char* e = std::getenv("MLG_CG_C0");  // tuning hook
-      return e ? std::atoi(e) : 6;
-    }();
-    double best = 1e300;
-    int best_k = krows;
-    for (int kr = std::max(4, krows / 2); kr <= max_rows; ++kr) {
-      const long long waves = (tiles_for(kr) + resident - 1) / resident;
-      const double cost = static_cast<double>(waves) * (kr + c0);
-      if (cost < best - 1e-9) {
-        best = cost;
-        best_k = kr;
+      krows = best_k;
+      static const int strip_rows = [] {
+        const char* e = std::getenv("MLG_CG_STRIP_ROWS");  // tuning hook (strip batches)
+        return e ? std::atoi(e) : 0;
+      }();
+      if (mask_ && strip_rows > 0) krows = strip_rows;
+      // Persistent batches: one tile per CTA leaves the slow (edge) tiles on the
+      // critical path; aim for ~`tpc` tiles per CTA so the LPT assignment can
+      // pair them with cheap ones.
+      static const int tpc = [] {
+        const char* e = std::getenv("MLG_CG_PTPC");  // tuning hook
+        return e ? std::atoi(e) : 1;
+      }();
+      if (use_persist && tpc > 1) {
+        int kr = krows;
+        while (kr > 4 && tiles_for(kr) < static_cast<long long>(tpc) * resident) --kr;
+        krows = kr;
+      }
+      if (use_persist && (tiles_for(krows) + resident - 1) / resident > kPersistTiles) {
+        use_persist = false;  // too many tiles per CTA: multi-launch path, retiled
+        use_async = streaming_async;
+        continue;
       }
     }
-    krows = best_k;
-    static const int strip_rows = [] {
-      const char* e = std::getenv("MLG_CG_STRIP_ROWS");  // tuning hook (strip batches)
-      return e ? std::atoi(e) : 0;
-    }();
-    if (mask_ && strip_rows > 0) krows = strip_rows;
-    // Persistent batches: one tile per CTA leaves the slow (edge) tiles on the
-    // critical path; aim for ~`tpc` tiles per CTA so the LPT assignment can
-    // pair them with cheap ones.
-    static const int tpc = [] {
-      const char* e = std::getenv("MLG_CG_PTPC");  // tuning hook
-      return e ? std::atoi(e) : 1;
-    }();
-    if (use_persist && tpc > 1) {
-      int kr = krows;
-      while (kr > 4 && tiles_for(kr) < static_cast<long long>(tpc) * resident) --kr;
-      krows = kr;
-    }
-    if (use_persist && (tiles_for(krows) + resident - 1) / resident > kPersistTiles) {
-      use_persist = false;  // too many tiles per CTA: multi-launch path, retiled
-      use_async = streaming_async;
-      continue;
-    }
-  }
-  s_krows = krows;
-  break;
+    s_krows = krows;
+    break;
   }
   const int krows = s_krows;
   for (CgSys& s : systems) {
