@@ -1311,7 +1311,10 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
 // cooperative launch).  Same tile bodies, same reductions (the last tile of a
 // system advances its scalars before arriving at the barrier), so the iterates
 // are identical to the multi-launch path.
-constexpr int kPersistTiles = 8;
+#ifndef MLG_CG_PERSIST_TILES
+#define MLG_CG_PERSIST_TILES 8  // A/B: 16 takes config 5's strip batches persistent: strip +15 % time
+#endif
+constexpr int kPersistTiles = MLG_CG_PERSIST_TILES;
 
 struct GridSync {
   unsigned* count;    // arrivals since the launch began (zeroed before each launch)
