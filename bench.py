@@ -2,17 +2,22 @@
 """Benchmark of the B200 correction step (BASELINE.json metric: fine-grid DOF/s
 per correction step; local-solve SpMV HBM GB/s vs B200 peak).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4|c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c2|c3|c4]
     python bench.py --impl reference ...        # the reference's CPU path (oracle/_ref)
 
+Headline workload: BASELINE config 5 (its reference-valid substitute: 4096^2
+cells, m=64, nev=4), the largest single-GPU configuration and the north star.
 A "step" is one correction step L-1 -> L (one_correction_step,
-corrector.cpp:336-412) of the named workload; its input eigenpairs come from
-the multilevel pipeline itself (level-1 dense solve + correction steps).
-`value` times the step with coefficient arrays resident in HBM (device C-ABI
-entry point, CUDA events on the library stream); `e2e` times the same step
-through the host C-ABI call with pinned host buffers (H2D/D2H inside).  Under
-torchrun every rank runs an independent replica on its GPU ("replicas only",
-DESIGN.md): value = all ranks' DOF / max-over-ranks time.
+corrector.cpp:336-412); its input eigenpairs come from the multilevel pipeline
+itself (level-1 dense solve + correction steps).  `value` times the step with
+coefficient arrays resident in HBM (device C-ABI entry point, CUDA events on
+the library stream); `e2e` times the same step through the host C-ABI call
+with pinned host buffers (H2D/D2H inside).  `rooflines` holds one entry per
+kernel family of the step (local-solve CG, strip-solve CG, operator assembly);
+`roofline` is the one with the largest share of the step.  Config 2, 3 and 4
+are measured in the same run under `config*_workload` (--no-extras skips them).
+Under torchrun every rank runs an independent replica on its GPU ("replicas
+only"): value = all ranks' DOF / max-over-ranks time.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -31,15 +36,16 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "fine-grid DOF/s per correction step; local-solve SpMV HBM GB/s vs B200 peak"
+UNIT_SQUARE = (0.0, 1.0, 0.0, 1.0)
 WORKLOADS = {
+    "c5": dict(desc="config 5 (reference-valid substitute m=64): unit square, Laplace P1 FP64, "
+                    "32x32 coarse squares, 7 levels (4096^2 cells, 16.77M interior dofs), 8x8 "
+                    "overlapping subdomains, delta=1/32, nev=4; step level 6 -> 7",
+               H=1 / 32, delta=1 / 32, m=64, n_levels=7, nev=4),
     "c2": dict(desc="config 2 (reference-valid substitute m=16): unit square, Laplace P1 FP64, "
                     "16x16 coarse squares, 6 levels (1024^2 cells), 4x4 overlapping subdomains, "
                     "delta=1/16, nev=1; step level 5 -> 6",
                H=1 / 16, delta=1 / 16, m=16, n_levels=6, nev=1),
-    "c5": dict(desc="config 5 (reference-valid substitute m=64): unit square, Laplace P1 FP64, "
-                    "32x32 coarse squares, 7 levels (4096^2 cells), 8x8 overlapping subdomains, "
-                    "delta=1/32, nev=4; step level 6 -> 7",
-               H=1 / 32, delta=1 / 32, m=64, n_levels=7, nev=4),
     "c3": dict(desc="config 3 (B200 extension, no reference code path): L-shaped domain "
                     "(-1,1)^2 minus [0,1]x[-1,0], Laplace P1 FP64, 3 unit squares of 16x16 "
                     "cells (768 coarse triangles), 6 levels (3.1M fine triangles), 48 "
@@ -54,7 +60,13 @@ WORKLOADS = {
                     "delta=1/16, nev=1; step level 6 -> 7 (no reference code path)",
                H=1 / 16, delta=1 / 16, m=16, n_levels=7, nev=1, example="reaction", seed=0),
 }
+DEFAULT_WORKLOAD = "c5"
 FALLBACK_HBM = 6650.0
+# k_assemble: per dof it writes the A and M stencils (2 x 32 B) and D^-1 (8 B) and
+# reads its cell's geometric triangle map (2 x 4 B per cell, shared by the dofs of
+# the cell): 80 B per dof.
+ASSEMBLE_BYTES_PER_DOF = 80
+KERNEL_NAMES = {0: "k_cg_iter", 1: "k_cg_persist", 2: "k_cg_resident"}
 
 
 def cg_bytes_per_row(uniform=0):
@@ -120,23 +132,31 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def measured_peak():
-    p = ROOT / "MEASURED_PEAKS.json"
+def measured_peak(bound="hbm"):
+    """(peak GB/s, source) for a roofline bound: HBM from the driver's
+    MEASURED_PEAKS.json; on-chip bounds (L2, shared memory) from our own
+    microbenchmark, committed under profiles/onchip_peaks.json."""
+    if bound == "hbm":
+        p = ROOT / "MEASURED_PEAKS.json"
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
     try:
-        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        d = json.loads((ROOT / "profiles" / "onchip_peaks.json").read_text())
+        return float(d[f"{bound}_gbs"]), f"measured (profiles/onchip_peaks.json: {d['_source']})"
     except Exception:
-        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+        return None, f"no measured {bound} peak committed"
 
 
-def ncu_traffic(workload):
-    """Per-row DRAM traffic of k_cg_iter from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "ka_traffic.json"
+def ncu_traffic(key):
+    """DRAM bytes per algorithmic row-iteration of a kernel from the committed
+    ncu --set full summaries (profiles/ka_traffic.json, keyed workload:role)."""
     try:
-        d = json.loads(p.read_text())
-        e = d.get(workload)
-        return e["dram_bytes_per_launch"] / e["rows_per_launch"]
+        d = json.loads((ROOT / "profiles" / "ka_traffic.json").read_text())
+        return float(d[key]["dram_bytes_per_row"]), d[key].get("source", "")
     except Exception:
-        return None
+        return None, None
 
 
 def dist_setup(args):
@@ -167,21 +187,28 @@ def allreduce_max(x, ws, device=None):
 
 
 # ------------------------------------------------------------ reference arm --
-def reference_step_run(wl, steps, warmup, workers):
-    """The reference's own implementation (oracle/_ref = unmodified reference
-    sources) on host cores: setup to level L-1, then one_correction_step L-1->L."""
+def _ref_setup(wl, workers):
+    """The reference (oracle/_ref = unmodified reference sources) brought to the
+    step's input: multilevel_correction up to L-1, then a hierarchy with level L
+    and its region systems (Hierarchy::extend_to, build_region_systems)."""
     from oracle import ref
     L = wl["n_levels"]
     t0 = time.time()
-    setup = ref.RefHierarchy(domain=(0.0, 1.0, 0.0, 1.0), H=wl["H"], delta=wl["delta"], m=wl["m"],
+    setup = ref.RefHierarchy(domain=UNIT_SQUARE, H=wl["H"], delta=wl["delta"], m=wl["m"],
                              n_levels=L - 1, nev=wl["nev"], workers=workers)
     lam, co, _, _ = setup.multilevel(L - 1, wl["nev"])
     setup.close()
-    h = ref.RefHierarchy(domain=(0.0, 1.0, 0.0, 1.0), H=wl["H"], delta=wl["delta"], m=wl["m"],
+    h = ref.RefHierarchy(domain=UNIT_SQUARE, H=wl["H"], delta=wl["delta"], m=wl["m"],
                          n_levels=L, nev=wl["nev"], workers=workers)
     build = h.extend_to(L)
     regions = h.build_region_systems(L)
-    setup_s = time.time() - t0
+    return h, lam, co, dict(build_s=build, regions_s=regions, setup_s=time.time() - t0)
+
+
+def reference_full_steps(wl, steps, warmup, workers):
+    """Whole one_correction_step calls L-1 -> L of the reference (small workloads)."""
+    h, lam, co, info = _ref_setup(wl, workers)
+    L = wl["n_levels"]
     times, splits = [], []
     for k in range(warmup + steps):
         t = time.perf_counter()
@@ -192,8 +219,67 @@ def reference_step_run(wl, steps, warmup, workers):
             splits.append(t3)
     n = h.sizes(L)["n_int"]
     h.close()
-    return dict(n_int=n, times=times, splits=splits, build_s=build, regions_s=regions,
-                setup_s=setup_s, lam=list(lo))
+    return dict(n_int=n, times=times, splits=splits, lam=list(lo), **info)
+
+
+def reference_sampled_steps(wl, steps, workers, strip_maxit=30):
+    """Bounded sample of the reference's correction step L-1 -> L for workloads
+    whose full step runs for tens of minutes on the host (config 5: ~30 min on
+    8 cores).  The step is one_correction_step (corrector.cpp:336-412): nev*m
+    local_bvp_solve tasks on the worker pool (:364-370), nev strip solves
+    (interface_solve, one task per eigenvector, :372-376) and the serial
+    augmented eigensolve (:378-381).  Each sampled step times, with the
+    reference's own code:
+      * one wave of `workers` local_bvp_solve tasks run concurrently (the
+        worker pool's steady state), successive steps taking successive tasks;
+        local estimate = mean task time x nev*m / workers;
+      * cg_solve on the strip system capped at strip_maxit iterations
+        (ref_strip_cg_sample); strip estimate = time per iteration x the
+        reference's strip iteration count (tests/golden/golden_l7.json) -- the
+        nev strips run concurrently, so the step waits for one of them;
+      * the augmented eigensolve once (setup) on the prolonged input.
+    The sum is the estimated step time; DESIGN.md §5 checks the estimate
+    against a full reference step measured in the build container."""
+    import numpy as np
+    h, lam, co, info = _ref_setup(wl, workers)
+    L, nev, m = wl["n_levels"], wl["nev"], wl["m"]
+    s_prev, s = h.sizes(L - 1), h.sizes(L)
+    lam_in = lam[-1]
+    u = []
+    for i in range(nev):
+        full = np.zeros(s_prev["ndofs"])
+        full.reshape(s_prev["ny"] + 1, s_prev["nx"] + 1)[1:-1, 1:-1] = co[i].reshape(
+            s_prev["ny"] - 1, s_prev["nx"] - 1)
+        u.append(h.prolong(full, L - 1, L))
+    t = time.perf_counter()
+    h.augmented_eigensolve(L, np.stack(u), nev)  # glued vectors are full-space
+    aug_s = time.perf_counter() - t
+    golden = json.loads((ROOT / "tests" / "golden" / "golden_l7.json").read_text())
+    strip_iters = int(max(golden["reference_strip_iterations_L7"]))
+    tasks = [(i, j) for i in range(nev) for j in range(m)]
+    out = []
+    for k in range(steps):
+        wave = [tasks[(k * workers + q) % len(tasks)] for q in range(workers)]
+        res = [None] * len(wave)
+
+        def run(q):
+            i, j = wave[q]
+            res[q] = h.local_bvp_time(L, j, lam_in[i], u[i], 1e-10)
+        th = [threading.Thread(target=run, args=(q,)) for q in range(len(wave))]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        task_s = [r[0] for r in res]
+        local_est = statistics.mean(task_s) * len(tasks) / workers
+        sec, its = h.strip_cg_sample(L, lam_in[0], u[0], 1e-10, strip_maxit)
+        strip_est = sec / its * strip_iters
+        out.append(dict(step_s=local_est + strip_est + aug_s, local_s=local_est,
+                        iface_s=strip_est, aug_s=aug_s, wave_tasks=len(wave),
+                        wave_mean_task_s=statistics.mean(task_s),
+                        wave_iterations=[r[1] for r in res], strip_s_per_iter=sec / its))
+    h.close()
+    return dict(n_int=s["n_int"], samples=out, strip_iters=strip_iters, **info)
 
 
 def run_reference(args, ws, rank):
@@ -213,39 +299,109 @@ def run_reference(args, ws, rank):
     except Exception as e:
         print(json.dumps({"impl": "reference", "unavailable": f"{e}"}))
         return
-    # bounded sample: at most 1 warm-up and 3 timed full steps (each a complete
-    # reference correction step of the workload)
-    r = reference_step_run(wl, steps=min(args.steps, 3), warmup=min(args.warmup, 1),
-                           workers=cores)
-    step_s = statistics.mean(r["times"])
+    line = {"impl": "reference", "metric": METRIC, "unit": "DOF/s", "n_gpus": args.gpus,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "steps_requested": args.steps, "warmup_requested": args.warmup}
+    if args.workload == "c5":
+        # bounded samples (see reference_sampled_steps): warm-up 0, at most 2 steps
+        n_steps = max(1, min(args.steps, 2))
+        r = reference_sampled_steps(wl, n_steps, cores)
+        step_s = statistics.mean(x["step_s"] for x in r["samples"])
+        sample = (f"{n_steps} sampled steps L6->L7: each one wave of {cores} concurrent "
+                  f"local_bvp_solve tasks (of {wl['nev'] * wl['m']}) + cg_solve on the strip "
+                  f"system capped at 30 iterations, scaled to the reference's "
+                  f"{r['strip_iters']} strip iterations; augmented eigensolve timed once")
+        line.update(steps=n_steps, warmup=0, steps_cap="warm-up 0, at most 2 sampled steps "
+                    "(a full reference step takes ~30 min at this size)",
+                    reference_split_s={
+                        "local_est": statistics.mean(x["local_s"] for x in r["samples"]),
+                        "iface_est": statistics.mean(x["iface_s"] for x in r["samples"]),
+                        "aug": r["samples"][0]["aug_s"], "level_build": r["build_s"],
+                        "region_systems": r["regions_s"], "setup": r["setup_s"]},
+                    samples=r["samples"])
+    else:
+        n_steps, n_warm = max(1, min(args.steps, 3)), min(args.warmup, 1)
+        r = reference_full_steps(wl, n_steps, n_warm, cores)
+        step_s = statistics.mean(r["times"])
+        sample = (f"{n_steps} full one_correction_step calls (L{wl['n_levels'] - 1}->"
+                  f"L{wl['n_levels']}) of the workload")
+        line.update(steps=n_steps, warmup=n_warm, steps_cap="at most 1 warm-up and 3 timed "
+                    "full steps", reference_split_s={
+                        "local": statistics.mean(s[0] for s in r["splits"]),
+                        "iface": statistics.mean(s[1] for s in r["splits"]),
+                        "aug": statistics.mean(s[2] for s in r["splits"]),
+                        "level_build": r["build_s"], "region_systems": r["regions_s"]})
     value = r["n_int"] / step_s
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s",
-        "n_gpus": args.gpus, "steps": len(r["times"]), "warmup": min(args.warmup, 1),
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "n_interior": r["n_int"], "threads": cores},
-        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "reference",
-                         "sample": f"{len(r['times'])} full one_correction_step calls "
-                                   f"(L{wl['n_levels'] - 1}->L{wl['n_levels']}) of the workload, "
-                                   f"reference sources built by oracle/Makefile, workers={cores}"},
-        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-        "reference_split_s": {"local": statistics.mean(s[0] for s in r["splits"]),
-                              "iface": statistics.mean(s[1] for s in r["splits"]),
-                              "aug": statistics.mean(s[2] for s in r["splits"]),
-                              "level_build": r["build_s"], "region_systems": r["regions_s"]},
-    }
+    line.update(value=value, ms_per_step=step_s * 1e3,
+                config={"workload": wl["desc"], "n_interior": r["n_int"], "threads": cores},
+                cpu_baseline={"value": value, "unit": "DOF/s", "cores": cores,
+                              "kind": "reference",
+                              "sample": sample + f"; reference sources built by oracle/Makefile, "
+                                                 f"workers={cores}"},
+                e2e={"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline_leg(workload):
+    """The reference's CPU path for our line's cpu_baseline, run in a SUBPROCESS
+    (the product process never maps oracle/_ref).  Config 5's full reference
+    step takes ~30 min, so for it the baseline is the full L6->L7 step measured
+    by tests/golden/make_golden_l7.py in the 8-core build container (labelled);
+    the box-measured number is the --impl reference arm."""
+    if workload == "c5":
+        try:
+            g = json.loads((ROOT / "tests" / "golden" / "golden_l7.json").read_text())
+            step = float(g["step_wall_s"][-1])
+            n = 4095 * 4095
+            return {"value": n / step, "unit": "DOF/s", "cores": int(g.get("workers", 8)),
+                    "kind": "reference", "seconds": step,
+                    "sample": "one full one_correction_step L6->L7 of this workload through the "
+                              "unmodified reference (oracle/_ref), measured in the 8-core build "
+                              "container by tests/golden/make_golden_l7.py, NOT on the GPU "
+                              "box (the box-measured figure is `bench.py --impl reference`)"}
+        except Exception as e:
+            return {"value": None, "unavailable": f"golden_l7.json: {e}"}
+    try:
+        r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                            "--workload", workload, "--steps", "1", "--warmup", "0"],
+                           capture_output=True, text=True, timeout=900, cwd=ROOT)
+        d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+        if "unavailable" in d:
+            return {"value": None, "unavailable": d["unavailable"]}
+        cb = d["cpu_baseline"]
+        cb["seconds"] = d["ms_per_step"] * 1e-3
+        cb["sample"] = "subprocess `bench.py --impl reference --steps 1`: " + cb["sample"]
+        return cb
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "unavailable": str(e)}
+
+
 # -------------------------------------------------------------------- ours ---
+def _roofline(kernel, bound, achieved, role, workload, rows_per_launch, launch_ms, launches,
+              launches_all, share, bytes_per_row, extra=None):
+    peak, src = measured_peak(bound)
+    tr, tr_src = ncu_traffic(f"{workload}:{role}:{kernel}")
+    e = {"kernel": kernel, "role": role, "bound": bound, "achieved": achieved, "peak": peak,
+         "unit": "GB/s", "frac": (achieved / peak) if peak else None, "peak_source": src,
+         "traffic": None if tr is None else tr * rows_per_launch,
+         "traffic_source": tr_src, "algorithmic_bytes_per_launch": bytes_per_row * rows_per_launch,
+         "bytes_per_row": bytes_per_row, "rows_per_launch": rows_per_launch,
+         "avg_launch_ms": launch_ms, "launches": launches, "launches_all": launches_all,
+         "share_of_step": share}
+    if bound != "hbm":  # the same algorithmic bytes against HBM, for reference
+        hp, _ = measured_peak("hbm")
+        e["frac_of_hbm_peak"] = achieved / hp
+    if extra:
+        e.update(extra)
+    return e
+
+
 def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, profile=True):
-    import numpy as np
     import torch
 
     import paper_1401_4969_b200 as mlg
-    from paper_1401_4969_b200.corrector import (multilevel_correction_device,
+    from paper_1401_4969_b200.corrector import (coarse_eigensolve, multilevel_correction_device,
                                                 one_correction_step_device,
                                                 one_correction_step_raw)
     wl = WORKLOADS[workload]
@@ -253,7 +409,7 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     hole = wl.get("hole")
-    cfg = mlg.RunConfig(domain=mlg.DomainRect(*wl.get("domain", (0.0, 1.0, 0.0, 1.0))),
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*wl.get("domain", UNIT_SQUARE)),
                         H=wl["H"], delta=wl["delta"], m=wl["m"], n_levels=L, nev=nev,
                         cg_tol=1e-10, device=local, example=wl.get("example", "laplace"),
                         seed=wl.get("seed", 0), hole=mlg.DomainRect(*hole) if hole else None)
@@ -267,17 +423,20 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
     setup_s = time.time() - t0
     # the level-1 dense generalized eigensolve that starts the multilevel run
     # (solve_interior_eigenproblem, sparse.cpp:326-355; cuSOLVER sygvd), timed alone
-    from paper_1401_4969_b200.corrector import coarse_eigensolve
     t = time.perf_counter()
     coarse_eigensolve(hy, 1, nev)
     torch.cuda.synchronize()
     level1_s = time.perf_counter() - t
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
 
-    # level build of the target level, measured once (Hierarchy::extend_to)
+    # level build of the target level, measured once (Hierarchy::extend_to), with
+    # the assembly launch timed by CUDA events (profiling on)
+    hy.set_profiling(profile)
     t = time.perf_counter()
     hy.extend_to(L)
     build_s = time.perf_counter() - t
+    asm_ms, asm_dofs = hy.build_profile()
+    hy.set_profiling(False)
     n_out = hy.level_info(L).n_interior
     d_out = torch.empty((nev, n_out), dtype=torch.float64, device=dev)
 
@@ -300,6 +459,7 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
     hy.set_profiling(False)
     total = allreduce_max(sum(step_s), ws, dev)
     value = ws * n_out * steps / total
+    tstep = sum(step_s)
 
     out = dict(value=value, ms_per_step=total / steps * 1e3, n_int=n_out, setup_s=setup_s,
                level1_dense_s=level1_s,
@@ -310,35 +470,53 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
                         "local_cg_iterations": tims[-1].local_iterations_max,
                         "strip_cg_iterations": tims[-1].strip_iterations_max},
                gpu_launches=int(sum(t.kernel_launches for t in tims)))
+    rl = {}
+    # local-solve CG kernel: sampled launches, rows counted on the device
     ka_ms = sum(t.spmv_kernel_ms for t in tims)
     ka_n = sum(t.spmv_launches for t in tims)
     ka_rows = sum(t.spmv_rows for t in tims)
     ka_chk = sum(t.spmv_check_rows for t in tims)
     ka_all = sum(t.spmv_launches_all for t in tims)
-    # one cooperative launch per solve vs one launch per CG iteration
-    persistent = ka_all < 0.5 * sum(t.local_iterations_max for t in tims)
+    kk = tims[-1].local_kernel
     if ka_n:
         bpr, bpc = cg_bytes_per_row(tims[-1].spmv_uniform_stencil)
         ka_bytes = ka_rows * bpr + ka_chk * bpc
-        achieved = ka_bytes / (ka_ms * 1e-3) / 1e9
-        peak, peak_src = measured_peak()
-        tr = ncu_traffic(workload)
-        out["roofline"] = {
-            "kernel": ("k_cg_persist (local solves: the fused PCG sweep, all iterations in one "
-                       "cooperative launch, cp.async row ring)" if persistent else
-                       "k_cg_iter (local solves: fused PCG sweep, one launch per iteration)"),
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_source": peak_src,
-            "traffic": None if tr is None else tr * (ka_rows + ka_chk) / ka_n,
-            "algorithmic_bytes_per_launch": ka_bytes / ka_n,
-            "bytes_per_row": bpr, "bytes_per_check_row": bpc,
-            "rows_per_launch": (ka_rows + ka_chk) / ka_n,
-            "uniform_stencil": int(tims[-1].spmv_uniform_stencil),
-            "avg_launch_ms": ka_ms / ka_n, "launches": int(ka_n),
-            "launches_all": int(ka_all),
-            # the sampled launches' mean duration x every launch of the kernel
-            "share_of_step": ka_ms / ka_n * ka_all * 1e-3 / sum(step_s),
-        }
+        kname = KERNEL_NAMES[kk]
+        # per-iteration launches stream every iterate from HBM; the persistent
+        # kernel keeps the batch in L2 (ncu: DRAM << algorithmic bytes)
+        rl["local"] = _roofline(
+            kname, "hbm" if kk == 0 else "l2", ka_bytes / (ka_ms * 1e-3) / 1e9, "local",
+            workload, (ka_rows + ka_chk) / ka_n, ka_ms / ka_n, int(ka_n), int(ka_all),
+            ka_ms / ka_n * ka_all * 1e-3 / tstep, bpr,
+            {"bytes_per_check_row": bpc, "uniform_stencil": int(tims[-1].spmv_uniform_stencil),
+             "what": "local-solve batched Jacobi-PCG, fused one-reduction sweep "
+                     "(local_bvp_solve corrector.cpp:198-214, cg_solve sparse.cpp:199-258)"})
+    # strip-solve CG kernel: every launch timed, unknowns x CG updates from the host
+    ks_ms = sum(t.strip_kernel_ms for t in tims)
+    ks_n = sum(t.strip_launches for t in tims)
+    ks_ri = sum(t.strip_row_iters for t in tims)
+    if ks_n and ks_ri:
+        bpr = tims[-1].strip_bytes_per_row
+        sk = tims[-1].strip_kernel
+        rl["strip"] = _roofline(
+            KERNEL_NAMES[sk], "hbm" if sk == 0 else "l2", ks_ri * bpr / (ks_ms * 1e-3) / 1e9,
+            "strip", workload, ks_ri / ks_n, ks_ms / ks_n, int(ks_n), int(ks_n),
+            ks_ms * 1e-3 / tstep, bpr,
+            {"what": "strip-solve Jacobi-PCG over the masked strip window "
+                     "(interface_solve corrector.cpp:216-254); bytes = strip unknowns x CG "
+                     "updates x bytes_per_row (true-residual sweeps not counted)"})
+    if asm_ms > 0:
+        rl["assembly"] = _roofline(
+            "k_assemble", "hbm", asm_dofs * ASSEMBLE_BYTES_PER_DOF / (asm_ms * 1e-3) / 1e9,
+            "assembly", workload, asm_dofs, asm_ms, 1, 1, None, ASSEMBLE_BYTES_PER_DOF,
+            {"what": "P1 stiffness + mass assembly of the level (assemble_form "
+                     "fespace.cpp:314-341 + from_upper_triplets sparse.cpp:24-61): one thread "
+                     "per dof, element matrices recomputed per dof, stencil rows written once; "
+                     "timed once in the level build (not part of the step)"})
+    out["rooflines"] = rl
+    steprl = [v for k, v in rl.items() if k in ("local", "strip")]
+    if steprl:
+        out["roofline"] = max(steprl, key=lambda e: e["share_of_step"] or 0.0)
 
     if with_e2e:  # through the host C-ABI with pinned host buffers
         h_in = torch.empty((nev, n_in), dtype=torch.float64, pin_memory=True)
@@ -361,10 +539,19 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
                       "ms_per_step": etot / steps * 1e3}
     ms, by = hy.bench_spmv(L, 20)
     out["spmv_microbench"] = {"kernel": "interior stiffness SpMV (stencil format)",
-                              "ms": ms, "GB/s": by / ms / 1e6, "bytes": by,
-                              "csr_equivalent_GB/s": None}
+                              "ms": ms, "GB/s": by / ms / 1e6, "bytes": by}
     hy.close()
     return out
+
+
+def _extra(res, wl):
+    return {"workload": wl["desc"], "value": res["value"], "unit": "DOF/s",
+            "ms_per_step": res["ms_per_step"], "n_interior": res["n_int"],
+            "level_build_s": res["build_s"],
+            "timings": {**res["timings"], "setup_s": res["setup_s"],
+                        "level1_dense_eigensolve_s": res["level1_dense_s"]},
+            "roofline": res.get("roofline"), "rooflines": res.get("rooflines"),
+            "e2e": res.get("e2e"), "lambdas": res["lam"], "clocks": res["clocks"]}
 
 
 def main():
@@ -373,9 +560,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--no-north-star", action="store_true",
-                    help="skip the extra config-5 (4096^2), config-4 and config-3 measurements")
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-extras", "--no-north-star", dest="no_extras", action="store_true",
+                    help="skip the extra config-2, config-3 and config-4 measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
@@ -384,29 +571,15 @@ def main():
         return
     wl = WORKLOADS[args.workload]
     res = run_ours(args, ws, rank, local, args.workload, args.steps, args.warmup)
-    extra = extra4 = None
-    if not args.no_north_star and args.workload != "c5":
-        extra = run_ours(args, ws, rank, local, "c5", steps=2, warmup=1, with_e2e=False)
-    if not args.no_north_star and args.workload != "c4":
-        extra4 = run_ours(args, ws, rank, local, "c4", steps=2, warmup=1, with_e2e=False)
-    extra3 = None
-    if not args.no_north_star and args.workload != "c3":
-        extra3 = run_ours(args, ws, rank, local, "c3", steps=2, warmup=1, with_e2e=False)
+    extras = {}
+    if not args.no_extras:
+        for w in ("c2", "c3", "c4"):
+            if w != args.workload:
+                extras[w] = run_ours(args, ws, rank, local, w, steps=3, warmup=3,
+                                     with_e2e=(w == "c2"))
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        try:
-            from oracle import ref
-            if ref.available():
-                cores = os.cpu_count() or 1
-                r = reference_step_run(wl, steps=1, warmup=0, workers=cores)
-                cpu = {"value": r["n_int"] / r["times"][0], "unit": "DOF/s", "cores": cores,
-                       "kind": "reference",
-                       "sample": f"one full one_correction_step L{wl['n_levels'] - 1}->"
-                                 f"L{wl['n_levels']} of the headline workload on the reference "
-                                 f"(oracle/_ref, workers={cores}); setup untimed",
-                       "seconds": r["times"][0]}
-        except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unavailable": str(e)}
+        cpu = cpu_baseline_leg(args.workload)
     if rank != 0:
         return
     line = {
@@ -418,35 +591,16 @@ def main():
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MiB write)",
                    "lambdas": res["lam"]},
-        "roofline": res.get("roofline"), "cpu_baseline": cpu, "e2e": res.get("e2e"),
+        "roofline": res.get("roofline"), "rooflines": res.get("rooflines"),
+        "cpu_baseline": cpu, "e2e": res.get("e2e"),
         "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
         "timings": {**res["timings"], "level_build_s": res["build_s"], "setup_s": res["setup_s"],
                     "level1_dense_eigensolve_s": res["level1_dense_s"]},
         "spmv_microbench": res["spmv_microbench"],
     }
-    if extra:
-        line["north_star_workload"] = {
-            "workload": WORKLOADS["c5"]["desc"], "value": extra["value"], "unit": "DOF/s",
-            "ms_per_step": extra["ms_per_step"], "n_interior": extra["n_int"],
-            "level_build_s": extra["build_s"],
-            "timings": {**extra["timings"], "setup_s": extra["setup_s"],
-                        "level1_dense_eigensolve_s": extra["level1_dense_s"]},
-            "roofline": extra.get("roofline"), "lambdas": extra["lam"],
-            "clocks": extra["clocks"], "spmv_microbench": extra["spmv_microbench"]}
-    if extra3:
-        line["config3_workload"] = {
-            "workload": WORKLOADS["c3"]["desc"], "value": extra3["value"], "unit": "DOF/s",
-            "ms_per_step": extra3["ms_per_step"], "n_interior": extra3["n_int"],
-            "level_build_s": extra3["build_s"], "timings": extra3["timings"],
-            "roofline": extra3.get("roofline"), "lambdas": extra3["lam"],
-            "clocks": extra3["clocks"]}
-    if extra4:
-        line["config4_workload"] = {
-            "workload": WORKLOADS["c4"]["desc"], "value": extra4["value"], "unit": "DOF/s",
-            "ms_per_step": extra4["ms_per_step"], "n_interior": extra4["n_int"],
-            "level_build_s": extra4["build_s"], "timings": extra4["timings"],
-            "roofline": extra4.get("roofline"), "lambdas": extra4["lam"],
-            "clocks": extra4["clocks"]}
+    for w, r in extras.items():
+        line[{"c2": "config2_workload", "c3": "config3_workload",
+              "c4": "config4_workload"}[w]] = _extra(r, WORKLOADS[w])
     print(json.dumps(line), flush=True)
 
 

@@ -106,6 +106,14 @@ typedef struct mlg_step_timings {
   int64_t spmv_launches_all; /* all launches of that kernel in the step (sampled or not):
                                 the kernel's share of the step is
                                 spmv_kernel_ms / spmv_launches * spmv_launches_all */
+  double strip_kernel_ms;  /* summed device time of EVERY strip-solve CG launch (profiling on) */
+  int64_t strip_launches;  /* number of those launches */
+  double strip_row_iters;  /* sum over strip systems of unknowns x CG updates (host count) */
+  int strip_kernel;        /* CG kernel of the strip batch: 0 k_cg_iter (one launch per
+                              iteration), 1 k_cg_persist (one cooperative launch per
+                              solve), 2 k_cg_resident (iterates resident on chip) */
+  int local_kernel;        /* the same for the local-solve batch */
+  int strip_bytes_per_row; /* algorithmic bytes per unknown and CG update of that kernel */
 } mlg_step_timings;
 
 const char* mlg_last_error(void);
@@ -166,6 +174,14 @@ int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const dou
 
 /* interface_solve (corrector.hpp:118-120, corrector.cpp:216-254);
  * corrections[m][ndofs]. */
+/* The CG of local_bvp_solve with cg_solve's own contract (sparse.hpp:109-116,
+ * sparse.cpp:199-258): maxit > 0 replaces the default 10 n, non-convergence is
+ * REPORTED (report->converged = 0, final_residual = true relative residual),
+ * not thrown; a zero right-hand side returns after 0 iterations.  e_full as in
+ * mlg_local_bvp_solve. */
+int mlg_local_cg_solve(mlg_ctx* ctx, int level, int j, double lambda, const double* u_full,
+                       double cg_tol, int maxit, double* e_full, mlg_solve_report* report);
+
 int mlg_interface_solve(mlg_ctx* ctx, int level, double lambda, const double* u_full,
                         const double* corrections, double cg_tol, double* glued_full,
                         mlg_solve_report* report);
@@ -182,7 +198,12 @@ int mlg_correction_step(mlg_ctx* ctx, int from_level, int to_level, int nev,
                         const double* lambdas_in, const double* coeffs_in, double* lambdas_out,
                         double* coeffs_out, int* matched, mlg_step_timings* timings);
 
-/* Same, with coefficient arrays resident in device memory (same layout). */
+/* Same, with coefficient arrays resident in device memory (same layout).
+ * Ordering: before touching d_coeffs_in / d_coeffs_out the call makes the
+ * context's stream wait for all work already queued on the input stream
+ * (mlg_set_input_stream; default the legacy default stream 0), so a caller that
+ * filled the input with asynchronous kernels or copies on that stream need not
+ * synchronize first.  The call returns after the outputs are written. */
 int mlg_correction_step_device(mlg_ctx* ctx, int from_level, int to_level, int nev,
                                const double* lambdas_in, const double* d_coeffs_in,
                                double* lambdas_out, double* d_coeffs_out, int* matched,
@@ -196,8 +217,18 @@ int mlg_multilevel_correction(mlg_ctx* ctx, int last_level, double* lambdas,
                               double* final_coeffs, double* d_final_coeffs, int* matched,
                               mlg_step_timings* timings);
 
+/* The CUDA stream (cudaStream_t, as void*) whose queued work the *_device entry
+ * points wait for before reading or writing caller device buffers; NULL (the
+ * default) = the legacy default stream. */
+int mlg_set_input_stream(mlg_ctx* ctx, void* stream);
+
 /* Record CUDA events around every local-solve SpMV launch (roofline evidence). */
 int mlg_set_profiling(mlg_ctx* ctx, int on);
+
+/* Assembly kernel evidence of the most recent level built with profiling on:
+ * summed CUDA-event time of its operator assembly launch(es) and the dofs they
+ * assembled (fespace.cpp:314-341 replaced by k_assemble). */
+int mlg_build_profile(mlg_ctx* ctx, double* assemble_ms, double* assemble_dofs);
 
 /* Interior-stiffness SpMV microbenchmark (extract_submatrix(A, interior) x):
  * average device ms per launch over `reps` launches, and its algorithmic bytes. */

@@ -196,6 +196,22 @@ class RefHierarchy:
                                        _d(e), C.byref(it), C.byref(fr)))
         return e, it.value, fr.value
 
+    def local_bvp_time(self, level, j, lam, u_full, tol):
+        """(seconds, iterations) of one local_bvp_solve task, timed in C++."""
+        u = np.ascontiguousarray(u_full, np.float64)
+        sec = C.c_double(); it = C.c_int()
+        _chk(lib().ref_local_bvp_time(self.h, level, j, C.c_double(lam), _d(u), C.c_double(tol),
+                                      C.byref(sec), C.byref(it)))
+        return sec.value, it.value
+
+    def strip_cg_sample(self, level, lam, u_full, tol, maxit):
+        """(seconds, iterations) of cg_solve on the strip system capped at maxit."""
+        u = np.ascontiguousarray(u_full, np.float64)
+        sec = C.c_double(); it = C.c_int()
+        _chk(lib().ref_strip_cg_sample(self.h, level, C.c_double(lam), _d(u), C.c_double(tol),
+                                       int(maxit), C.byref(sec), C.byref(it)))
+        return sec.value, it.value
+
     def interface_solve(self, level, lam, u_full, corr, tol):
         u = np.ascontiguousarray(u_full, np.float64); corr = np.ascontiguousarray(corr, np.float64)
         g = np.empty_like(u); it = C.c_int(); fr = C.c_double()

@@ -325,6 +325,47 @@ int ref_local_bvp_solve(void* h, int level, int j, double lambda, const double* 
   });
 }
 
+// Timing samples for bench.py's reference arm (bounded samples of a correction
+// step whose full run takes tens of minutes at 4096^2):
+//  * ref_local_bvp_time: one local_bvp_solve task exactly as one_correction_step
+//    runs it (corrector.cpp:364-370 -> :198-214), timed around the call only;
+//    concurrent calls from several host threads are what parallel_tasks does
+//    (region systems are built first, then only read).
+//  * ref_strip_cg_sample: the reference's cg_solve (sparse.cpp:199-258) on the
+//    level's strip system with interface_solve's load form (corrector.cpp:238-242,
+//    glued = u), capped at maxit iterations, timed around cg_solve only.
+int ref_local_bvp_time(void* h, int level, int j, double lambda, const double* u_full,
+                       double tol, double* seconds, int* iters) {
+  return guarded([&] {
+    LevelSystem& L = H(h).level(level);
+    L.build_region_systems(H(h).partition());
+    const Vector u = to_vec(u_full, L.space.ndofs);
+    SolveReport rep;
+    const auto t0 = std::chrono::steady_clock::now();
+    const Vector e = local_bvp_solve(L, j, lambda, u, tol, &rep);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (iters) *iters = rep.iterations;
+  });
+}
+
+int ref_strip_cg_sample(void* h, int level, double lambda, const double* u_full, double tol,
+                        int maxit, double* seconds, int* iters) {
+  return guarded([&] {
+    LevelSystem& L = H(h).level(level);
+    L.build_region_systems(H(h).partition());
+    const Vector u = to_vec(u_full, L.space.ndofs);
+    const Vector load = lambda * L.mass.apply(u) - L.stiffness.apply(u);
+    const RegionSystem& strip = L.strip_system;
+    Vector rhs(static_cast<int>(strip.dofs.size()));
+    for (std::size_t i = 0; i < strip.dofs.size(); ++i)
+      rhs[static_cast<int>(i)] = load[strip.dofs[i]];
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [x, rep] = cg_solve(strip.a_sub, rhs, tol, maxit);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (iters) *iters = rep.iterations;
+  });
+}
+
 int ref_interface_solve(void* h, int level, double lambda, const double* u_full,
                         const double* corrections, double tol, double* glued, int* iters,
                         double* final_res) {

@@ -5,7 +5,7 @@ reference's corrector interface."""
 from ._lib import ConfigError, CudaError, IoError, MlgError, SolverError, lib
 from .corrector import (CorrectionState, DomainRect, EigenPair, Hierarchy, RunConfig,
                         SolveReport, StepTimings, augmented_eigensolve, coarse_eigensolve,
-                        interface_solve, local_bvp_solve, multilevel_correction,
+                        interface_solve, local_bvp_solve, local_cg_solve, multilevel_correction,
                         one_correction_step)
 from . import harness
 
@@ -13,5 +13,5 @@ __all__ = [
     "ConfigError", "CudaError", "IoError", "MlgError", "SolverError", "lib",
     "CorrectionState", "DomainRect", "EigenPair", "Hierarchy", "RunConfig", "SolveReport",
     "StepTimings", "augmented_eigensolve", "coarse_eigensolve", "interface_solve",
-    "local_bvp_solve", "multilevel_correction", "one_correction_step", "harness",
+    "local_bvp_solve", "local_cg_solve", "multilevel_correction", "one_correction_step", "harness",
 ]

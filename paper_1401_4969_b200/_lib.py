@@ -77,6 +77,9 @@ class MlgStepTimings(C.Structure):
         ("spmv_rows", C.c_double), ("kernel_launches", C.c_int64),
         ("step_seconds", C.c_double), ("spmv_uniform_stencil", C.c_int),
         ("spmv_check_rows", C.c_double), ("spmv_launches_all", C.c_int64),
+        ("strip_kernel_ms", C.c_double), ("strip_launches", C.c_int64),
+        ("strip_row_iters", C.c_double), ("strip_kernel", C.c_int),
+        ("strip_bytes_per_row", C.c_int), ("local_kernel", C.c_int),
     ]
 
 
@@ -118,6 +121,8 @@ SIGNATURES = {
     "mlg_coarse_eigensolve": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
     "mlg_local_bvp_solve": [C.c_void_p, C.c_int, C.c_int, C.c_double, c_double_p, C.c_double,
                             c_double_p, C.POINTER(MlgSolveReport)],
+    "mlg_local_cg_solve": [C.c_void_p, C.c_int, C.c_int, C.c_double, c_double_p, C.c_double,
+                           C.c_int, c_double_p, C.POINTER(MlgSolveReport)],
     "mlg_interface_solve": [C.c_void_p, C.c_int, C.c_double, c_double_p, c_double_p,
                             C.c_double, c_double_p, C.POINTER(MlgSolveReport)],
     "mlg_augmented_eigensolve": [C.c_void_p, C.c_int, C.c_int, c_double_p, C.c_int,
@@ -147,6 +152,8 @@ SIGNATURES = {
     "mlg_print_table": [C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
     "mlg_export_vtk": [C.POINTER(MlgConfig), C.c_char_p],
     "mlg_set_profiling": [C.c_void_p, C.c_int],
+    "mlg_set_input_stream": [C.c_void_p, C.c_void_p],
+    "mlg_build_profile": [C.c_void_p, c_double_p, c_double_p],
     "mlg_bench_spmv": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
 }
 

@@ -89,13 +89,22 @@ class StepTimings:  # corrector.hpp:97-101 (+ device evidence)
     spmv_uniform_stencil: int = 0  # 0 general, 1 uniform, 2 uniform + deferred x
     spmv_check_rows: float = 0.0
     spmv_launches_all: int = 0  # every launch of the sampled kernel in the step
+    strip_kernel_ms: float = 0.0  # every strip-solve CG launch (profiling on)
+    strip_launches: int = 0
+    strip_row_iters: float = 0.0  # strip unknowns x CG updates
+    strip_kernel: int = 0
+    strip_bytes_per_row: int = 0
+    local_kernel: int = 0  # 0 k_cg_iter, 1 k_cg_persist, 2 k_cg_resident
 
     @classmethod
     def from_c(cls, t: MlgStepTimings) -> "StepTimings":
         return cls(t.local_seconds, t.iface_seconds, t.aug_seconds, t.build_seconds,
                    t.local_iterations_max, t.strip_iterations_max, t.spmv_kernel_ms,
                    t.spmv_launches, t.spmv_rows, t.kernel_launches, t.step_seconds,
-                   int(t.spmv_uniform_stencil), t.spmv_check_rows, t.spmv_launches_all)
+                   int(t.spmv_uniform_stencil), t.spmv_check_rows, t.spmv_launches_all,
+                   t.strip_kernel_ms, t.strip_launches, t.strip_row_iters,
+                   int(t.strip_kernel), int(t.strip_bytes_per_row),
+                   int(t.local_kernel))
 
 
 @dataclass
@@ -291,6 +300,17 @@ class Hierarchy:
     def restrict_interior(self, level: int, full) -> np.ndarray:  # fespace.cpp:417-423
         return np.ascontiguousarray(np.asarray(full)[self._interior(level)])
 
+    def set_input_stream(self, stream: int) -> None:
+        """CUDA stream (raw handle; 0 = legacy default) the *_device calls order after."""
+        check(lib().mlg_set_input_stream(self._h, C.c_void_p(stream)))
+
+    def build_profile(self):
+        """(assemble_ms, assembled dofs) of the last level built with profiling on."""
+        ms = C.c_double()
+        n = C.c_double()
+        check(lib().mlg_build_profile(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     def set_profiling(self, on: bool) -> None:
         check(lib().mlg_set_profiling(self._h, int(on)))
 
@@ -318,6 +338,18 @@ def local_bvp_solve(hy: Hierarchy, level: int, j: int, lam: float, u_full, cg_to
     rep = MlgSolveReport()
     check(lib().mlg_local_bvp_solve(hy.handle, level, j, lam, _dp(u), cg_tol, _dp(e),
                                     C.byref(rep)))
+    return e, SolveReport(rep.iterations, rep.final_residual, bool(rep.converged))
+
+
+def local_cg_solve(hy: Hierarchy, level: int, j: int, lam: float, u_full, cg_tol: float,
+                   maxit: int = 0):
+    """The CG of local_bvp_solve with cg_solve's contract (sparse.cpp:199-258):
+    maxit > 0 caps the iterations and non-convergence is reported, not raised."""
+    u = _f64(u_full)
+    e = np.empty_like(u)
+    rep = MlgSolveReport()
+    check(lib().mlg_local_cg_solve(hy.handle, level, j, lam, _dp(u), cg_tol, int(maxit),
+                                   _dp(e), C.byref(rep)))
     return e, SolveReport(rep.iterations, rep.final_residual, bool(rep.converged))
 
 
@@ -361,12 +393,29 @@ def one_correction_step(hy: Hierarchy, state: CorrectionState, to_level: int):
     return CorrectionState(to_level, pairs, bool(matched.value)), StepTimings.from_c(t)
 
 
+def _check_host_block(a, shape, name, writeable):
+    """The raw entry point hands the buffer to C as nev*n doubles: refuse anything
+    else (dtype, layout, shape) instead of letting the library overrun it."""
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"{name} must be a numpy array")
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise TypeError(f"{name} must be a C-contiguous float64 array")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {a.shape}, expected {tuple(shape)}")
+    if writeable and not a.flags.writeable:
+        raise ValueError(f"{name} must be writeable")
+
+
 def one_correction_step_raw(hy: Hierarchy, from_level: int, to_level: int, lambdas_in,
                             coeffs_in: np.ndarray, coeffs_out: np.ndarray):
     """one_correction_step on caller-owned (e.g. pinned) host arrays, no copies on
     the Python side: coeffs_in (nev, n_int(from)), coeffs_out (nev, n_int(to))."""
     lam_in = _f64(lambdas_in)
     nev = len(lam_in)
+    _check_host_block(coeffs_in, (nev, hy.level_info(from_level).n_interior), "coeffs_in",
+                      writeable=False)
+    _check_host_block(coeffs_out, (nev, hy.level_info(to_level).n_interior), "coeffs_out",
+                      writeable=True)
     lam_out = np.empty(nev, np.float64)
     matched = C.c_int()
     t = MlgStepTimings()

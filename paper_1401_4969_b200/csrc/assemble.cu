@@ -510,6 +510,12 @@ void assemble_level(Ctx& c, Level& L) {
   L.stM.alloc(nd);
   L.dinv.alloc(nd);
   LevelGeom G{L.nx, L.ny, c.cfg.x_min, c.cfg.y_min, L.dx, L.dy, L.geo.get()};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (c.profile) {  // roofline evidence: the assembly launch alone
+    ev0 = c.event(0);
+    ev1 = c.event(1);
+    MLG_CUDA(cudaEventRecord(ev0, c.stream));
+  }
   if (c.cfg.example == 1) {
     {  // make_degree6 (fespace.cpp:49-75), same point order
       const double a1 = 0.501426509658179, b1 = 0.249286745170910, w1 = 0.116786275726379;
@@ -535,6 +541,14 @@ void assemble_level(Ctx& c, Level& L) {
                                                                  L.dinv.get());
   }
   MLG_LAUNCH_CHECK();
+  if (c.profile) {
+    MLG_CUDA(cudaEventRecord(ev1, c.stream));
+    MLG_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    MLG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    c.asm_ms = ms;
+    c.asm_dofs = static_cast<double>(nd);
+  }
   // Constant-coefficient detection for the CG fast path (MLG_GENERAL_STENCIL=1
   // forces the general per-row path, used by the tests to cover both).
   L.uniform = 0;

@@ -26,10 +26,11 @@ std::string& last_error_slot() {
 
 namespace {
 
-std::string& g_err = mlg::last_error_slot();
-
+// The message slot is thread-local: look it up on the calling thread every
+// time (a namespace-scope reference would bind the loader thread's slot).
 template <class F>
 int guarded(F&& f) {
+  std::string& g_err = mlg::last_error_slot();
   try {
     f();
     g_err.clear();
@@ -73,6 +74,12 @@ void fill_timings(mlg_step_timings* t, const mlg::StepTimes& s, const mlg::Ctx& 
   t->kernel_launches = mlg::launch_counter().load() - c.times.launch_base;
   t->spmv_uniform_stencil = c.times.ka_uniform;
   t->spmv_launches_all = c.times.ka_launches_all;
+  t->strip_kernel_ms = c.times.ks_ms;
+  t->strip_launches = c.times.ks_launches;
+  t->strip_row_iters = c.times.ks_row_iters;
+  t->strip_kernel = c.times.ks_kernel;
+  t->local_kernel = c.times.ka_kernel;
+  t->strip_bytes_per_row = c.times.ks_bytes_per_row;
 }
 
 void reset_kernel_stats(mlg::Ctx& c) {
@@ -82,6 +89,11 @@ void reset_kernel_stats(mlg::Ctx& c) {
   c.times.ka_rows = 0;
   c.times.ka_check_rows = 0;
   c.times.kernel_launches = 0;
+  c.times.ks_ms = 0;
+  c.times.ks_launches = 0;
+  c.times.ks_row_iters = 0;
+  c.times.ks_kernel = 0;
+  c.times.ks_bytes_per_row = 0;
   c.times.launch_base = mlg::launch_counter().load();
 }
 
@@ -172,7 +184,10 @@ void multilevel_impl(mlg_ctx* ctx, int last_level, int n_refs, const double* ref
     record(k + 1, lam);
   }
   const mlg::Level& L = c.level(nlev);
-  if (d_final_coeffs) mlg::deinterleave(c, L, nr, nev, nullptr, u.get(), 1, d_final_coeffs);
+  if (d_final_coeffs) {
+    c.order_after_input();  // the caller's buffer may still be in use on its stream
+    mlg::deinterleave(c, L, nr, nev, nullptr, u.get(), 1, d_final_coeffs);
+  }
   if (final_coeffs) {
     mlg::DevBuf<double> out(L.nint() * nev);
     mlg::deinterleave(c, L, nr, nev, nullptr, u.get(), 1, out.get());
@@ -185,7 +200,7 @@ void multilevel_impl(mlg_ctx* ctx, int last_level, int n_refs, const double* ref
 
 extern "C" {
 
-const char* mlg_last_error(void) { return g_err.c_str(); }
+const char* mlg_last_error(void) { return mlg::last_error_slot().c_str(); }
 
 int mlg_create(const mlg_config* cfg, mlg_ctx** out) {
   return guarded([&] {
@@ -400,9 +415,12 @@ int mlg_coarse_eigensolve(mlg_ctx* ctx, int level, int nev, double* lambdas, dou
   });
 }
 
-int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const double* u_full,
-                        double cg_tol, double* e_full, mlg_solve_report* report) {
-  return guarded([&] {
+namespace {
+// local_bvp_solve (corrector.cpp:198-214) on one subdomain; maxit > 0 overrides
+// cg_solve's default 10 n (sparse.cpp:204).
+void local_solve_impl(mlg_ctx* ctx, int level, int j, double lambda, const double* u_full,
+                      double cg_tol, int maxit, double* e_full, mlg_solve_report* report,
+                      bool throw_unconverged) {
     mlg::Ctx& c = C(ctx);
     mlg::Level& F = c.level(level);
     if (j < 0 || j >= c.part.m) throw mlg::ConfigError("subdomain index out of range");
@@ -415,7 +433,7 @@ int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const dou
     mlg::interleave(c, F, 1, 1, u.get(), 0, ui.get());
     mlg::residual(c, F, 1, ui.get(), &lambda, res.get());
     std::vector<mlg::SolveReport> rep;
-    mlg::local_solves(c, F, 1, 1, res.get(), cg_tol, 0, &rep, j);
+    mlg::local_solves(c, F, 1, 1, res.get(), cg_tol, maxit, &rep, j);
     const mlg::LocalView b = mlg::local_view(c);
     const mlg::CgSys s = b.systems[0];
     std::vector<double> x(static_cast<std::size_t>(s.h) * s.pitch);  // window rows, pitched
@@ -432,11 +450,26 @@ int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const dou
       report->final_residual = rep[0].final_residual;
       report->converged = rep[0].converged;
     }
-    if (!rep[0].converged)
+    if (throw_unconverged && !rep[0].converged)
       throw mlg::SolverError("subdomain " + std::to_string(j + 1) +
                              " solve did not converge (" + std::to_string(rep[0].iterations) +
                              " iterations, residual " + std::to_string(rep[0].final_residual) +
                              ")");
+}
+}  // namespace
+
+int mlg_local_bvp_solve(mlg_ctx* ctx, int level, int j, double lambda, const double* u_full,
+                        double cg_tol, double* e_full, mlg_solve_report* report) {
+  return guarded([&] {
+    local_solve_impl(ctx, level, j, lambda, u_full, cg_tol, 0, e_full, report, true);
+  });
+}
+
+int mlg_local_cg_solve(mlg_ctx* ctx, int level, int j, double lambda, const double* u_full,
+                       double cg_tol, int maxit, double* e_full, mlg_solve_report* report) {
+  return guarded([&] {
+    if (maxit < 0) throw mlg::ConfigError("maxit must be nonnegative");
+    local_solve_impl(ctx, level, j, lambda, u_full, cg_tol, maxit, e_full, report, false);
   });
 }
 
@@ -495,6 +528,23 @@ int mlg_augmented_eigensolve(mlg_ctx* ctx, int level, int k_in, const double* gl
   });
 }
 
+namespace {
+// Timing events of one C-ABI call, destroyed on every exit path.
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventPair() {
+    MLG_CUDA(cudaEventCreate(&a));
+    MLG_CUDA(cudaEventCreate(&b));
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  EventPair(const EventPair&) = delete;
+  EventPair& operator=(const EventPair&) = delete;
+};
+}  // namespace
+
 static int step_impl(mlg_ctx* ctx, int from_level, int to_level, int nev,
                      const double* lambdas_in, const double* coeffs_in, bool device_in,
                      double* lambdas_out, double* coeffs_out, bool device_out, int* matched,
@@ -505,10 +555,9 @@ static int step_impl(mlg_ctx* ctx, int from_level, int to_level, int nev,
     const int nr = mlg::nr_for(nev);
     const mlg::Level& A = c.level(from_level);
     reset_kernel_stats(c);
-    cudaEvent_t ev0, ev1;
-    MLG_CUDA(cudaEventCreate(&ev0));
-    MLG_CUDA(cudaEventCreate(&ev1));
-    MLG_CUDA(cudaEventRecord(ev0, c.stream));
+    if (device_in || device_out) c.order_after_input();  // caller's writes to its buffers
+    EventPair ev;
+    MLG_CUDA(cudaEventRecord(ev.a, c.stream));
     // grow-only context buffers: no allocation inside a steady-state step
     mlg::DevBuf<double>& in_ri = c.io_in;
     mlg::DevBuf<double>& u_in = c.io_u_in;
@@ -535,12 +584,10 @@ static int step_impl(mlg_ctx* ctx, int from_level, int to_level, int nev,
         out.download(coeffs_out, B.nint() * nev, c.stream);
       }
     }
-    MLG_CUDA(cudaEventRecord(ev1, c.stream));
+    MLG_CUDA(cudaEventRecord(ev.b, c.stream));
     c.sync();
     float ms = 0.f;
-    MLG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
+    MLG_CUDA(cudaEventElapsedTime(&ms, ev.a, ev.b));
     if (matched) *matched = r.matched ? 1 : 0;
     fill_timings(timings, r.times, c);
     if (timings) timings->step_seconds = ms * 1e-3;
@@ -629,6 +676,18 @@ int mlg_compute_errors(mlg_ctx* ctx, int level, const double* coeffs_full, doubl
     const mlg::ErrorReport r = mlg::compute_errors(c, L, d.get(), 1, 0, lambda_h, lambda_ref,
                                                    reference ? &md : nullptr);
     *out = {r.eig_err, r.l2_err, r.h1_err};
+  });
+}
+
+int mlg_set_input_stream(mlg_ctx* ctx, void* stream) {
+  return guarded([&] { C(ctx).input_stream = static_cast<cudaStream_t>(stream); });
+}
+
+int mlg_build_profile(mlg_ctx* ctx, double* assemble_ms, double* assemble_dofs) {
+  return guarded([&] {
+    const mlg::Ctx& c = C(ctx);
+    if (assemble_ms) *assemble_ms = c.asm_ms;
+    if (assemble_dofs) *assemble_dofs = c.asm_dofs;
   });
 }
 

@@ -1862,7 +1862,11 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
                    L->ust.ne == 0.0 && L->udinv == 0.25 && std::getenv("MLG_CG_NOLAP") == nullptr;
   SweepArgs A = sweep_args(*L, mask);
   A.task_map = task_map.get();
+  // Roofline evidence: local batches (no mask) sample launches and count swept
+  // rows on the device; strip batches time every launch and count unknowns x
+  // CG updates on the host at the end.
   const bool profiling = c.profile && mask == nullptr;
+  const bool sprof = c.profile && mask != nullptr;
   if (profiling) {
     prof_rows.ensure(2);
     prof_rows.zero(c.stream);
@@ -1937,13 +1941,14 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     double* xp = X.get();
     double *r0 = R0.get(), *r1 = R1.get(), *p0 = P0.get(), *p1 = P1.get();
     const Finish& Fl = profiling ? Fp : F;
+    const bool timed = profiling || sprof;
     GridSync G{gsync.get(), gsync.get() + 1, kIters};
     void* args[] = {(void*)&sp, (void*)&tp, (void*)&ntiles, (void*)&A, (void*)&bsrc,
                     (void*)&bstride, (void*)&xp, (void*)&r0, (void*)&r1, (void*)&p0,
                     (void*)&p1, (void*)&Fl, (void*)&G};
     for (int launch = 0;; ++launch) {
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-      if (profiling) {
+      if (timed) {
         ev0 = c.event(2 * evs.size());
         ev1 = c.event(2 * evs.size() + 1);
         MLG_CUDA(cudaEventRecord(ev0, st));
@@ -1957,10 +1962,10 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       MLG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args,
                                            persist_async ? kRingBytes : 0, st));
       ++launch_counter();
-      if (profiling) {
+      if (timed) {
         MLG_CUDA(cudaEventRecord(ev1, st));
         evs.emplace_back(ev0, ev1);
-        ++c.times.ka_launches_all;
+        if (profiling) ++c.times.ka_launches_all;
       }
       ctl_d.download(ctl.data(), ctl.size(), st);
       c.sync();
@@ -2025,7 +2030,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       // bracketed by pooled CUDA events (cheap enough not to starve the stream).
       // (pairs of consecutive launches: with deferred x updates the two phases
       // move 32 and 56 B/row, so a pair is the unit the 44 B/row average holds for)
-      const bool prof = profiling && (iter_count++ % 8 < 2);
+      const bool prof = sprof || (profiling && (iter_count++ % 8 < 2));
       if (profiling) ++c.times.ka_launches_all;
       cudaEvent_t ev0 = nullptr, ev1 = nullptr;
       if (prof) {
@@ -2033,7 +2038,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
         ev1 = c.event(2 * evs.size() + 1);
         MLG_CUDA(cudaEventRecord(ev0, st));
       }
-      const Finish& Fl = prof ? Fp : F;
+      const Finish& Fl = prof && profiling ? Fp : F;
       if (uni && use_async && lap)
         k_cg_iter<true, true, true><<<nt, kBlock, kRingBytes, st>>>(
             sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
@@ -2079,9 +2084,19 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
   for (auto& e : evs) {
     float ms = 0.f;
     MLG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
-    c.times.ka_ms_sum += ms;
-    c.times.ka_launches += 1;
+    if (sprof) {
+      c.times.ks_ms += ms;
+      c.times.ks_launches += 1;
+    } else {
+      c.times.ka_ms_sum += ms;
+      c.times.ka_launches += 1;
+    }
   }
+  if (sprof) {
+    for (std::size_t k = 0; k < ctl.size(); ++k)
+      c.times.ks_row_iters += static_cast<double>(sys_h[k].nrows) * ctl[k].iters;
+  }
+  (mask ? c.times.ks_kernel : c.times.ka_kernel) = use_persist ? 1 : 0;
   if (profiling) {
     unsigned long long rows[2] = {0, 0};
     prof_rows.download(rows, 2, c.stream);
@@ -2089,7 +2104,10 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     c.times.ka_rows += static_cast<double>(rows[0]);
     c.times.ka_check_rows += static_cast<double>(rows[1]);
   }
-  c.times.ka_uniform = uni ? (xdefer ? 2 : 1) : 0;
+  if (mask)
+    c.times.ks_bytes_per_row = uni ? (xdefer ? 44 : 48) : 88;  // cg_bytes_per_row (bench.py)
+  else
+    c.times.ka_uniform = uni ? (xdefer ? 2 : 1) : 0;
   CgResult res;
   res.reports.resize(ctl.size());
   for (std::size_t k = 0; k < ctl.size(); ++k) {

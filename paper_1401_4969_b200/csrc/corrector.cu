@@ -832,6 +832,7 @@ Ctx::~Ctx() {
   ws.reset();
   levels.clear();
   for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  if (input_ready) cudaEventDestroy(input_ready);
   if (solver) cusolverDnDestroy(solver);
   if (stream) cudaStreamDestroy(stream);
 }

@@ -249,6 +249,14 @@ struct StepTimes {
   long long kernel_launches = 0;
   int ka_uniform = 0;  // the CG ran the constant-coefficient (no stencil stream) variant
   long long launch_base = 0;  // launch_counter() at the start of the step
+  // strip-solve CG kernel (profiling on): every launch timed; algorithmic work =
+  // sum over strip systems of unknowns x CG updates (host count, check sweeps excluded)
+  double ks_ms = 0;
+  long long ks_launches = 0;
+  double ks_row_iters = 0;
+  int ks_kernel = 0;  // strip batch CG kernel: 0 k_cg_iter, 1 k_cg_persist, 2 k_cg_resident
+  int ka_kernel = 0;  // the same for the local batch
+  int ks_bytes_per_row = 0;  // algorithmic bytes per unknown and CG update of that kernel
 };
 
 struct SolveReport {
@@ -322,6 +330,17 @@ class Ctx {
   }
   bool profile = false;  // record CUDA events around the local-solve SpMV kernel
   StepTimes times;
+  // Stream whose prior work the *_device entry points wait for before reading
+  // caller-owned device memory (mlg_set_input_stream; 0 = legacy default stream).
+  cudaStream_t input_stream = nullptr;
+  // k_assemble of the most recent level built with profiling on (CUDA events)
+  double asm_ms = 0, asm_dofs = 0;
+  cudaEvent_t input_ready = nullptr;
+  void order_after_input() {
+    if (!input_ready) MLG_CUDA(cudaEventCreateWithFlags(&input_ready, cudaEventDisableTiming));
+    MLG_CUDA(cudaEventRecord(input_ready, input_stream));
+    MLG_CUDA(cudaStreamWaitEvent(stream, input_ready, 0));
+  }
 };
 
 }  // namespace mlg
