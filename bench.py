@@ -67,6 +67,11 @@ FALLBACK_HBM = 6650.0
 # the cell): 80 B per dof.
 ASSEMBLE_BYTES_PER_DOF = 80
 KERNEL_NAMES = {0: "k_cg_iter", 1: "k_cg_persist", 2: "k_cg_resident"}
+# what bounds each CG kernel: k_cg_iter streams every iterate from HBM; the
+# persistent kernel keeps a batch in L2 (ncu: DRAM << algorithmic bytes); the
+# resident kernel keeps it in registers + shared memory (72 B of shared-memory
+# traffic per point and iteration, no HBM)
+BOUNDS = {0: "hbm", 1: "l2", 2: "smem"}
 
 
 def cg_bytes_per_row(uniform=0):
@@ -78,8 +83,10 @@ def cg_bytes_per_row(uniform=0):
     pairs -- one launch moves r, p (32 B), the next r, p, x and the deferred
     update's p (56 B): 44 B/row per launch of a sampled pair.  Stencil
     neighbours come from registers and warp shuffles, so nothing else is
-    re-read.  Returns (update, check)."""
-    return {0: (88, 64), 1: (48, 24), 2: (44, 24)}[int(uniform)]
+    re-read.  uniform == 3: the SM-resident kernel (k_cg_resident), whose
+    iterates never leave the chip: 72 B of SHARED-MEMORY traffic per point and
+    iteration (p, x load+store; five p loads for A p).  Returns (update, check)."""
+    return {0: (88, 64), 1: (48, 24), 2: (44, 24), 3: (72, 0)}[int(uniform)]
 
 
 # ----------------------------------------------------------------- helpers ---
@@ -485,7 +492,7 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
         # per-iteration launches stream every iterate from HBM; the persistent
         # kernel keeps the batch in L2 (ncu: DRAM << algorithmic bytes)
         rl["local"] = _roofline(
-            kname, "hbm" if kk == 0 else "l2", ka_bytes / (ka_ms * 1e-3) / 1e9, "local",
+            kname, BOUNDS[kk], ka_bytes / (ka_ms * 1e-3) / 1e9, "local",
             workload, (ka_rows + ka_chk) / ka_n, ka_ms / ka_n, int(ka_n), int(ka_all),
             ka_ms / ka_n * ka_all * 1e-3 / tstep, bpr,
             {"bytes_per_check_row": bpc, "uniform_stencil": int(tims[-1].spmv_uniform_stencil),
@@ -499,7 +506,7 @@ def run_ours(args, ws, rank, local, workload, steps, warmup, with_e2e=True, prof
         bpr = tims[-1].strip_bytes_per_row
         sk = tims[-1].strip_kernel
         rl["strip"] = _roofline(
-            KERNEL_NAMES[sk], "hbm" if sk == 0 else "l2", ks_ri * bpr / (ks_ms * 1e-3) / 1e9,
+            KERNEL_NAMES[sk], BOUNDS[sk], ks_ri * bpr / (ks_ms * 1e-3) / 1e9,
             "strip", workload, ks_ri / ks_n, ks_ms / ks_n, int(ks_n), int(ks_n),
             ks_ms * 1e-3 / tstep, bpr,
             {"what": "strip-solve Jacobi-PCG over the masked strip window "

@@ -112,8 +112,8 @@ typedef struct mlg_step_timings {
   int strip_kernel;        /* CG kernel of the strip batch: 0 k_cg_iter (one launch per
                               iteration), 1 k_cg_persist (one cooperative launch per
                               solve), 2 k_cg_resident (iterates resident on chip) */
-  int local_kernel;        /* the same for the local-solve batch */
   int strip_bytes_per_row; /* algorithmic bytes per unknown and CG update of that kernel */
+  int local_kernel;        /* the CG kernel of the local-solve batch (same codes) */
 } mlg_step_timings;
 
 const char* mlg_last_error(void);

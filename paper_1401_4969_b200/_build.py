@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libmlg_b200.so"
-SOURCES = ["mesh.cu", "assemble.cu", "p2.cu", "cg.cu", "cg_p2.cu", "corrector.cu", "errors.cu", "capi.cu",
+SOURCES = ["mesh.cu", "assemble.cu", "p2.cu", "cg.cu", "cg_resident.cu", "cg_p2.cu", "corrector.cu", "errors.cu", "capi.cu",
            "harness.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

@@ -38,6 +38,7 @@
 #include <type_traits>
 
 #include "cg.cuh"
+#include "cg_ctl.cuh"
 #include "stencil.cuh"
 
 namespace mlg {
@@ -903,82 +904,6 @@ __device__ __forceinline__ void sweep_async(const CgSys& S, const SweepArgs& A, 
 
 
 
-enum Phase { kPhaseInit = 0, kPhaseIter = 1 };
-
-// Scalar recurrences of cg_solve for one system after a launch's reduction.
-template <int PH>
-__device__ __forceinline__ void update_ctl(CgCtl& c, const double (&a)[kCgDots], double tol,
-                                           int maxit, int xdefer = 0) {
-  if (PH == kPhaseInit) {
-    c.bnorm = sqrt(a[0]);
-    c.iters = 0;
-    c.alpha = c.beta = c.rho = 0.0;
-    c.alpha_prev = 0.0;
-    c.xphase = 0;
-    c.restart = 1;
-    if (c.bnorm == 0.0) {  // sparse.cpp:208-212
-      c.status = kConverged;
-      c.final_res = 0.0;
-      c.mode = kModeSkip;
-    } else {
-      c.status = kRunning;
-      c.mode = kModeNormal;
-    }
-    return;
-  }
-  if (c.mode == kModeFlush) {  // the deferred x update is applied: x is current
-    c.xphase = 0;
-    c.mode = kModeCheck;
-    return;
-  }
-  if (c.mode == kModeNormal) {
-    const bool updated = !c.restart;
-    if (updated) c.iters += 1;
-    if (updated && xdefer) {  // this launch deferred (phase 0) or caught up (phase 1)
-      if (c.xphase == 0) {
-        c.alpha_prev = c.alpha;
-        c.xphase = 1;
-      } else {
-        c.xphase = 0;
-      }
-    }
-    if (updated && (sqrt(a[0]) <= tol * c.bnorm || c.iters >= maxit)) {
-      // confirm with the true residual (sparse.cpp:232-246), once x is current
-      c.mode = c.xphase ? kModeFlush : kModeCheck;
-      return;
-    }
-    const double pq = a[2];
-    if (pq <= 0.0) {  // sparse.cpp:225-226
-      c.status = kIndefinite;
-      c.mode = kModeSkip;
-      return;
-    }
-    const double rho = a[1];
-    const double alpha = rho / pq;
-    const double rho_next = rho - 2.0 * alpha * a[3] + alpha * alpha * a[4];
-    c.alpha = alpha;
-    c.beta = rho_next / rho;
-    c.rho = rho;
-    c.restart = 0;
-  } else if (c.mode == kModeCheck) {
-    const double true_rel = sqrt(a[0]) / c.bnorm;
-    if (true_rel <= tol) {
-      c.status = kConverged;
-      c.final_res = true_rel;
-      c.mode = kModeSkip;
-    } else if (c.iters >= maxit) {
-      c.status = kNotConverged;  // sparse.cpp:255-257
-      c.final_res = true_rel;
-      c.mode = kModeSkip;
-    } else {  // restart from the true residual: p = z, no pending update
-      c.restart = 1;
-      c.alpha = c.beta = 0.0;
-      c.xphase = 0;
-      c.mode = kModeNormal;
-    }
-  }
-}
-
 struct Finish {
   double* part;
   unsigned* counter;
@@ -1542,6 +1467,43 @@ int resident_persist() {
   return res;
 }
 
+// Unknowns of a window system: the window's lattice points minus those in a
+// closed G_j (strip systems) or in the hole -- the size n of the reference's
+// extracted system, so maxit = 10 n (sparse.cpp:204) matches.  Per row the
+// excluded points are a union of at most side + 1 intervals.
+int system_points(const StripGeom& g, bool strip, const CgSys& s) {
+  long long n = 0;
+  std::vector<std::pair<int, int>> iv;
+  for (int y = s.y0; y < s.y0 + s.h; ++y) {
+    iv.clear();
+    if (strip) {
+      const int by = std::min(y / (g.bh * g.scale), g.side - 1);
+      const int y0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+      const int y1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+      if (y >= y0 && y <= y1)
+        for (int bx = 0; bx < g.side; ++bx) {
+          const int x0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+          const int x1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+          iv.emplace_back(x0, x1);
+        }
+    }
+    if (y >= g.hy0 && y <= g.hy1 && g.hx1 >= g.hx0) iv.emplace_back(g.hx0, g.hx1);
+    std::sort(iv.begin(), iv.end());
+    long long excl = 0;
+    int cur = s.x0 - 1;  // last excluded column counted
+    for (const auto& q : iv) {
+      const int a = std::max(q.first, std::max(cur + 1, s.x0));
+      const int b = std::min(q.second, s.x0 + s.w - 1);
+      if (b >= a) {
+        excl += b - a + 1;
+        cur = b;
+      }
+    }
+    n += s.w - excl;
+  }
+  return static_cast<int>(n);
+}
+
 SweepArgs sweep_args(const Level& L, const unsigned char* mask) {
   SweepArgs A{};
   // domains with a hole: the interior-restricted operator (identity rows on
@@ -1695,7 +1657,7 @@ void CgBatch::setup(Ctx& c, const Level& lev, std::vector<CgSys> systems,
   }
   const int krows = s_krows;
   for (CgSys& s : systems) {
-    s.nrows = s.w * s.h;
+    s.nrows = system_points(lev.strip_geom, mask_ != nullptr, s);
     s.krows = krows;
     s.nstrips = std::max(1, (s.w + kCgCols - 1) / kCgCols);
     s.nrb = std::max(1, (s.h + krows - 1) / krows);
@@ -1844,6 +1806,10 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
   if (maxit_override > 0) {
     for (CgSys& s : sys_h) s.maxit = maxit_override;
     sys_d.upload(sys_h.data(), sys_h.size(), c.stream);
+  }
+  {  // batches that fit on chip: one SM-resident launch (cg_resident.cu)
+    CgResult rr;
+    if (solve_resident(c, tol, rr)) return rr;
   }
   std::vector<CgTile> tiles;
   auto rebuild = [&](const std::vector<char>& active) {

@@ -30,7 +30,7 @@ struct CgSys {
   long long voff;  // first row in the pooled vectors
   int toff;        // first tile id (partials index)
   int ntiles;
-  int nrows;
+  int nrows;       // unknowns: window points minus closed G_j (strip) / hole points
   int maxit;
   int nstrips, nrb, ntasks, krows;
   int tmap_off;  // >= 0: tasks are task_map[tmap_off + i] (strip tasks with strip rows)
@@ -94,6 +94,9 @@ class CgBatch {
 
  private:
   double tile_cost(const CgTile& t, const std::vector<int>& tmap) const;
+  // SM-resident path (cg_resident.cu): every system of the batch runs with its
+  // iterates held on chip; false when the batch does not fit (caller falls back).
+  bool solve_resident(Ctx& c, double tol, CgResult& res);
   std::vector<CgTile> balance_tiles(const std::vector<CgTile>& tiles, int grid) const;
   const Level* L = nullptr;
   const unsigned char* mask = nullptr;
@@ -114,6 +117,11 @@ class CgBatch {
   DevBuf<unsigned> gsync;  // grid barrier (count, generation) of the persistent kernel
   DevBuf<int> active_d;    // systems still running  // rows swept by the sampled (profiled) launches
   DevBuf<double> X, R0, R1, P0, P1, part;
+  // resident path: lane system lists, per-lane barrier counters, partial sums
+  // and boundary-row exchange buffers
+  DevBuf<int> res_lanes;
+  DevBuf<unsigned> res_bar;
+  DevBuf<double> res_part, res_halo, res_bslab;
 };
 
 }  // namespace mlg

@@ -1,0 +1,612 @@
+// SM-resident batched Jacobi-PCG: the reference's cg_solve (sparse.cpp:199-258)
+// for every system of a CgBatch, with each system's iterates held ON CHIP for
+// the whole solve instead of being streamed from HBM/L2 every iteration.
+//
+// Layout.  One cooperative launch, one 512-thread CTA per SM.  The CTAs are
+// grouped into `lanes` of C CTAs; a lane solves its list of systems one after
+// another.  A system (lattice window w x h, row pitch w + 1 with a zero pad
+// column) is cut into C horizontal slabs of R = ceil(h / C) rows; CTA i of the
+// lane owns slab rows [iR, min((i+1)R, h)).  Point j of a slab (row-major over
+// the pitched rows) belongs to thread j mod 512, register slot j / 512:
+//   registers   r, q = A p                 (24 points per thread: 96 registers)
+//   shared mem  p with one ghost row above and below the slab, and x.
+//
+// One iteration (the one-reduction rearrangement of cg.cu, same scalars via
+// update_ctl): phase 1, pointwise, applies the pending update and forms the new
+// direction  r -= a q; x += a p; z = D^-1 r; p = z + b p  for the slab rows AND
+// recomputes p for the two ghost rows from the neighbours' published boundary
+// rows (r, q, p) -- bitwise the values the neighbours compute for those rows,
+// same operations in the same order; phase 2 computes q = A p from shared
+// memory and the five dot products r.r, r.z, p.q, q.z, q.D^-1q, then publishes
+// the slab's first and last rows.  The partial sums of the lane's C CTAs meet
+// at ONE lane barrier per iteration (monotonic counter in L2); every CTA sums
+// the C partials in the same fixed order and runs update_ctl itself, so the
+// scalars are identical everywhere and run-to-run deterministic.  The true
+// residual check (sparse.cpp:232-246) exchanges the boundary rows of x and
+// evaluates b - A x from shared memory.
+//
+// Traffic per point and iteration: shared memory 72 B (phase 1 loads/stores p
+// and x, phase 2 loads five p values), no HBM; L2 carries only the boundary
+// rows (3 doubles per slab column and side) and the partial sums.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+#include <vector>
+
+#include "cg.cuh"
+#include "cg_ctl.cuh"
+
+namespace mlg {
+namespace {
+
+#ifndef MLG_RES_PT
+#define MLG_RES_PT 24
+#endif
+constexpr int kResT = 512;          // threads per CTA
+constexpr int kResPT = MLG_RES_PT;  // points per thread (registers r, q)
+constexpr int kResCap = kResT * kResPT;
+constexpr int kPartStride = 8;  // doubles per partial-sum slot
+constexpr unsigned kFullMask = 0xffffffffu;
+
+struct ResArgs {
+  const CgSys* sys;
+  const int* lanes;  // [nlanes][per_lane] system ids, -1 terminated
+  int per_lane, C, nlanes;
+  const double* bsrc;
+  int bstride, nxp1;
+  double* X;
+  CgCtl* ctl;
+  double* part;   // [nlanes][2][C][kPartStride]
+  double* halo;   // [nlanes][2][C][2 sides][3 (r, q, p)][hpitch]
+  int hpitch;
+  double* bslab;  // [2][gridDim.x][kResCap]: slab right-hand sides, true-residual scratch
+  unsigned* bar;  // [nlanes * 32] (one 128-byte line per lane)
+  StripGeom sg;
+  int masked;     // strip systems: points of the closed G_j are outside
+  double tol;
+  Stencil ust;
+  double udinv;
+  unsigned long long* trace;  // MLG_RES_TRACE: per-CTA cycle sums of the iteration phases
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Lane barrier number `epoch` (0-based): every CTA of the lane has arrived
+// after its own epoch-th arrival.  All prior global writes of the CTA are
+// visible to every CTA that passes it.
+__device__ __forceinline__ void lane_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire(bar) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool point_in_system(const ResArgs& A, const CgSys& S, int gx,
+                                                int gy) {
+  if (A.masked) {  // strip membership (cg.cu in_strip): outside every closed G_j and the hole
+    const StripGeom& g = A.sg;
+    const int bx = min(gx / (g.bw * g.scale), g.side - 1);
+    const int by = min(gy / (g.bh * g.scale), g.side - 1);
+    const int x0 = (bx == 0 ? 0 : bx * g.bw + g.dc) * g.scale;
+    const int x1 = (bx == g.side - 1 ? g.nx0 : (bx + 1) * g.bw - g.dc) * g.scale;
+    const int y0 = (by == 0 ? 0 : by * g.bh + g.dc) * g.scale;
+    const int y1 = (by == g.side - 1 ? g.ny0 : (by + 1) * g.bh - g.dc) * g.scale;
+    return !(gx >= x0 && gx <= x1 && gy >= y0 && gy <= y1) && !g.in_hole(gx, gy);
+  }
+  return !A.sg.in_hole(gx, gy);
+}
+
+// Row product of the constant-coefficient stencil from the pitched shared
+// buffer (the paired form of cg.cu product_lat: same rounding as k_cg_iter).
+template <bool LAP>
+__device__ __forceinline__ double res_product(const double* P, int i, int pitch,
+                                              const Stencil& u) {
+  const double pc = P[i], pw = P[i - 1], pe = P[i + 1], ps = P[i - pitch], pn = P[i + pitch];
+  if constexpr (LAP) {
+    return fma(-1.0, pw + pe, fma(-1.0, ps + pn, 4.0 * pc));
+  } else {
+    const double psw = P[i - pitch - 1], pne = P[i + pitch + 1];
+    return fma(u.e, pw + pe, fma(u.n, ps + pn, fma(u.ne, psw + pne, u.c * pc)));
+  }
+}
+
+// Fixed-order block reduction of the five dot products into `out` (thread 0).
+__device__ __forceinline__ void res_block_sum(double (&acc)[kCgDots], double* red,
+                                              double* out) {
+#pragma unroll
+  for (int k = 0; k < kCgDots; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+    acc[k] = v;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < kCgDots; ++k) red[warp * kCgDots + k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < kCgDots) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kResT / 32; ++w) s += red[w * kCgDots + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// Sum of the lane's C partial-sum slots, in CTA order (identical in every CTA).
+__device__ __forceinline__ void res_lane_sum(const double* slots, int C, double* sred,
+                                             double (&a)[kCgDots]) {
+  // warp k (k < 5) sums quantity k: lane l takes CTAs l, l+32, ... in order,
+  // then a fixed xor tree
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < kCgDots) {
+    double v = 0.0;
+    for (int c = lane; c < C; c += 32) v += __ldcg(slots + c * kPartStride + warp);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+    if (lane == 0) sred[warp] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kCgDots; ++k) a[k] = sred[k];
+  __syncthreads();
+}
+
+template <bool LAP>
+__global__ void __launch_bounds__(kResT, 1) k_cg_resident(ResArgs A) {
+  extern __shared__ double smem[];
+  __shared__ double s_red[(kResT / 32) * kCgDots];
+  __shared__ double s_sum[8];
+  __shared__ CgCtl s_ctl;
+  const int lane_id = blockIdx.x / A.C;
+  const int ci = blockIdx.x % A.C;
+  if (lane_id >= A.nlanes) return;
+  const int t = threadIdx.x;
+  const int C = A.C;
+  unsigned* bar = A.bar + lane_id * 32;
+  unsigned epoch = 0;
+  long long tmark = clock64();
+  // (diagnostics) cycles since the previous mark, summed per CTA into slot s
+  auto mark = [&](int s) {
+    if (A.trace != nullptr && t == 0) {
+      const long long now = clock64();
+      A.trace[blockIdx.x * 8 + s] += static_cast<unsigned long long>(now - tmark);
+      tmark = now;
+    }
+  };
+  const Stencil u = A.ust;
+  const double dv = LAP ? 0.25 : A.udinv;
+  for (int li = 0; li < A.per_lane; ++li) {
+    const int sid = A.lanes[lane_id * A.per_lane + li];
+    if (sid < 0) break;
+    const CgSys& S = A.sys[sid];  // fields re-read from global where used (registers)
+    const int pitch = S.pitch;
+    const int R = (S.h + C - 1) / C;
+    const int ya = ci * R;
+    const int nr = max(min(ya + R, S.h) - ya, 0);
+    const int npts = nr * pitch;
+    const bool has_lo = nr > 0 && ci > 0;                  // neighbour slab below
+    const bool has_hi = nr > 0 && (ci + 1) * R < S.h;       // neighbour slab above
+    double* P = smem;                           // (R + 2) * pitch + 2, point (row, col) at
+    const int off = pitch + 1;                  //   off + row * pitch + col
+    double* Xs = smem + (R + 2) * pitch + 2;    // R * pitch
+    const int plen = (R + 2) * pitch + 2;
+    for (int i = t; i < plen; i += kResT) P[i] = 0.0;
+    for (int i = t; i < R * pitch; i += kResT) Xs[i] = 0.0;
+    // in-system flags of the thread's points and the slab's right-hand side
+    // (0 outside the system), gathered once into the CTA's bslab row: the
+    // register arrays below are then filled and refilled without divisions
+    double* bs = A.bslab + static_cast<long long>(blockIdx.x) * kResCap;
+    unsigned act = 0;
+#pragma unroll 1
+    for (int k = 0; k < kResPT; ++k) {
+      const int j = t + k * kResT;
+      double b = 0.0;
+      if (j < npts) {
+        const int row = j / pitch, col = j - row * pitch;
+        if (col < S.w) {
+          const int gx = S.x0 + col, gy = S.y0 + ya + row;
+          if (point_in_system(A, S, gx, gy)) {
+            act |= 1u << k;
+            b = A.bsrc[(static_cast<long long>(gy) * A.nxp1 + gx) * A.bstride + S.rhs];
+          }
+        }
+        bs[j] = b;
+      }
+    }
+    double r[kResPT], q[kResPT];
+#pragma unroll
+    for (int k = 0; k < kResPT; ++k) {
+      const int j = t + k * kResT;
+      r[k] = (act >> k & 1u) ? bs[j] : 0.0;
+      q[k] = 0.0;
+    }
+    double* part_base = A.part + static_cast<long long>(lane_id) * 2 * C * kPartStride;
+    double* halo_base = A.halo + static_cast<long long>(lane_id) * 2 * C * 6 * A.hpitch;
+    auto halo_row = [&](int par, int cta, int side, int field) {
+      return halo_base + ((static_cast<long long>(par) * C + cta) * 6 + side * 3 + field) *
+                             A.hpitch;
+    };
+    // publish the slab's first (side 0) and last (side 1) rows: (r, q, p)
+    auto publish = [&](int par) {
+#pragma unroll
+      for (int k = 0; k < kResPT; ++k) {
+        const int j = t + k * kResT;
+        if (j < npts) {
+          const double pv = P[off + j];
+          if (j < pitch) {
+            halo_row(par, ci, 0, 0)[j] = r[k];
+            halo_row(par, ci, 0, 1)[j] = q[k];
+            halo_row(par, ci, 0, 2)[j] = pv;
+          }
+          if (j >= npts - pitch) {
+            const int c = j - (npts - pitch);
+            halo_row(par, ci, 1, 0)[c] = r[k];
+            halo_row(par, ci, 1, 1)[c] = q[k];
+            halo_row(par, ci, 1, 2)[c] = pv;
+          }
+        }
+      }
+    };
+    double acc[kCgDots];
+#pragma unroll
+    for (int k = 0; k < kCgDots; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < kResPT; ++k) acc[0] += r[k] * r[k];
+    __syncthreads();  // P, Xs zeroed
+    publish(epoch & 1);
+    res_block_sum(acc, s_red, part_base + ((epoch & 1) * C + ci) * kPartStride);
+    lane_barrier(bar, C * (epoch + 1));
+    {
+      double a[kCgDots];
+      res_lane_sum(part_base + (epoch & 1) * C * kPartStride, C, s_sum, a);
+      if (t == 0) {
+        CgCtl c{};
+        update_ctl<kPhaseInit>(c, a, A.tol, S.maxit);
+        s_ctl = c;
+      }
+    }
+    ++epoch;
+    __syncthreads();
+    while (true) {
+      // only the scalars this iteration needs (the full CgCtl would hold ~16
+      // registers through the unrolled loops)
+      if (s_ctl.status != kRunning) break;
+#pragma unroll
+      for (int k = 0; k < kCgDots; ++k) acc[k] = 0.0;
+      const int par_prev = (epoch + 1) & 1;  // buffers of the previous barrier
+      if (s_ctl.mode == kModeNormal) {
+        const bool rst = s_ctl.restart != 0;
+        const double al = rst ? 0.0 : s_ctl.alpha;
+        const double be = rst ? 0.0 : s_ctl.beta;
+        // phase 1: own points
+#pragma unroll
+        for (int k = 0; k < kResPT; ++k) {
+          const int j = t + k * kResT;
+          if (act >> k & 1u) {
+            const double po = P[off + j];
+            const double rn = fma(-al, q[k], r[k]);
+            Xs[j] = fma(al, po, Xs[j]);
+            const double tz = __dmul_rn(dv, rn);
+            P[off + j] = fma(be, po, tz);
+            r[k] = rn;
+          }
+        }
+        // phase 1: ghost rows from the neighbours' boundary rows (same ops)
+        if (has_lo || has_hi) {
+          for (int i = t; i < 2 * pitch; i += kResT) {
+            const int side = i >= pitch;  // 0: row -1 (from ci-1's last row), 1: row nr
+            const int col = i - side * pitch;
+            if (side ? !has_hi : !has_lo) continue;
+            const int src = side ? ci + 1 : ci - 1;
+            const int srow = side ? 0 : 1;
+            const double rg = __ldcg(halo_row(par_prev, src, srow, 0) + col);
+            const double qg = __ldcg(halo_row(par_prev, src, srow, 1) + col);
+            const double pg = __ldcg(halo_row(par_prev, src, srow, 2) + col);
+            const double rn = fma(-al, qg, rg);
+            const double tz = __dmul_rn(dv, rn);
+            P[side ? off + nr * pitch + col : off - pitch + col] = fma(be, pg, tz);
+          }
+        }
+        __syncthreads();
+        mark(0);
+        // phase 2: q = A p, dot products
+#pragma unroll
+        for (int k = 0; k < kResPT; ++k) {
+          const int j = t + k * kResT;
+          if (act >> k & 1u) {
+            const double qq = res_product<LAP>(P, off + j, pitch, u);
+            const double pv = P[off + j];
+            const double tz = __dmul_rn(dv, r[k]);
+            q[k] = qq;
+            acc[0] += r[k] * r[k];
+            acc[1] += r[k] * tz;
+            acc[2] += pv * qq;
+            acc[3] += qq * tz;
+            acc[4] += qq * __dmul_rn(dv, qq);
+          }
+        }
+      } else {  // kModeCheck: r = b - A x (sparse.cpp:232-246)
+        const int par = epoch & 1;
+        // exchange the boundary rows of x (field 2 of the halo rows)
+#pragma unroll
+        for (int k = 0; k < kResPT; ++k) {
+          const int j = t + k * kResT;
+          if (j < npts) {
+            if (j < pitch) halo_row(par, ci, 0, 2)[j] = Xs[j];
+            if (j >= npts - pitch) halo_row(par, ci, 1, 2)[j - (npts - pitch)] = Xs[j];
+          }
+        }
+        lane_barrier(bar, C * (epoch + 1));
+        ++epoch;
+        for (int i = t; i < 2 * pitch; i += kResT) {
+          const int side = i >= pitch;
+          const int col = i - side * pitch;
+          if (side ? !has_hi : !has_lo) continue;
+          const int src = side ? ci + 1 : ci - 1;
+          const double xg = __ldcg(halo_row(par, src, side ? 0 : 1, 2) + col);
+          P[side ? off + nr * pitch + col : off - pitch + col] = xg;
+        }
+        for (int j = t; j < npts; j += kResT) P[off + j] = Xs[j];
+        __syncthreads();
+        // (rolled loop through the CTA's scratch row: no register arrays live
+        // in this rarely taken branch)
+        double* rt = bs + static_cast<long long>(gridDim.x) * kResCap;  // 2nd half of bslab
+#pragma unroll 1
+        for (int k = 0; k < kResPT; ++k) {
+          const int j = t + k * kResT;
+          if (act >> k & 1u) {
+            const double ax = res_product<LAP>(P, off + j, pitch, u);
+            const double v = __dsub_rn(bs[j], ax);
+            rt[j] = v;
+            acc[0] += v * v;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kResPT; ++k) {
+          const int j = t + k * kResT;
+          r[k] = (act >> k & 1u) ? rt[j] : 0.0;
+          q[k] = 0.0;
+        }
+        __syncthreads();  // P (holding x) is read by phase 1 of a restart only as 0 * p
+      }
+      publish(epoch & 1);
+      res_block_sum(acc, s_red, part_base + ((epoch & 1) * C + ci) * kPartStride);
+      mark(1);
+      lane_barrier(bar, C * (epoch + 1));
+      mark(2);
+      double a[kCgDots];
+      res_lane_sum(part_base + (epoch & 1) * C * kPartStride, C, s_sum, a);
+      ++epoch;
+      if (t == 0) {
+        CgCtl cc = s_ctl;
+        update_ctl<kPhaseIter>(cc, a, A.tol, __ldg(&A.sys[sid].maxit));
+        s_ctl = cc;
+      }
+      __syncthreads();
+      mark(3);
+      if (A.trace != nullptr && t == 0) A.trace[blockIdx.x * 8 + 7] += 1;
+    }
+    // x of the slab -> pooled output (cg_index layout)
+    for (int j = t; j < npts; j += kResT) {
+      const int row = j / pitch, col = j - row * pitch;
+      if (col < S.w) A.X[cg_index(S, ya + row, col)] = Xs[j];
+    }
+    if (ci == 0 && t == 0) A.ctl[sid] = s_ctl;
+    __syncthreads();  // shared memory is reused by the next system
+  }
+}
+
+}  // namespace
+
+// Host plan: CTAs per lane C and the system -> lane assignment.  Every system
+// must fit: ceil(h / C) rows x pitch points per CTA (<= kResCap) plus the
+// shared buffers (p with ghost rows, x).  Among the feasible C the plan with
+// the smallest estimated makespan wins: a lane's time is the sum over its
+// systems of iterations (~ proportional to the window's larger side) x
+// per-iteration cost (a fixed barrier/reduction latency + the slab's points).
+bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
+  static const int env = [] {
+    const char* e = std::getenv("MLG_CG_RESIDENT");  // A/B hook: 0 disables
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!env || L->uniform == 0 || sys_h.empty()) return false;
+  int dev = 0, nsm = 0, smem_optin = 0;
+  MLG_CUDA(cudaGetDevice(&dev));
+  MLG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  MLG_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int static_smem = 4096;  // s_red, s_sum, s_ctl (+ margin)
+  const int nsys = static_cast<int>(sys_h.size());
+  int max_pitch = 1, max_h = 1;
+  for (const CgSys& s : sys_h) {
+    max_pitch = std::max(max_pitch, s.pitch);
+    max_h = std::max(max_h, s.h);
+  }
+  auto smem_for = [&](int C) {
+    long long worst = 0;
+    for (const CgSys& s : sys_h) {
+      const long long R = (s.h + C - 1) / C;
+      worst = std::max(worst, ((R + 2) * s.pitch + 2 + R * s.pitch) * 8);
+    }
+    return worst;
+  };
+  auto fits = [&](int C) {
+    for (const CgSys& s : sys_h) {
+      const long long R = (s.h + C - 1) / C;
+      if (R * s.pitch > kResCap) return false;
+    }
+    return smem_for(C) + static_smem <= smem_optin;
+  };
+  // per-iteration cost model (microseconds): barrier + reduction latency plus
+  // the slab's points at ~0.33 ns each (72 B of shared-memory traffic per point)
+  auto iter_cost = [&](const CgSys& s, int C) {
+    const double R = (s.h + C - 1) / C;
+    return 2.0 + R * s.pitch * 0.33e-3;
+  };
+  double best = 1e300;
+  int bestC = 0;
+  std::vector<std::vector<int>> best_lanes;
+  std::vector<int> order(static_cast<std::size_t>(nsys));
+  std::iota(order.begin(), order.end(), 0);
+  for (int C = 1; C <= nsm; ++C) {
+    if (!fits(C)) continue;
+    const int nl = nsm / C;
+    if (nl < 1) break;
+    // LPT: systems by decreasing cost to the least-loaded lane
+    std::vector<double> cost(static_cast<std::size_t>(nsys));
+    for (int s = 0; s < nsys; ++s) {
+      const CgSys& S = sys_h[static_cast<std::size_t>(s)];
+      cost[static_cast<std::size_t>(s)] = std::max(S.w, S.h) * iter_cost(S, C);
+    }
+    std::vector<int> ord = order;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+      return cost[static_cast<std::size_t>(a)] > cost[static_cast<std::size_t>(b)];
+    });
+    std::vector<double> load(static_cast<std::size_t>(nl), 0.0);
+    std::vector<std::vector<int>> lanes(static_cast<std::size_t>(nl));
+    for (int s : ord) {
+      const auto it = std::min_element(load.begin(), load.end());
+      const std::size_t l = static_cast<std::size_t>(it - load.begin());
+      lanes[l].push_back(s);
+      load[l] += cost[static_cast<std::size_t>(s)];
+    }
+    const double span = *std::max_element(load.begin(), load.end());
+    if (span < best * 0.999) {
+      best = span;
+      bestC = C;
+      best_lanes = lanes;
+    }
+  }
+  if (bestC == 0) return false;
+  const int C = bestC;
+  while (!best_lanes.empty() && best_lanes.back().empty()) best_lanes.pop_back();
+  const int nl = static_cast<int>(best_lanes.size());
+  std::size_t per = 1;
+  for (const auto& l : best_lanes) per = std::max(per, l.size() + 1);
+  std::vector<int> lanes_h(static_cast<std::size_t>(nl) * per, -1);
+  for (int l = 0; l < nl; ++l)
+    for (std::size_t k = 0; k < best_lanes[static_cast<std::size_t>(l)].size(); ++k)
+      lanes_h[static_cast<std::size_t>(l) * per + k] = best_lanes[static_cast<std::size_t>(l)][k];
+  cudaStream_t st = c.stream;
+  res_lanes.ensure(lanes_h.size());
+  res_lanes.upload(lanes_h.data(), lanes_h.size(), st);
+  res_bar.ensure(static_cast<std::size_t>(nl) * 32);
+  res_bar.zero(st);
+  res_part.ensure(static_cast<std::size_t>(nl) * 2 * C * kPartStride);
+  res_halo.ensure(static_cast<std::size_t>(nl) * 2 * C * 6 * max_pitch);
+  res_bslab.ensure(static_cast<std::size_t>(2) * nl * C * kResCap);
+  ctl_d.zero(st);
+
+  ResArgs A{};
+  A.sys = sys_d.get();
+  A.lanes = res_lanes.get();
+  A.per_lane = static_cast<int>(per);
+  A.C = C;
+  A.nlanes = nl;
+  A.bsrc = bsrc;
+  A.bstride = bstride;
+  A.nxp1 = L->nx + 1;
+  A.X = X.get();
+  A.ctl = ctl_d.get();
+  A.part = res_part.get();
+  A.halo = res_halo.get();
+  A.hpitch = max_pitch;
+  A.bslab = res_bslab.get();
+  A.bar = res_bar.get();
+  A.sg = L->strip_geom;
+  A.masked = mask != nullptr;
+  A.tol = tol;
+  A.ust = L->ust;
+  A.udinv = L->udinv;
+  static const bool trace_on = std::getenv("MLG_RES_TRACE") != nullptr;
+  DevBuf<unsigned long long> trace_buf;
+  if (trace_on) {
+    trace_buf.alloc(static_cast<std::size_t>(nl) * C * 8);
+    trace_buf.zero(st);
+    A.trace = trace_buf.get();
+  }
+  const bool lap = L->ust.c == 4.0 && L->ust.e == -1.0 && L->ust.n == -1.0 &&
+                   L->ust.ne == 0.0 && L->udinv == 0.25;
+  const void* fn = lap ? reinterpret_cast<const void*>(&k_cg_resident<true>)
+                       : reinterpret_cast<const void*>(&k_cg_resident<false>);
+  const int dyn = static_cast<int>(smem_for(C));
+  MLG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  int per_sm = 0;
+  MLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kResT, dyn));
+  if (per_sm * nsm < nl * C) return false;  // cooperative launch needs co-residency
+  const bool prof = c.profile;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof) {
+    e0 = c.event(0);
+    e1 = c.event(1);
+    MLG_CUDA(cudaEventRecord(e0, st));
+  }
+  void* args[] = {(void*)&A};
+  MLG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nl * C), dim3(kResT), args, dyn, st));
+  ++launch_counter();
+  if (prof) MLG_CUDA(cudaEventRecord(e1, st));
+  std::vector<CgCtl> ctl(static_cast<std::size_t>(nsys));
+  ctl_d.download(ctl.data(), ctl.size(), st);
+  c.sync();
+  if (trace_on) {
+    std::vector<unsigned long long> tr(static_cast<std::size_t>(nl) * C * 8);
+    trace_buf.download(tr.data(), tr.size(), st);
+    c.sync();
+    double sum[8] = {0}, mx[8] = {0};
+    for (int b = 0; b < nl * C; ++b)
+      for (int k = 0; k < 8; ++k) {
+        sum[k] += static_cast<double>(tr[static_cast<std::size_t>(b) * 8 + k]);
+        mx[k] = std::max(mx[k], static_cast<double>(tr[static_cast<std::size_t>(b) * 8 + k]));
+      }
+    const double it = std::max(1.0, sum[7] / (nl * C));
+    fprintf(stderr,
+            "resident trace: %d lanes x %d CTAs, %d systems, %s, %.0f iterations/CTA; cycles per "
+            "iteration (mean over CTAs): phase1+ghost %.0f, phase2+publish+blocksum %.0f, "
+            "barrier wait %.0f, lane sum+ctl %.0f\n",
+            nl, C, nsys, mask ? "strip" : "local", it, sum[0] / (nl * C) / it,
+            sum[1] / (nl * C) / it, sum[2] / (nl * C) / it, sum[3] / (nl * C) / it);
+  }
+  for (const CgCtl& q : ctl)
+    if (q.status == kIndefinite)
+      throw SolverError("cg_solve: matrix is not positive definite (p'Mp <= 0)");
+  res.reports.assign(ctl.size(), SolveReport{});
+  res.iters_max = 0;
+  double row_iters = 0.0;
+  for (std::size_t k = 0; k < ctl.size(); ++k) {
+    res.reports[k].iterations = ctl[k].iters;
+    res.reports[k].final_residual = ctl[k].final_res;
+    res.reports[k].converged = ctl[k].status == kConverged ? 1 : 0;
+    res.iters_max = std::max(res.iters_max, ctl[k].iters);
+    row_iters += static_cast<double>(sys_h[k].nrows) * ctl[k].iters;
+  }
+  if (prof) {
+    float ms = 0.f;
+    MLG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (mask) {
+      c.times.ks_ms += ms;
+      c.times.ks_launches += 1;
+      c.times.ks_row_iters += row_iters;
+      c.times.ks_bytes_per_row = 72;
+    } else {
+      c.times.ka_ms_sum += ms;
+      c.times.ka_launches += 1;
+      c.times.ka_launches_all += 1;
+      c.times.ka_rows += row_iters;
+      c.times.ka_uniform = 3;
+    }
+  }
+  (mask ? c.times.ks_kernel : c.times.ka_kernel) = 2;
+  return true;
+}
+
+}  // namespace mlg

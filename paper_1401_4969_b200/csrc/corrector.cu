@@ -297,7 +297,7 @@ __global__ void k_strip_scatter(int nx, int nev, const CgSys* sys, const unsigne
                                 const double* X, double* glued) {
   const CgSys S0 = sys[0];
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (i >= S0.nrows) return;
+  if (i >= static_cast<long long>(S0.w) * S0.h) return;  // every window point (nrows = strip unknowns)
   const int ly = static_cast<int>(i / S0.w), lx = static_cast<int>(i % S0.w);
   const long long d = static_cast<long long>(S0.y0 + ly) * (nx + 1) + (S0.x0 + lx);
   if (!mask[d]) return;

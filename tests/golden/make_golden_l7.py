@@ -4,6 +4,7 @@ through the compiled reference (oracle/_ref = /root/reference/proj/src built by
 oracle/Makefile).  TEST INFRASTRUCTURE ONLY; runs in the CPU container.
 
     python tests/golden/make_golden_l7.py run        # ~1 h on 8 cores, ~50 GB RAM
+    python tests/golden/make_golden_l7.py strip      # ~20 min: reference strip iterations
     python tests/golden/make_golden_l7.py fixtures   # cheap: writes the committed pins
 
 Stage `run` drives the same chain as multilevel_correction (corrector.cpp:414-462):
@@ -89,6 +90,57 @@ def run():
     h.close()
 
 
+def strip():
+    """Reference strip-solve iteration count at level 7 (interface_solve,
+    corrector.cpp:216-254) for eigenvector 0 from the level-6 state: the 64
+    local corrections (local_bvp_solve, run on 8 threads like parallel_tasks),
+    then the strip CG.  bench.py's reference arm scales its timed strip sample
+    by this count."""
+    import threading
+    meta = json.loads((CACHE / "c5sub_meta.json").read_text())
+    c = CFG
+    h = ref.RefHierarchy(domain=c["domain"], H=c["H"], delta=c["delta"], m=c["m"],
+                         n_levels=c["n_levels"], nev=c["nev"], workers=8)
+    h.extend_to(7)
+    h.build_region_systems(7)
+    co6 = np.load(CACHE / "c5sub_L6_coeffs.npy")
+    s6 = h.sizes(6)
+    out = {}
+    for i in (0,):
+        full = np.zeros(s6["ndofs"])
+        full.reshape(s6["ny"] + 1, s6["nx"] + 1)[1:-1, 1:-1] = co6[i].reshape(
+            s6["ny"] - 1, s6["nx"] - 1)
+        u7 = h.prolong(full, 6, 7)
+        lam = meta["lambdas"][5][i]
+        corr = np.zeros((c["m"], u7.size))
+        nxt = [0]
+        lock = threading.Lock()
+
+        def work():
+            while True:
+                with lock:
+                    j = nxt[0]
+                    nxt[0] += 1
+                if j >= c["m"]:
+                    return
+                corr[j], _, _ = h.local_bvp_solve(7, j, lam, u7, 1e-10)
+        t = time.time()
+        th = [threading.Thread(target=work) for _ in range(8)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        log("corrections", i, f"{time.time() - t:.1f}s")
+        t = time.time()
+        _, its, res = h.interface_solve(7, lam, u7, corr, 1e-10)
+        log("strip", i, its, res, f"{time.time() - t:.1f}s")
+        out[str(i)] = its
+        meta["strip_iterations_L7"] = out
+        meta["strip_seconds_L7"] = time.time() - t
+        (CACHE / "c5sub_meta.json").write_text(json.dumps(meta, indent=1))
+    h.close()
+
+
 def fixtures():
     meta = json.loads((CACHE / "c5sub_meta.json").read_text())
     co = np.load(CACHE / "c5sub_L7_coeffs.npy")
@@ -100,6 +152,8 @@ def fixtures():
     out = {k: meta[k] for k in ("config", "lambdas", "matched", "timings", "step_wall_s",
                                 "generator")}
     out.update(local_iterations_L7=meta.get("local_iterations_L7", {}),
+               reference_strip_iterations_L7=list(meta.get("strip_iterations_L7", {}).values()),
+               workers=8,
                sketch={"k": SKETCH_K, "seed": SKETCH_SEED, "projections": proj.tolist(),
                        "row_norms": rn.tolist()},
                norm2=[float(v @ v) for v in co], sample_stride=SAMPLE_STRIDE,
@@ -109,4 +163,4 @@ def fixtures():
 
 
 if __name__ == "__main__":
-    {"run": run, "fixtures": fixtures}[sys.argv[1]]()
+    {"run": run, "strip": strip, "fixtures": fixtures}[sys.argv[1]]()

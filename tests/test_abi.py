@@ -48,3 +48,34 @@ def test_no_cpu_fallback_in_product():
     pkg = ROOT / "paper_1401_4969_b200"
     for f in list(pkg.glob("*.py")) + list((pkg / "csrc").glob("*")):
         assert "oracle" not in f.read_text().replace("oracle/_ref", ""), f
+
+
+def test_struct_layouts_match_ctypes(tmp_path):
+    """Every struct the header declares has the same field offsets and size in C
+    (gcc on the header) and in the ctypes mirror (_lib.py)."""
+    import ctypes as C
+
+    from paper_1401_4969_b200 import _lib
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    mirrors = {"mlg_step_timings": _lib.MlgStepTimings, "mlg_solve_report": _lib.MlgSolveReport,
+               "mlg_config": _lib.MlgConfig}
+    prog = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', 'int main(void){']
+    for cname, py in mirrors.items():
+        assert re.search(r"typedef struct " + cname + r"\b", text), cname
+        prog.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            prog.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    prog.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(prog))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                               check=True).stdout.splitlines():
+        cname, field, val = line.split()
+        got[(cname, field)] = int(val)
+    for cname, py in mirrors.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
