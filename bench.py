@@ -229,7 +229,7 @@ def reference_full_steps(wl, steps, warmup, workers):
     return dict(n_int=n, times=times, splits=splits, lam=list(lo), **info)
 
 
-def reference_sampled_steps(wl, steps, workers, strip_maxit=30):
+def reference_sampled_steps(wl, steps, workers, strip_maxit=45):
     """Bounded sample of the reference's correction step L-1 -> L for workloads
     whose full step runs for tens of minutes on the host (config 5: ~30 min on
     8 cores).  The step is one_correction_step (corrector.cpp:336-412): nev*m
@@ -238,12 +238,14 @@ def reference_sampled_steps(wl, steps, workers, strip_maxit=30):
     augmented eigensolve (:378-381).  Each sampled step times, with the
     reference's own code:
       * one wave of `workers` local_bvp_solve tasks run concurrently (the
-        worker pool's steady state), successive steps taking successive tasks;
-        local estimate = mean task time x nev*m / workers;
-      * cg_solve on the strip system capped at strip_maxit iterations
-        (ref_strip_cg_sample); strip estimate = time per iteration x the
-        reference's strip iteration count (tests/golden/golden_l7.json) -- the
-        nev strips run concurrently, so the step waits for one of them;
+        worker pool's steady state), spread over the partition; local estimate
+        = the wave's time per unit of task weight (N_j^1.5) x the weight of all
+        nev*m tasks / workers;
+      * cg_solve on the strip system capped at strip_maxit/3 and strip_maxit
+        iterations (ref_strip_cg_sample), nev of them concurrently as the worker
+        pool runs the strip tasks; the difference of the two (slowest) times
+        cancels cg_solve's set-up; strip estimate = time per iteration x the
+        reference's strip iteration count (tests/golden/golden_l7.json);
       * the augmented eigensolve once (setup) on the prolonged input.
     The sum is the estimated step time; DESIGN.md §5 checks the estimate
     against a full reference step measured in the build container."""
@@ -264,9 +266,15 @@ def reference_sampled_steps(wl, steps, workers, strip_maxit=30):
     golden = json.loads((ROOT / "tests" / "golden" / "golden_l7.json").read_text())
     strip_iters = int(max(golden["reference_strip_iterations_L7"]))
     tasks = [(i, j) for i in range(nev) for j in range(m)]
+    # a task's cost ~ its unknowns x its CG iterations ~ N_j^1.5 (iterations grow
+    # with the subdomain width): the wave's mean is rescaled to all nev*m tasks
+    wgt = {j: float(len(h.region_dofs(L, "overlap", j, zero_trace=True))) ** 1.5
+           for j in range(m)}
+    w_all = sum(wgt[j] for _, j in tasks)
     out = []
     for k in range(steps):
-        wave = [tasks[(k * workers + q) % len(tasks)] for q in range(workers)]
+        # spread the wave over the partition (stride coprime to m)
+        wave = [tasks[(k * workers + q) * 9 % len(tasks)] for q in range(workers)]
         res = [None] * len(wave)
 
         def run(q):
@@ -278,13 +286,28 @@ def reference_sampled_steps(wl, steps, workers, strip_maxit=30):
         for x in th:
             x.join()
         task_s = [r[0] for r in res]
-        local_est = statistics.mean(task_s) * len(tasks) / workers
-        sec, its = h.strip_cg_sample(L, lam_in[0], u[0], 1e-10, strip_maxit)
-        strip_est = sec / its * strip_iters
+        w_wave = sum(wgt[j] for _, j in wave)
+        local_est = sum(task_s) / w_wave * w_all / workers
+        # the nev strip solves run concurrently (one task per eigenvector): time
+        # nev concurrent capped cg_solve calls, the step waits for the slowest
+        sres = [None] * nev
+
+        def run_strip(i, mi):
+            sres[i] = h.strip_cg_sample(L, lam_in[i], u[i], 1e-10, mi)
+        per = []
+        for mi in (strip_maxit // 3, strip_maxit):  # the difference cancels set-up costs
+            th = [threading.Thread(target=run_strip, args=(i, mi)) for i in range(nev)]
+            for x in th:
+                x.start()
+            for x in th:
+                x.join()
+            per.append(max(sec for sec, _ in sres))
+        per_it = (per[1] - per[0]) / (strip_maxit - strip_maxit // 3)
+        strip_est = per_it * strip_iters
         out.append(dict(step_s=local_est + strip_est + aug_s, local_s=local_est,
                         iface_s=strip_est, aug_s=aug_s, wave_tasks=len(wave),
                         wave_mean_task_s=statistics.mean(task_s),
-                        wave_iterations=[r[1] for r in res], strip_s_per_iter=sec / its))
+                        wave_iterations=[r[1] for r in res], strip_s_per_iter=per_it))
     h.close()
     return dict(n_int=s["n_int"], samples=out, strip_iters=strip_iters, **info)
 
@@ -316,7 +339,7 @@ def run_reference(args, ws, rank):
         step_s = statistics.mean(x["step_s"] for x in r["samples"])
         sample = (f"{n_steps} sampled steps L6->L7: each one wave of {cores} concurrent "
                   f"local_bvp_solve tasks (of {wl['nev'] * wl['m']}) + cg_solve on the strip "
-                  f"system capped at 30 iterations, scaled to the reference's "
+                  f"system capped at 15 and 45 iterations, scaled to the reference's "
                   f"{r['strip_iters']} strip iterations; augmented eigensolve timed once")
         line.update(steps=n_steps, warmup=0, steps_cap="warm-up 0, at most 2 sampled steps "
                     "(a full reference step takes ~30 min at this size)",

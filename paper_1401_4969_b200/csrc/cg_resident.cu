@@ -46,6 +46,17 @@ namespace {
 #endif
 constexpr int kResT = 512;          // threads per CTA
 constexpr int kResPT = MLG_RES_PT;  // points per thread (registers r, q)
+#ifndef MLG_RES_CHUNK
+#define MLG_RES_CHUNK MLG_RES_PT
+#endif
+// The pointwise phases run their kResPT points in chunks of kChunk with a
+// scheduling fence between chunks: the loads of one chunk are hoisted and
+// overlapped, but not across chunks (no spills of the r, q register arrays).
+constexpr int kChunk = MLG_RES_CHUNK;
+static_assert(kResPT % kChunk == 0, "chunk must divide the points per thread");
+__device__ __forceinline__ void sched_fence() {
+  if constexpr (kChunk < kResPT) asm volatile("" ::: "memory");
+}
 constexpr int kResCap = kResT * kResPT;
 constexpr int kPartStride = 8;  // doubles per partial-sum slot
 constexpr unsigned kFullMask = 0xffffffffu;
@@ -291,16 +302,20 @@ __global__ void __launch_bounds__(kResT, 1) k_cg_resident(ResArgs A) {
         const double be = rst ? 0.0 : s_ctl.beta;
         // phase 1: own points
 #pragma unroll
-        for (int k = 0; k < kResPT; ++k) {
-          const int j = t + k * kResT;
-          if (act >> k & 1u) {
-            const double po = P[off + j];
-            const double rn = fma(-al, q[k], r[k]);
-            Xs[j] = fma(al, po, Xs[j]);
-            const double tz = __dmul_rn(dv, rn);
-            P[off + j] = fma(be, po, tz);
-            r[k] = rn;
+        for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
+#pragma unroll
+          for (int k = k0; k < k0 + kChunk; ++k) {
+            const int j = t + k * kResT;
+            if (act >> k & 1u) {
+              const double po = P[off + j];
+              const double rn = fma(-al, q[k], r[k]);
+              Xs[j] = fma(al, po, Xs[j]);
+              const double tz = __dmul_rn(dv, rn);
+              P[off + j] = fma(be, po, tz);
+              r[k] = rn;
+            }
           }
+          sched_fence();
         }
         // phase 1: ghost rows from the neighbours' boundary rows (same ops)
         if (has_lo || has_hi) {
@@ -322,19 +337,23 @@ __global__ void __launch_bounds__(kResT, 1) k_cg_resident(ResArgs A) {
         mark(0);
         // phase 2: q = A p, dot products
 #pragma unroll
-        for (int k = 0; k < kResPT; ++k) {
-          const int j = t + k * kResT;
-          if (act >> k & 1u) {
-            const double qq = res_product<LAP>(P, off + j, pitch, u);
-            const double pv = P[off + j];
-            const double tz = __dmul_rn(dv, r[k]);
-            q[k] = qq;
-            acc[0] += r[k] * r[k];
-            acc[1] += r[k] * tz;
-            acc[2] += pv * qq;
-            acc[3] += qq * tz;
-            acc[4] += qq * __dmul_rn(dv, qq);
+        for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
+#pragma unroll
+          for (int k = k0; k < k0 + kChunk; ++k) {
+            const int j = t + k * kResT;
+            if (act >> k & 1u) {
+              const double qq = res_product<LAP>(P, off + j, pitch, u);
+              const double pv = P[off + j];
+              const double tz = __dmul_rn(dv, r[k]);
+              q[k] = qq;
+              acc[0] += r[k] * r[k];
+              acc[1] += r[k] * tz;
+              acc[2] += pv * qq;
+              acc[3] += qq * tz;
+              acc[4] += qq * __dmul_rn(dv, qq);
+            }
           }
+          sched_fence();
         }
       } else {  // kModeCheck: r = b - A x (sparse.cpp:232-246)
         const int par = epoch & 1;
