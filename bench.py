@@ -273,8 +273,8 @@ def reference_sampled_steps(wl, steps, workers, strip_maxit=45):
     w_all = sum(wgt[j] for _, j in tasks)
     out = []
     for k in range(steps):
-        # spread the wave over the partition (stride coprime to m)
-        wave = [tasks[(k * workers + q) * 9 % len(tasks)] for q in range(workers)]
+        # spread the wave over eigenvectors and subdomains (stride coprime to nev*m)
+        wave = [tasks[(k * workers + q) * 37 % len(tasks)] for q in range(workers)]
         res = [None] * len(wave)
 
         def run(q):

@@ -44,7 +44,11 @@ namespace {
 #ifndef MLG_RES_PT
 #define MLG_RES_PT 24
 #endif
-constexpr int kResT = 512;          // threads per CTA
+#ifndef MLG_RES_T
+#define MLG_RES_T 512
+#endif
+constexpr int kResT = MLG_RES_T;     // threads per CTA
+constexpr int kResPerSM = 512 / kResT;  // co-resident CTAs per SM
 constexpr int kResPT = MLG_RES_PT;  // points per thread (registers r, q)
 #ifndef MLG_RES_CHUNK
 #define MLG_RES_CHUNK MLG_RES_PT
@@ -117,6 +121,15 @@ __device__ __forceinline__ bool point_in_system(const ResArgs& A, const CgSys& S
   return !A.sg.in_hole(gx, gy);
 }
 
+// Predicated shared-memory store (a predicate, not a branch: keeps the unrolled
+// point loops straight-line so their loads can overlap).
+__device__ __forceinline__ void sts_if(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f64 [%0], %1;\n\t}" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(p))),
+      "d"(v), "r"(static_cast<int>(pred)));  // no memory clobber: other points' loads may
+}                                              // move across (they never read this point)
+
 // Row product of the constant-coefficient stencil from the pitched shared
 // buffer (the paired form of cg.cu product_lat: same rounding as k_cg_iter).
 template <bool LAP>
@@ -134,17 +147,17 @@ __device__ __forceinline__ double res_product(const double* P, int i, int pitch,
 // Fixed-order block reduction of the five dot products into `out` (thread 0).
 __device__ __forceinline__ void res_block_sum(double (&acc)[kCgDots], double* red,
                                               double* out) {
+  // one quantity at a time (the fence keeps the five trees from being
+  // interleaved: few live registers next to the r, q arrays, no spills)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < kCgDots; ++k) {
     double v = acc[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
-    acc[k] = v;
+    if (lane == 0) red[warp * kCgDots + k] = v;
+    asm volatile("" ::: "memory");
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < kCgDots; ++k) red[warp * kCgDots + k] = acc[k];
   __syncthreads();
   if (threadIdx.x < kCgDots) {
     double s = 0.0;
@@ -174,7 +187,7 @@ __device__ __forceinline__ void res_lane_sum(const double* slots, int C, double*
 }
 
 template <bool LAP>
-__global__ void __launch_bounds__(kResT, 1) k_cg_resident(ResArgs A) {
+__global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
   extern __shared__ double smem[];
   __shared__ double s_red[(kResT / 32) * kCgDots];
   __shared__ double s_sum[8];
@@ -210,10 +223,13 @@ __global__ void __launch_bounds__(kResT, 1) k_cg_resident(ResArgs A) {
     const bool has_hi = nr > 0 && (ci + 1) * R < S.h;       // neighbour slab above
     double* P = smem;                           // (R + 2) * pitch + 2, point (row, col) at
     const int off = pitch + 1;                  //   off + row * pitch + col
-    double* Xs = smem + (R + 2) * pitch + 2;    // R * pitch
-    const int plen = (R + 2) * pitch + 2;
+    // Every slot j < kResCap of the unrolled point loops may READ P[off + j +-
+    // pitch +- 1] and Xs[j] (slots past the slab are masked, never stored), so
+    // the buffers cover the full capacity: straight-line loops, affine addresses.
+    const int plen = kResCap + 2 * pitch + 4;
+    double* Xs = smem + plen;                   // kResCap
     for (int i = t; i < plen; i += kResT) P[i] = 0.0;
-    for (int i = t; i < R * pitch; i += kResT) Xs[i] = 0.0;
+    for (int i = t; i < kResCap; i += kResT) Xs[i] = 0.0;
     // in-system flags of the thread's points and the slab's right-hand side
     // (0 outside the system), gathered once into the CTA's bslab row: the
     // register arrays below are then filled and refilled without divisions
@@ -305,15 +321,18 @@ __global__ void __launch_bounds__(kResT, 1) k_cg_resident(ResArgs A) {
         for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
 #pragma unroll
           for (int k = k0; k < k0 + kChunk; ++k) {
+            // branch-free (loads of consecutive points overlap): points of the
+            // slab outside the system hold r = q = p = 0 and stay so; slots past
+            // the slab read a valid dummy point and do not store
             const int j = t + k * kResT;
-            if (act >> k & 1u) {
-              const double po = P[off + j];
-              const double rn = fma(-al, q[k], r[k]);
-              Xs[j] = fma(al, po, Xs[j]);
-              const double tz = __dmul_rn(dv, rn);
-              P[off + j] = fma(be, po, tz);
-              r[k] = rn;
-            }
+            const bool in = j < npts;
+            const double po = P[off + j];
+            const double xo = Xs[j];
+            const double rn = fma(-al, q[k], r[k]);
+            const double tz = __dmul_rn(dv, rn);
+            sts_if(P + off + j, fma(be, po, tz), in);
+            sts_if(Xs + j, fma(al, po, xo), in);
+            r[k] = rn;
           }
           sched_fence();
         }
@@ -340,20 +359,34 @@ __global__ void __launch_bounds__(kResT, 1) k_cg_resident(ResArgs A) {
         for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
 #pragma unroll
           for (int k = k0; k < k0 + kChunk; ++k) {
+            // branch-free: q of points outside the system is forced to 0, so
+            // every dot term of such a point is an exact zero (r = p = 0 there)
             const int j = t + k * kResT;
-            if (act >> k & 1u) {
-              const double qq = res_product<LAP>(P, off + j, pitch, u);
-              const double pv = P[off + j];
+            const double qa = res_product<LAP>(P, off + j, pitch, u);
+            const double qq = (act >> k & 1u) ? qa : 0.0;
+            const double pv = P[off + j];  // finite; its term is 0 where qq is masked
+            q[k] = qq;
+            acc[0] += r[k] * r[k];
+            acc[2] += pv * qq;
+            if constexpr (LAP) {  // D^-1 = 1/4: the z terms are exact quarters (below)
+              acc[1] += qq * r[k];
+              acc[4] += qq * qq;
+            } else {
               const double tz = __dmul_rn(dv, r[k]);
-              q[k] = qq;
-              acc[0] += r[k] * r[k];
               acc[1] += r[k] * tz;
-              acc[2] += pv * qq;
               acc[3] += qq * tz;
               acc[4] += qq * __dmul_rn(dv, qq);
             }
           }
           sched_fence();
+        }
+        if constexpr (LAP) {
+          // z = r / 4 exactly, so r.z = (r.r)/4, q.z = (q.r)/4, q.D^-1q = (q.q)/4
+          // term by term (power-of-two scaling commutes with every rounding of
+          // the sums): bitwise the sums of the general formula
+          acc[3] = 0.25 * acc[1];
+          acc[1] = 0.25 * acc[0];
+          acc[4] = 0.25 * acc[4];
         }
       } else {  // kModeCheck: r = b - A x (sparse.cpp:232-246)
         const int par = epoch & 1;
@@ -444,6 +477,11 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   MLG_CUDA(cudaGetDevice(&dev));
   MLG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   MLG_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  int smem_sm = 0;
+  MLG_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  // kResPerSM CTAs share an SM's shared memory (1 KB per CTA reserved by the driver)
+  const int smem_cta = std::min(smem_optin, smem_sm / kResPerSM - 1024);
+  const int slots = nsm * kResPerSM;  // co-resident CTAs of the cooperative launch
   const int static_smem = 4096;  // s_red, s_sum, s_ctl (+ margin)
   const int nsys = static_cast<int>(sys_h.size());
   int max_pitch = 1, max_h = 1;
@@ -455,7 +493,7 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
     long long worst = 0;
     for (const CgSys& s : sys_h) {
       const long long R = (s.h + C - 1) / C;
-      worst = std::max(worst, ((R + 2) * s.pitch + 2 + R * s.pitch) * 8);
+      worst = std::max(worst, (2LL * kResCap + 2 * s.pitch + 4) * 8 + 0 * R);
     }
     return worst;
   };
@@ -464,7 +502,7 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
       const long long R = (s.h + C - 1) / C;
       if (R * s.pitch > kResCap) return false;
     }
-    return smem_for(C) + static_smem <= smem_optin;
+    return smem_for(C) + static_smem <= smem_cta;
   };
   // per-iteration cost model (microseconds): barrier + reduction latency plus
   // the slab's points at ~0.33 ns each (72 B of shared-memory traffic per point)
@@ -477,9 +515,9 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   std::vector<std::vector<int>> best_lanes;
   std::vector<int> order(static_cast<std::size_t>(nsys));
   std::iota(order.begin(), order.end(), 0);
-  for (int C = 1; C <= nsm; ++C) {
+  for (int C = 1; C <= slots; ++C) {
     if (!fits(C)) continue;
-    const int nl = nsm / C;
+    const int nl = slots / C;
     if (nl < 1) break;
     // LPT: systems by decreasing cost to the least-loaded lane
     std::vector<double> cost(static_cast<std::size_t>(nsys));
