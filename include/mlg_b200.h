@@ -229,6 +229,10 @@ int mlg_set_profiling(mlg_ctx* ctx, int on);
  * summed CUDA-event time of its operator assembly launch(es) and the dofs they
  * assembled (fespace.cpp:314-341 replaced by k_assemble). */
 int mlg_build_profile(mlg_ctx* ctx, double* assemble_ms, double* assemble_dofs);
+/* Which assembly kernel that launch was: 0 k_assemble (generic row gather),
+ * 1 k_assemble_table (translation-invariant lattice: element matrices from a
+ * six-variant table, bitwise the generic result), 2 k_assemble_var. */
+int mlg_build_profile_kernel(mlg_ctx* ctx, int* kernel);
 
 /* Interior-stiffness SpMV microbenchmark (extract_submatrix(A, interior) x):
  * average device ms per launch over `reps` launches, and its algorithmic bytes. */

@@ -154,6 +154,7 @@ SIGNATURES = {
     "mlg_set_profiling": [C.c_void_p, C.c_int],
     "mlg_set_input_stream": [C.c_void_p, C.c_void_p],
     "mlg_build_profile": [C.c_void_p, c_double_p, c_double_p],
+    "mlg_build_profile_kernel": [C.c_void_p, c_int_p],
     "mlg_bench_spmv": [C.c_void_p, C.c_int, C.c_int, c_double_p, c_double_p],
 }
 

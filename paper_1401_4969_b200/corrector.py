@@ -311,6 +311,12 @@ class Hierarchy:
         check(lib().mlg_build_profile(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def build_profile_kernel(self) -> str:
+        """Name of the assembly kernel `build_profile` timed."""
+        k = C.c_int()
+        check(lib().mlg_build_profile_kernel(self._h, C.byref(k)))
+        return ("k_assemble", "k_assemble_table", "k_assemble_var")[k.value]
+
     def set_profiling(self, on: bool) -> None:
         check(lib().mlg_set_profiling(self._h, int(on)))
 

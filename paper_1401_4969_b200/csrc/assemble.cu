@@ -329,6 +329,137 @@ __global__ void __launch_bounds__(kBlock) k_assemble(LevelGeom G, Stencil* stA, 
   dinv[d] = A.c != 0.0 ? 1.0 / A.c : 0.0;  // JacobiPreconditioner inv_diag (0 for inactive points)
 }
 
+// ---- translation-invariant lattices: table-driven assembly (HBM-bound) ----
+// local_entry reads the vertex coordinates only through differences between
+// two vertices of the same triangle: 0 (same column / row, exact), or
+// +-(x(cx+1) - x(cx)), +-(y(cy+1) - y(cy)) (negation is exact).  When every
+// column step is bitwise one value EX and every row step one value EY (always
+// the case for the BASELINE lattices, whose dx is a power of two), the element
+// matrices of a triangle depend only on (lower/upper, rotation): six variants.
+// k_lattice_steps proves the premise on the device; k_assemble_table then
+// evaluates the variants ONCE per CTA with local_entry itself (the reference's
+// operation sequence) and each dof only looks its <= 12 entries up, orders
+// them by element id and sums from 0.0 -- bitwise the generic kernel, without
+// its 72 FP64 divisions per dof.  Any other lattice keeps k_assemble.
+__global__ void k_lattice_steps(LevelGeom G, int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < G.nx) {
+    const double e0 = xsub(lattice_coord(G.x0, 1, G.dx), lattice_coord(G.x0, 0, G.dx));
+    const double e = xsub(lattice_coord(G.x0, i + 1, G.dx), lattice_coord(G.x0, i, G.dx));
+    if (__double_as_longlong(e) != __double_as_longlong(e0)) atomicAnd(flag, 0);
+  }
+  if (i < G.ny) {
+    const double e0 = xsub(lattice_coord(G.y0, 1, G.dy), lattice_coord(G.y0, 0, G.dy));
+    const double e = xsub(lattice_coord(G.y0, i + 1, G.dy), lattice_coord(G.y0, i, G.dy));
+    if (__double_as_longlong(e) != __double_as_longlong(e0)) atomicAnd(flag, 0);
+  }
+}
+
+constexpr int kTabEntries = 2 * 3 * 3 * 3;  // (upper, rot, kd, kn)
+__device__ __forceinline__ int tab_index(int upper, int rot, int kd, int kn) {
+  return ((upper * 3 + rot) * 3 + kd) * 3 + kn;
+}
+
+// Sort key: element id above the 6-bit table index; all ones = absent.  KEY is
+// unsigned when (max element id << 6) fits 32 bits, else unsigned long long.
+template <typename KEY>
+__device__ __forceinline__ void cswap(KEY& a, KEY& b) {
+  const KEY lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
+}
+
+__device__ __forceinline__ void st_stencil(Stencil* p, const Stencil& s) {
+  // one 32-byte store per thread (sm_100: 256-bit global stores)
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(s.c), "d"(s.e), "d"(s.n),
+               "d"(s.ne)
+               : "memory");
+}
+
+template <typename KEY>
+__global__ void __launch_bounds__(kBlock) k_assemble_table(LevelGeom G, Stencil* stA,
+                                                           Stencil* stM, double* dinv) {
+  constexpr KEY kAbsent = ~static_cast<KEY>(0);
+  __shared__ double tabA[kTabEntries], tabM[kTabEntries];
+  if (threadIdx.x < kTabEntries) {
+    const int kn = threadIdx.x % 3, kd = threadIdx.x / 3 % 3, rot = threadIdx.x / 9 % 3,
+              upper = threadIdx.x / 27;
+    double vx[3], vy[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      int lx, ly;
+      canon_vertex(0, 0, upper, (rot + j) % 3, &lx, &ly);
+      vx[j] = lattice_coord(G.x0, lx, G.dx);
+      vy[j] = lattice_coord(G.y0, ly, G.dy);
+    }
+    const int ld = (kd - rot + 3) % 3, ln = (kn - rot + 3) % 3;
+    double a, m;
+    local_entry(vx[0], vy[0], vx[1], vy[1], vx[2], vy[2], min(ld, ln), max(ld, ln), &a, &m);
+    tabA[threadIdx.x] = a;
+    tabM[threadIdx.x] = m;
+  }
+  __syncthreads();
+  const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  const std::int64_t nd = static_cast<std::int64_t>(G.nx + 1) * (G.ny + 1);
+  if (d >= nd) return;
+  const int ix = static_cast<int>(d % (G.nx + 1)), iy = static_cast<int>(d / (G.nx + 1));
+  // geo codes of the four cells around the dof: (L, U) pairs, 0xFFFFFFFF = absent
+  const uint2 none = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+  const uint2* geo2 = reinterpret_cast<const uint2*>(G.geo);
+  const bool xin = ix < G.nx, yin = iy < G.ny, xm = ix > 0, ym = iy > 0;
+  const std::int64_t cell = static_cast<std::int64_t>(iy) * G.nx + ix;
+  const uint2 g11 = xin && yin ? __ldg(geo2 + cell) : none;              // cell (ix, iy)
+  const uint2 g01 = xm && yin ? __ldg(geo2 + cell - 1) : none;           // cell (ix-1, iy)
+  const uint2 g10 = xin && ym ? __ldg(geo2 + cell - G.nx) : none;        // cell (ix, iy-1)
+  const uint2 g00 = xm && ym ? __ldg(geo2 + cell - G.nx - 1) : none;     // cell (ix-1, iy-1)
+  auto key = [](unsigned code, int upper, int kd, int kn) -> KEY {
+    if (code == 0xFFFFFFFFu) return kAbsent;
+    return (static_cast<KEY>(code >> 2) << 6) |
+           static_cast<unsigned>(tab_index(upper, static_cast<int>(code & 3u), kd, kn));
+  };
+  auto pair_sum = [&](KEY k0, KEY k1, double* a, double* m) {
+    cswap(k0, k1);
+    double sa = 0.0, sm = 0.0;
+    if (k0 != kAbsent) {
+      sa = xadd(sa, tabA[k0 & 63u]);
+      sm = xadd(sm, tabM[k0 & 63u]);
+    }
+    if (k1 != kAbsent) {
+      sa = xadd(sa, tabA[k1 & 63u]);
+      sm = xadd(sm, tabM[k1 & 63u]);
+    }
+    *a = sa;
+    *m = sm;
+  };
+  Stencil A, M;
+  {  // diagonal: the six triangles around the dof (same list as k_assemble)
+    KEY k0 = key(g11.x, 0, 0, 0), k1 = key(g11.y, 1, 0, 0), k2 = key(g01.x, 0, 1, 1),
+        k3 = key(g10.y, 1, 2, 2), k4 = key(g00.x, 0, 2, 2), k5 = key(g00.y, 1, 1, 1);
+    // 12-comparator sorting network for 6 keys
+    cswap(k0, k5); cswap(k1, k3); cswap(k2, k4);
+    cswap(k1, k2); cswap(k3, k4);
+    cswap(k0, k3); cswap(k2, k5);
+    cswap(k0, k1); cswap(k2, k3); cswap(k4, k5);
+    cswap(k1, k2); cswap(k3, k4);
+    double sa = 0.0, sm = 0.0;
+    const KEY ks[6] = {k0, k1, k2, k3, k4, k5};
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+      if (ks[i] != kAbsent) {
+        sa = xadd(sa, tabA[ks[i] & 63u]);
+        sm = xadd(sm, tabM[ks[i] & 63u]);
+      }
+    A.c = sa;
+    M.c = sm;
+  }
+  pair_sum(key(g11.x, 0, 0, 1), key(g10.y, 1, 2, 1), &A.e, &M.e);   // E
+  pair_sum(key(g11.y, 1, 0, 2), key(g01.x, 0, 1, 2), &A.n, &M.n);   // N
+  pair_sum(key(g11.x, 0, 0, 2), key(g11.y, 1, 0, 1), &A.ne, &M.ne); // NE
+  st_stencil(stA + d, A);
+  st_stencil(stM + d, M);
+  dinv[d] = A.c != 0.0 ? 1.0 / A.c : 0.0;
+}
+
 // row_ptr of the full 7-point pattern in closed form.
 __device__ __forceinline__ long long row_start(int ix, int iy, int nx, int ny) {
   const long long r = static_cast<long long>(iy) * (3LL * nx + 1) +
@@ -537,8 +668,32 @@ void assemble_level(Ctx& c, Level& L) {
     k_assemble<2><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
                                                                  L.dinv.get());
   } else {
-    k_assemble<0><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
-                                                                 L.dinv.get());
+    // translation-invariant lattice (all column steps bitwise equal, all row
+    // steps bitwise equal): table-driven kernel, else the generic gather
+    const char* tenv = std::getenv("MLG_ASSEMBLE_TABLE");  // A/B and test hook: 0 disables
+    const bool no_table = tenv && tenv[0] == '0';
+    int uniform_steps = 0;
+    if (!no_table) {
+      DevBuf<int> flag(1);
+      const int one = 1;
+      flag.upload(&one, 1, c.stream);
+      k_lattice_steps<<<grid_for(std::max(L.nx, L.ny), kBlock), kBlock, 0, c.stream>>>(
+          G, flag.get());
+      MLG_LAUNCH_CHECK();
+      flag.download(&uniform_steps, 1, c.stream);
+      c.sync();
+    }
+    L.asm_table = uniform_steps;
+    if (c.profile) MLG_CUDA(cudaEventRecord(ev0, c.stream));  // the assembly launch alone
+    if (uniform_steps && (static_cast<std::uint64_t>(L.nt) << 6) < 0xFFFFFFFFull)
+      k_assemble_table<unsigned><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(
+          G, L.stA.get(), L.stM.get(), L.dinv.get());
+    else if (uniform_steps)
+      k_assemble_table<unsigned long long><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(
+          G, L.stA.get(), L.stM.get(), L.dinv.get());
+    else
+      k_assemble<0><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
+                                                                   L.dinv.get());
   }
   MLG_LAUNCH_CHECK();
   if (c.profile) {
@@ -548,6 +703,7 @@ void assemble_level(Ctx& c, Level& L) {
     MLG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     c.asm_ms = ms;
     c.asm_dofs = static_cast<double>(nd);
+    c.asm_kernel = c.cfg.example == 1 ? 2 : L.asm_table;
   }
   // Constant-coefficient detection for the CG fast path (MLG_GENERAL_STENCIL=1
   // forces the general per-row path, used by the tests to cover both).

@@ -691,6 +691,12 @@ int mlg_build_profile(mlg_ctx* ctx, double* assemble_ms, double* assemble_dofs) 
   });
 }
 
+int mlg_build_profile_kernel(mlg_ctx* ctx, int* kernel) {
+  return guarded([&] {
+    if (kernel) *kernel = C(ctx).asm_kernel;
+  });
+}
+
 int mlg_set_profiling(mlg_ctx* ctx, int on) {
   return guarded([&] { C(ctx).profile = on != 0; });
 }

@@ -14,20 +14,30 @@
 // One iteration (the one-reduction rearrangement of cg.cu, same scalars via
 // update_ctl): phase 1, pointwise, applies the pending update and forms the new
 // direction  r -= a q; x += a p; z = D^-1 r; p = z + b p  for the slab rows AND
-// recomputes p for the two ghost rows from the neighbours' published boundary
-// rows (r, q, p) -- bitwise the values the neighbours compute for those rows,
-// same operations in the same order; phase 2 computes q = A p from shared
-// memory and the five dot products r.r, r.z, p.q, q.z, q.D^-1q, then publishes
-// the slab's first and last rows.  The partial sums of the lane's C CTAs meet
-// at ONE lane barrier per iteration (monotonic counter in L2); every CTA sums
-// the C partials in the same fixed order and runs update_ctl itself, so the
-// scalars are identical everywhere and run-to-run deterministic.  The true
-// residual check (sparse.cpp:232-246) exchanges the boundary rows of x and
-// evaluates b - A x from shared memory.
+// for the two ghost rows, whose r and p the CTA keeps itself (shared memory)
+// and advances with the neighbour's published q row -- bitwise the values the
+// neighbour computes for those rows, same operations in the same order, so
+// only ONE row per side (q) crosses L2 per iteration; phase 2 computes q = A p
+// from shared memory and the five dot products r.r, r.z, p.q, q.z, q.D^-1q,
+// then publishes q of the slab's first and last rows.  (At the start and after
+// a true-residual restart the published row is r, which re-seeds the ghosts.)
+//
+// Lane synchronisation = the reduction itself: the CTA's five sums and its
+// boundary rows are released by one fence + arrival on the lane's monotonic
+// counter; after the C arrivals every CTA reads the C x 5 partials and sums
+// them in CTA order, and runs update_ctl: the scalars are identical in every
+// CTA and run-to-run deterministic.  (Measured alternatives, all slower on
+// B200, where a word written by one SM reaches another in about a
+// microsecond: partial sums as self-validating tagged words polled by five
+// warps, per-CTA mailboxes, tagged boundary rows -- strong .gpu loads and
+// stores cost far more than weak ones plus one fence -- one warp running the
+// whole chain, and two 256-thread CTAs per SM.)  The true residual check
+// (sparse.cpp:232-246) exchanges the boundary rows of x behind a plain lane
+// barrier and evaluates b - A x from shared memory.
 //
 // Traffic per point and iteration: shared memory 72 B (phase 1 loads/stores p
 // and x, phase 2 loads five p values), no HBM; L2 carries only the boundary
-// rows (3 doubles per slab column and side) and the partial sums.
+// rows (1 double per slab column and side) and the partial sums.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -62,8 +72,16 @@ __device__ __forceinline__ void sched_fence() {
   if constexpr (kChunk < kResPT) asm volatile("" ::: "memory");
 }
 constexpr int kResCap = kResT * kResPT;
-constexpr int kPartStride = 8;  // doubles per partial-sum slot
+// MLG_RES_GHOSTR = 1: the CTA keeps r of its two ghost rows in shared memory
+// and the neighbours publish one row per side (q); 0: they publish r and q and
+// no ghost r is kept (2 x pitch doubles less shared memory: the 2-CTAs/SM shape)
+#ifndef MLG_RES_GHOSTR
+#define MLG_RES_GHOSTR 1
+#endif
+constexpr bool kGhostR = MLG_RES_GHOSTR != 0;
+constexpr int kHaloFields = kGhostR ? 1 : 2;
 constexpr unsigned kFullMask = 0xffffffffu;
+__host__ __device__ constexpr int part_cpad(int C) { return (C + 15) & ~15; }  // 128-byte rows
 
 struct ResArgs {
   const CgSys* sys;
@@ -73,11 +91,11 @@ struct ResArgs {
   int bstride, nxp1;
   double* X;
   CgCtl* ctl;
-  double* part;   // [nlanes][2][C][kPartStride]
-  double* halo;   // [nlanes][2][C][2 sides][3 (r, q, p)][hpitch]
+  double* part;   // partial sums [nlanes][2 parity][kCgDots][part_cpad(C)]
+  double* halo;   // boundary rows [nlanes][2 parity][C][2 sides][kHaloFields][hpitch]
+  unsigned* bar;  // [nlanes * 32] arrival counters (one 128-byte line per lane)
   int hpitch;
   double* bslab;  // [2][gridDim.x][kResCap]: slab right-hand sides, true-residual scratch
-  unsigned* bar;  // [nlanes * 32] (one 128-byte line per lane)
   StripGeom sg;
   int masked;     // strip systems: points of the closed G_j are outside
   double tol;
@@ -85,26 +103,6 @@ struct ResArgs {
   double udinv;
   unsigned long long* trace;  // MLG_RES_TRACE: per-CTA cycle sums of the iteration phases
 };
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Lane barrier number `epoch` (0-based): every CTA of the lane has arrived
-// after its own epoch-th arrival.  All prior global writes of the CTA are
-// visible to every CTA that passes it.
-__device__ __forceinline__ void lane_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    while (ld_acquire(bar) < target) {
-    }
-  }
-  __syncthreads();
-}
 
 __device__ __forceinline__ bool point_in_system(const ResArgs& A, const CgSys& S, int gx,
                                                 int gy) {
@@ -144,67 +142,124 @@ __device__ __forceinline__ double res_product(const double* P, int i, int pitch,
   }
 }
 
-// Fixed-order block reduction of the five dot products into `out` (thread 0).
-__device__ __forceinline__ void res_block_sum(double (&acc)[kCgDots], double* red,
-                                              double* out) {
-  // one quantity at a time (the fence keeps the five trees from being
-  // interleaved: few live registers next to the r, q arrays, no spills)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < kCgDots; ++k) {
-    double v = acc[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
-    if (lane == 0) red[warp * kCgDots + k] = v;
-    asm volatile("" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x < kCgDots) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kResT / 32; ++w) s += red[w * kCgDots + threadIdx.x];
-    out[threadIdx.x] = s;
-  }
+// Release / acquire fence at gpu scope (lighter than __threadfence(), which is
+// the sequentially consistent fence.sc.gpu).
+__device__ __forceinline__ void fence_acq_rel() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-// Sum of the lane's C partial-sum slots, in CTA order (identical in every CTA).
-__device__ __forceinline__ void res_lane_sum(const double* slots, int C, double* sred,
-                                             double (&a)[kCgDots]) {
-  // warp k (k < 5) sums quantity k: lane l takes CTAs l, l+32, ... in order,
-  // then a fixed xor tree
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp < kCgDots) {
-    double v = 0.0;
-    for (int c = lane; c < C; c += 32) v += __ldcg(slots + c * kPartStride + warp);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
-    if (lane == 0) sred[warp] = v;
+// Plain lane barrier (true-residual checks only): arrival number `target` of
+// the lane's monotonic counter; release / acquire around it.
+__device__ __forceinline__ void lane_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel();
+    atomicAdd(bar, 1u);
+    while (ld_relaxed(bar) < target) {
+    }
+    fence_acq_rel();
   }
   __syncthreads();
+}
+
+// The lane's reduction and its only synchronisation.  Warp trees (the five
+// quantities interleaved), one bar.sync, warp k sums quantity k over the warps
+// and stores it; then ONE thread releases the five sums -- and, cumulatively,
+// every earlier global write of the CTA (its boundary rows) -- with one fence
+// + arrival on the lane's monotonic counter, waits for the C arrivals of this
+// reduction and acquires; warp k then reads the C partials of quantity k (both
+// loads of a lane in flight together) and sums them in CTA order (fixed xor
+// tree: identical in every CTA, run-to-run deterministic).
+//   part: the lane's partial sums [2 parity][kCgDots][C rounded up to 16] (dense per
+//   quantity; 64-byte slots per CTA measured 2 % slower)
+template <typename MARK>
+__device__ __forceinline__ void res_reduce(double (&acc)[kCgDots], double* red, double* ssum,
+                                           double* part, unsigned* bar, unsigned target, int par,
+                                           int ci, int C, double (&a)[kCgDots], MARK&& mark) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int nw = kResT / 32;
+  const int cpad = part_cpad(C);
 #pragma unroll
-  for (int k = 0; k < kCgDots; ++k) a[k] = sred[k];
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < kCgDots; ++k) acc[k] += __shfl_xor_sync(kFullMask, acc[k], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kCgDots; ++k) red[k * nw + warp] = acc[k];
+  }
   __syncthreads();
+  mark(6);
+  double* slots = part + (static_cast<long long>(par) * kCgDots + warp) * cpad;
+  if (warp < kCgDots) {
+    double v = lane < nw ? red[warp * nw + lane] : 0.0;
+#pragma unroll
+    for (int o = nw / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+    if (lane == 0) __stcg(slots + ci, v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel();
+    atomicAdd(bar, 1u);
+    while (ld_relaxed(bar) < target) {
+    }
+    fence_acq_rel();
+  }
+  __syncthreads();
+  mark(7);
+  if (warp < kCgDots) {
+    double s0 = 0.0, s1 = 0.0;
+    if (lane < C) s0 = __ldcg(slots + lane);
+    if (lane + 32 < C) s1 = __ldcg(slots + lane + 32);
+    double s = s0 + s1;
+    for (int c = lane + 64; c < C; c += 32) s += __ldcg(slots + c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFullMask, s, o);
+    if (lane == 0) ssum[warp] = s;
+  }
+  __syncthreads();
+  mark(8);
+#pragma unroll
+  for (int k = 0; k < kCgDots; ++k) a[k] = ssum[k];
 }
 
 template <bool LAP>
 __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
   extern __shared__ double smem[];
   __shared__ double s_red[(kResT / 32) * kCgDots];
-  __shared__ double s_sum[8];
   __shared__ CgCtl s_ctl;
+  __shared__ double s_sum[8];
+  __shared__ unsigned long long s_tr[16];
+  if (threadIdx.x < 16) s_tr[threadIdx.x] = 0;
   const int lane_id = blockIdx.x / A.C;
   const int ci = blockIdx.x % A.C;
   if (lane_id >= A.nlanes) return;
   const int t = threadIdx.x;
   const int C = A.C;
   unsigned* bar = A.bar + lane_id * 32;
-  unsigned epoch = 0;
+  unsigned epoch = 0;  // lane barriers so far: buffer parity; arrivals so far = C * epoch
   long long tmark = clock64();
   // (diagnostics) cycles since the previous mark, summed per CTA into slot s
+#ifdef MLG_RES_SKEW
+  // (diagnostics) GPU-wide timer stamps of 16 iterations of the lane's first
+  // system: iteration start, tagged store, reduction complete
+  auto stamp = [&](int li, int it, int what) {
+    if (A.trace != nullptr && t == 0 && li == 0 && it >= 500 && it < 516) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      A.trace[gridDim.x * 16 + (blockIdx.x * 16 + (it - 500)) * 4 + what] = g;
+    }
+  };
+#endif
   auto mark = [&](int s) {
     if (A.trace != nullptr && t == 0) {
       const long long now = clock64();
-      A.trace[blockIdx.x * 8 + s] += static_cast<unsigned long long>(now - tmark);
+      s_tr[s] += static_cast<unsigned long long>(now - tmark);
       tmark = now;
     }
   };
@@ -215,6 +270,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     if (sid < 0) break;
     const CgSys& S = A.sys[sid];  // fields re-read from global where used (registers)
     const int pitch = S.pitch;
+    const int maxit = S.maxit;
     const int R = (S.h + C - 1) / C;
     const int ya = ci * R;
     const int nr = max(min(ya + R, S.h) - ya, 0);
@@ -228,8 +284,11 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     // the buffers cover the full capacity: straight-line loops, affine addresses.
     const int plen = kResCap + 2 * pitch + 4;
     double* Xs = smem + plen;                   // kResCap
+    double* Rg = Xs + kResCap;                  // (kGhostR) r of the ghost rows: [2 sides][pitch]
     for (int i = t; i < plen; i += kResT) P[i] = 0.0;
     for (int i = t; i < kResCap; i += kResT) Xs[i] = 0.0;
+    if constexpr (kGhostR)
+      for (int i = t; i < 2 * pitch; i += kResT) Rg[i] = 0.0;
     // in-system flags of the thread's points and the slab's right-hand side
     // (0 outside the system), gathered once into the CTA's bslab row: the
     // register arrays below are then filled and refilled without divisions
@@ -258,30 +317,29 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
       r[k] = (act >> k & 1u) ? bs[j] : 0.0;
       q[k] = 0.0;
     }
-    double* part_base = A.part + static_cast<long long>(lane_id) * 2 * C * kPartStride;
-    double* halo_base = A.halo + static_cast<long long>(lane_id) * 2 * C * 6 * A.hpitch;
+    double* part_lane = A.part + static_cast<long long>(lane_id) * 2 * kCgDots * part_cpad(C);
+    double* halo_base =
+        A.halo + static_cast<long long>(lane_id) * 2 * C * 2 * kHaloFields * A.hpitch;
     auto halo_row = [&](int par, int cta, int side, int field) {
-      return halo_base + ((static_cast<long long>(par) * C + cta) * 6 + side * 3 + field) *
-                             A.hpitch;
+      return halo_base +
+             (((static_cast<long long>(par) * C + cta) * 2 + side) * kHaloFields + field) *
+                 A.hpitch;
     };
-    // publish the slab's first (side 0) and last (side 1) rows: (r, q, p)
-    auto publish = [&](int par) {
+    // publish one field of the slab's first (side 0) and last (side 1) rows.
+    // The slot tests are CTA-uniform (no divergence); only the slots that can
+    // hold a point of those rows reach the per-thread test.
+    const int first_end = min(pitch, npts), last_begin = npts - pitch;
+    auto publish = [&](const double (&v)[kResPT], int par, int field) {
+      double* row0 = halo_row(par, ci, 0, field);
+      double* row1 = halo_row(par, ci, 1, field) - last_begin;
 #pragma unroll
       for (int k = 0; k < kResPT; ++k) {
         const int j = t + k * kResT;
-        if (j < npts) {
-          const double pv = P[off + j];
-          if (j < pitch) {
-            halo_row(par, ci, 0, 0)[j] = r[k];
-            halo_row(par, ci, 0, 1)[j] = q[k];
-            halo_row(par, ci, 0, 2)[j] = pv;
-          }
-          if (j >= npts - pitch) {
-            const int c = j - (npts - pitch);
-            halo_row(par, ci, 1, 0)[c] = r[k];
-            halo_row(par, ci, 1, 1)[c] = q[k];
-            halo_row(par, ci, 1, 2)[c] = pv;
-          }
+        if (k * kResT < first_end) {
+          if (j < first_end) __stcg(row0 + j, v[k]);
+        }
+        if ((k + 1) * kResT > last_begin && k * kResT < npts) {
+          if (j >= last_begin && j < npts) __stcg(row1 + j, v[k]);
         }
       }
     };
@@ -290,13 +348,13 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     for (int k = 0; k < kCgDots; ++k) acc[k] = 0.0;
 #pragma unroll
     for (int k = 0; k < kResPT; ++k) acc[0] += r[k] * r[k];
-    __syncthreads();  // P, Xs zeroed
-    publish(epoch & 1);
-    res_block_sum(acc, s_red, part_base + ((epoch & 1) * C + ci) * kPartStride);
-    lane_barrier(bar, C * (epoch + 1));
+    __syncthreads();  // P, Xs, Rg zeroed
+    publish(r, epoch & 1, 0);  // r rows: the first iteration is a (re)start
+    if constexpr (!kGhostR) publish(q, epoch & 1, 1);  // (zeros)
     {
       double a[kCgDots];
-      res_lane_sum(part_base + (epoch & 1) * C * kPartStride, C, s_sum, a);
+      res_reduce(acc, s_red, s_sum, part_lane, bar, C * (epoch + 1), epoch & 1, ci, C, a,
+                 [](int) {});
       if (t == 0) {
         CgCtl c{};
         update_ctl<kPhaseInit>(c, a, A.tol, S.maxit);
@@ -309,6 +367,10 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
       // only the scalars this iteration needs (the full CgCtl would hold ~16
       // registers through the unrolled loops)
       if (s_ctl.status != kRunning) break;
+#ifdef MLG_RES_SKEW
+      const int it_now = s_ctl.iters;
+      stamp(li, it_now, 0);
+#endif
 #pragma unroll
       for (int k = 0; k < kCgDots; ++k) acc[k] = 0.0;
       const int par_prev = (epoch + 1) & 1;  // buffers of the previous barrier
@@ -336,24 +398,33 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
           }
           sched_fence();
         }
-        // phase 1: ghost rows from the neighbours' boundary rows (same ops)
+        mark(0);
+        // phase 1: ghost rows (same operations as their owner): r and p of
+        // the ghosts are kept here, the neighbour's q row (r row at a
+        // (re)start) comes from its published boundary row
         if (has_lo || has_hi) {
           for (int i = t; i < 2 * pitch; i += kResT) {
             const int side = i >= pitch;  // 0: row -1 (from ci-1's last row), 1: row nr
             const int col = i - side * pitch;
             if (side ? !has_hi : !has_lo) continue;
             const int src = side ? ci + 1 : ci - 1;
-            const int srow = side ? 0 : 1;
-            const double rg = __ldcg(halo_row(par_prev, src, srow, 0) + col);
-            const double qg = __ldcg(halo_row(par_prev, src, srow, 1) + col);
-            const double pg = __ldcg(halo_row(par_prev, src, srow, 2) + col);
-            const double rn = fma(-al, qg, rg);
+            double rn;
+            if constexpr (kGhostR) {
+              const double hv = __ldcg(halo_row(par_prev, src, side ? 0 : 1, 0) + col);
+              rn = rst ? hv : fma(-al, hv, Rg[i]);
+              Rg[i] = rn;
+            } else {
+              const double rg = __ldcg(halo_row(par_prev, src, side ? 0 : 1, 0) + col);
+              const double qg = __ldcg(halo_row(par_prev, src, side ? 0 : 1, 1) + col);
+              rn = fma(-al, qg, rg);
+            }
             const double tz = __dmul_rn(dv, rn);
-            P[side ? off + nr * pitch + col : off - pitch + col] = fma(be, pg, tz);
+            double* pg = P + (side ? off + nr * pitch + col : off - pitch + col);
+            *pg = fma(be, *pg, tz);
           }
         }
         __syncthreads();
-        mark(0);
+        mark(1);
         // phase 2: q = A p, dot products
 #pragma unroll
         for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
@@ -388,17 +459,13 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
           acc[1] = 0.25 * acc[0];
           acc[4] = 0.25 * acc[4];
         }
+        mark(2);
       } else {  // kModeCheck: r = b - A x (sparse.cpp:232-246)
         const int par = epoch & 1;
-        // exchange the boundary rows of x (field 2 of the halo rows)
-#pragma unroll
-        for (int k = 0; k < kResPT; ++k) {
-          const int j = t + k * kResT;
-          if (j < npts) {
-            if (j < pitch) halo_row(par, ci, 0, 2)[j] = Xs[j];
-            if (j >= npts - pitch) halo_row(par, ci, 1, 2)[j - (npts - pitch)] = Xs[j];
-          }
-        }
+        // exchange the boundary rows of x
+        for (int j = t; j < first_end; j += kResT) __stcg(halo_row(par, ci, 0, 0) + j, Xs[j]);
+        for (int j = max(last_begin, 0) + t; j < npts; j += kResT)
+          __stcg(halo_row(par, ci, 1, 0) + (j - last_begin), Xs[j]);
         lane_barrier(bar, C * (epoch + 1));
         ++epoch;
         for (int i = t; i < 2 * pitch; i += kResT) {
@@ -406,7 +473,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
           const int col = i - side * pitch;
           if (side ? !has_hi : !has_lo) continue;
           const int src = side ? ci + 1 : ci - 1;
-          const double xg = __ldcg(halo_row(par, src, side ? 0 : 1, 2) + col);
+          const double xg = __ldcg(halo_row(par, src, side ? 0 : 1, 0) + col);
           P[side ? off + nr * pitch + col : off - pitch + col] = xg;
         }
         for (int j = t; j < npts; j += kResT) P[off + j] = Xs[j];
@@ -432,22 +499,36 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         }
         __syncthreads();  // P (holding x) is read by phase 1 of a restart only as 0 * p
       }
-      publish(epoch & 1);
-      res_block_sum(acc, s_red, part_base + ((epoch & 1) * C + ci) * kPartStride);
-      mark(1);
-      lane_barrier(bar, C * (epoch + 1));
-      mark(2);
+      // normal iterations publish q; a true-residual check publishes the new
+      // r, which re-seeds the neighbours' ghost rows at the restart
+      if constexpr (kGhostR) {
+        if (s_ctl.mode == kModeNormal)
+          publish(q, epoch & 1, 0);
+        else
+          publish(r, epoch & 1, 0);
+      } else {
+        publish(r, epoch & 1, 0);
+        publish(q, epoch & 1, 1);
+      }
+      mark(3);
+#ifdef MLG_RES_SKEW
+      stamp(li, it_now, 1);
+#endif
       double a[kCgDots];
-      res_lane_sum(part_base + (epoch & 1) * C * kPartStride, C, s_sum, a);
+      res_reduce(acc, s_red, s_sum, part_lane, bar, C * (epoch + 1), epoch & 1, ci, C, a, mark);
+      mark(4);
+#ifdef MLG_RES_SKEW
+      stamp(li, it_now, 2);
+#endif
       ++epoch;
       if (t == 0) {
         CgCtl cc = s_ctl;
-        update_ctl<kPhaseIter>(cc, a, A.tol, __ldg(&A.sys[sid].maxit));
+        update_ctl<kPhaseIter>(cc, a, A.tol, maxit);
         s_ctl = cc;
       }
       __syncthreads();
-      mark(3);
-      if (A.trace != nullptr && t == 0) A.trace[blockIdx.x * 8 + 7] += 1;
+      mark(5);
+      if (A.trace != nullptr && t == 0) s_tr[15] += 1;
     }
     // x of the slab -> pooled output (cg_index layout)
     for (int j = t; j < npts; j += kResT) {
@@ -457,6 +538,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     if (ci == 0 && t == 0) A.ctl[sid] = s_ctl;
     __syncthreads();  // shared memory is reused by the next system
   }
+  if (A.trace != nullptr && t < 16) A.trace[blockIdx.x * 16 + t] = s_tr[t];
 }
 
 }  // namespace
@@ -493,7 +575,7 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
     long long worst = 0;
     for (const CgSys& s : sys_h) {
       const long long R = (s.h + C - 1) / C;
-      worst = std::max(worst, (2LL * kResCap + 2 * s.pitch + 4) * 8 + 0 * R);
+      worst = std::max(worst, (2LL * kResCap + (kGhostR ? 4 : 2) * s.pitch + 4) * 8 + 0 * R);
     }
     return worst;
   };
@@ -559,8 +641,8 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   res_lanes.upload(lanes_h.data(), lanes_h.size(), st);
   res_bar.ensure(static_cast<std::size_t>(nl) * 32);
   res_bar.zero(st);
-  res_part.ensure(static_cast<std::size_t>(nl) * 2 * C * kPartStride);
-  res_halo.ensure(static_cast<std::size_t>(nl) * 2 * C * 6 * max_pitch);
+  res_part.ensure(static_cast<std::size_t>(nl) * 2 * kCgDots * part_cpad(C));
+  res_halo.ensure(static_cast<std::size_t>(nl) * 2 * C * 2 * kHaloFields * max_pitch);
   res_bslab.ensure(static_cast<std::size_t>(2) * nl * C * kResCap);
   ctl_d.zero(st);
 
@@ -588,7 +670,7 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   static const bool trace_on = std::getenv("MLG_RES_TRACE") != nullptr;
   DevBuf<unsigned long long> trace_buf;
   if (trace_on) {
-    trace_buf.alloc(static_cast<std::size_t>(nl) * C * 8);
+    trace_buf.alloc(static_cast<std::size_t>(nl) * C * 16 * 5);
     trace_buf.zero(st);
     A.trace = trace_buf.get();
   }
@@ -616,22 +698,56 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   ctl_d.download(ctl.data(), ctl.size(), st);
   c.sync();
   if (trace_on) {
-    std::vector<unsigned long long> tr(static_cast<std::size_t>(nl) * C * 8);
+    std::vector<unsigned long long> tr(static_cast<std::size_t>(nl) * C * 16 * 5);
     trace_buf.download(tr.data(), tr.size(), st);
     c.sync();
-    double sum[8] = {0}, mx[8] = {0};
+    double sum[16] = {0}, mx[16] = {0};
     for (int b = 0; b < nl * C; ++b)
-      for (int k = 0; k < 8; ++k) {
-        sum[k] += static_cast<double>(tr[static_cast<std::size_t>(b) * 8 + k]);
-        mx[k] = std::max(mx[k], static_cast<double>(tr[static_cast<std::size_t>(b) * 8 + k]));
+      for (int k = 0; k < 16; ++k) {
+        sum[k] += static_cast<double>(tr[static_cast<std::size_t>(b) * 16 + k]);
+        mx[k] = std::max(mx[k], static_cast<double>(tr[static_cast<std::size_t>(b) * 16 + k]));
       }
-    const double it = std::max(1.0, sum[7] / (nl * C));
-    fprintf(stderr,
-            "resident trace: %d lanes x %d CTAs, %d systems, %s, %.0f iterations/CTA; cycles per "
-            "iteration (mean over CTAs): phase1+ghost %.0f, phase2+publish+blocksum %.0f, "
-            "barrier wait %.0f, lane sum+ctl %.0f\n",
-            nl, C, nsys, mask ? "strip" : "local", it, sum[0] / (nl * C) / it,
-            sum[1] / (nl * C) / it, sum[2] / (nl * C) / it, sum[3] / (nl * C) / it);
+    const double it = std::max(1.0, sum[15] / (nl * C));
+    // marks in program order (thread 0): cycles since the previous mark
+    static const int order[] = {0, 1, 2, 3, 6, 7, 8, 4, 5, 9};
+    static const char* names[] = {"phase1", "ghost+sync", "phase2", "publish", "warp trees+sync",
+                                  "block sums+arrive+wait", "lane sums+sync", "(-)", "ctl",
+                                  "(unused)"};
+    fprintf(stderr, "resident trace: %d lanes x %d CTAs, %d systems, %s, %.0f iterations/CTA; "
+            "cycles per iteration (thread 0), mean over CTAs (max over CTAs of the per-CTA mean):",
+            nl, C, nsys, mask ? "strip" : "local", it);
+    double tot = 0.0;
+    for (int k = 0; k < 10; ++k) {
+      fprintf(stderr, " %s %.0f (%.0f),", names[k], sum[order[k]] / (nl * C) / it,
+              mx[order[k]] / it);
+      tot += sum[order[k]] / (nl * C) / it;
+    }
+    fprintf(stderr, " total %.0f\n", tot);
+#ifdef MLG_RES_SKEW
+    {  // lane 0: per stamped iteration, spread over the lane's CTAs of each stamp (ns)
+      const std::size_t base = static_cast<std::size_t>(nl) * C * 16;
+      for (int i = 0; i < 16; ++i) {
+        unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+        for (int b = 0; b < C; ++b)
+          for (int w = 0; w < 3; ++w) {
+            const unsigned long long v = tr[base + (static_cast<std::size_t>(b) * 16 + i) * 4 + w];
+            lo[w] = std::min(lo[w], v);
+            hi[w] = std::max(hi[w], v);
+          }
+        fprintf(stderr, "skew it %d: start spread %llu ns, store spread %llu ns (first store "
+                "%llu ns after first start), done spread %llu ns (first done %llu ns after last "
+                "store)\n", 500 + i, hi[0] - lo[0], hi[1] - lo[1], lo[1] - lo[0], hi[2] - lo[2],
+                lo[2] - hi[1]);
+      }
+      // per-CTA store time relative to the lane's first store, iteration 508
+      fprintf(stderr, "skew it 508 store offsets (ns) by CTA:");
+      unsigned long long first = ~0ull;
+      for (int b = 0; b < C; ++b) first = std::min(first, tr[base + (static_cast<std::size_t>(b) * 16 + 8) * 4 + 1]);
+      for (int b = 0; b < C; ++b)
+        fprintf(stderr, " %llu", tr[base + (static_cast<std::size_t>(b) * 16 + 8) * 4 + 1] - first);
+      fprintf(stderr, "\n");
+    }
+#endif
   }
   for (const CgCtl& q : ctl)
     if (q.status == kIndefinite)

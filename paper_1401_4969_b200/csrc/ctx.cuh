@@ -211,6 +211,7 @@ struct Level {
   // All interior rows of A (and 1/A_ii) bitwise identical: the CG kernels then
   // take the stencil from kernel parameters (constant-coefficient lattice).
   int uniform = 0;
+  int asm_table = 0;  // operators came from k_assemble_table (translation-invariant lattice)
   Stencil ust{0.0, 0.0, 0.0, 0.0};
   double udinv = 0.0;
 
@@ -335,6 +336,7 @@ class Ctx {
   cudaStream_t input_stream = nullptr;
   // k_assemble of the most recent level built with profiling on (CUDA events)
   double asm_ms = 0, asm_dofs = 0;
+  int asm_kernel = 0;  // 0 k_assemble (generic gather), 1 k_assemble_table, 2 k_assemble_var
   cudaEvent_t input_ready = nullptr;
   void order_after_input() {
     if (!input_ready) MLG_CUDA(cudaEventCreateWithFlags(&input_ready, cudaEventDisableTiming));

@@ -12,6 +12,9 @@ CASES = [
     ("unit16_L3_m16", (0.0, 1.0, 0.0, 1.0), 1 / 16, 1 / 16, 16, 3),
     ("square_H025_m4", (-1.0, 1.0, -1.0, 1.0), 0.25, 0.25, 4, 3),
     ("rect_3x2_m1", (0.0, 3.0, -1.0, 1.0), 0.5, 0.5, 1, 3),
+    # lattice steps that are NOT bitwise uniform (8 distinct x steps at level 3):
+    # the generic k_assemble gather; the cases above take k_assemble_table
+    ("offset_H01_m1", (0.1, 1.3, -0.2, 0.4), 0.1, 0.1, 1, 3),
 ]
 
 
@@ -88,3 +91,31 @@ def test_spmv_prolong_restrict_bitexact(mlg, oracle_ref):
             y = rng.uniform(-1, 1, hy.level_info(b).ndofs)
             assert np.array_equal(bits(hy.restrict_transpose(y, b, a)),
                                   bits(rh.restrict_transpose(y, b, a)))
+
+
+def test_assembly_table_equals_generic_gather(mlg, monkeypatch):
+    """k_assemble_table (translation-invariant lattices) is bitwise the generic
+    k_assemble gather (fespace.cpp:314-341 + sparse.cpp:24-61), and the offset
+    domain falls back to the generic kernel."""
+    def operators(domain, H, levels):
+        cfg = mlg.RunConfig(domain=mlg.DomainRect(*domain), H=H, delta=H, m=1, n_levels=levels,
+                            nev=1)
+        with mlg.Hierarchy(cfg) as hy:
+            hy.set_profiling(True)
+            hy.extend_to(levels)
+            kernel = hy.build_profile_kernel()
+            return kernel, [hy.csr(levels, f) for f in ("stiffness", "mass")]
+
+    for domain, H, levels in (((0.0, 1.0, 0.0, 1.0), 1 / 8, 5), ((-1.0, 1.0, -1.0, 1.0), 0.25, 4),
+                              ((0.0, 3.0, -1.0, 1.0), 0.5, 4)):
+        monkeypatch.delenv("MLG_ASSEMBLE_TABLE", raising=False)
+        k1, ops1 = operators(domain, H, levels)
+        monkeypatch.setenv("MLG_ASSEMBLE_TABLE", "0")
+        k0, ops0 = operators(domain, H, levels)
+        assert (k1, k0) == ("k_assemble_table", "k_assemble")
+        for (rp1, c1, v1), (rp0, c0, v0) in zip(ops1, ops0):
+            assert np.array_equal(rp1, rp0) and np.array_equal(c1, c0)
+            assert np.array_equal(bits(v1), bits(v0))
+    monkeypatch.delenv("MLG_ASSEMBLE_TABLE", raising=False)
+    k, _ = operators((0.1, 1.3, -0.2, 0.4), 0.1, 3)
+    assert k == "k_assemble"
