@@ -371,14 +371,47 @@ def run_reference(args, ws, rank):
                 e2e={"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0,
                      "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
+    try:  # left for our arm's cpu_baseline on the same box (see cpu_baseline_leg)
+        import socket
+        REF_ARM_CACHE.write_text(json.dumps({"host": socket.gethostname(), "when": time.time(),
+                                             "workload": args.workload, "line": line}))
+    except OSError:
+        pass
+
+
+REF_ARM_CACHE = ROOT / ".bench_reference_arm.json"
+
+
+def cached_reference_arm(workload, max_age_s=6 * 3600):
+    """The line of a `bench.py --impl reference` run of this workload made on THIS
+    host within the last hours (the driver runs the reference arm first), or None."""
+    try:
+        import socket
+        d = json.loads(REF_ARM_CACHE.read_text())
+        if (d["host"] == socket.gethostname() and d["workload"] == workload
+                and 0 <= time.time() - d["when"] <= max_age_s):
+            return d
+    except Exception:
+        pass
+    return None
 
 
 def cpu_baseline_leg(workload):
     """The reference's CPU path for our line's cpu_baseline, run in a SUBPROCESS
-    (the product process never maps oracle/_ref).  Config 5's full reference
-    step takes ~30 min, so for it the baseline is the full L6->L7 step measured
-    by tests/golden/make_golden_l7.py in the 8-core build container (labelled);
-    the box-measured number is the --impl reference arm."""
+    (the product process never maps oracle/_ref).  If the reference arm already
+    ran on this host (the driver runs it first), its box-measured line is used.
+    Otherwise: config 5's reference needs ~5 min of serial level build before
+    its sampled step (the whole arm takes ~7 min on 16 cores), which does not
+    fit a default run, so the baseline falls back to the full L6->L7 step
+    measured by tests/golden/make_golden_l7.py in the 8-core build container
+    (labelled as such); the other workloads run the arm here (~1 min)."""
+    prev = cached_reference_arm(workload)
+    if prev is not None:
+        cb = dict(prev["line"]["cpu_baseline"])
+        cb["seconds"] = prev["line"]["ms_per_step"] * 1e-3
+        cb["sample"] = (f"the `bench.py --impl reference` run made on this host "
+                        f"{(time.time() - prev['when']) / 60:.0f} min earlier: " + cb["sample"])
+        return cb
     if workload == "c5":
         try:
             g = json.loads((ROOT / "tests" / "golden" / "golden_l7.json").read_text())

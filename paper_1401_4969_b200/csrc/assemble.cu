@@ -337,8 +337,9 @@ __global__ void __launch_bounds__(kBlock) k_assemble(LevelGeom G, Stencil* stA, 
 // the case for the BASELINE lattices, whose dx is a power of two), the element
 // matrices of a triangle depend only on (lower/upper, rotation): six variants.
 // k_lattice_steps proves the premise on the device; k_assemble_table then
-// evaluates the variants ONCE per CTA with local_entry itself (the reference's
-// operation sequence) and each dof only looks its <= 12 entries up, orders
+// reads the variants, evaluated ONCE per level by k_assemble_table_build with
+// local_entry itself (the reference's operation sequence), into shared memory
+// and each dof only looks its <= 12 entries up, orders
 // them by element id and sums from 0.0 -- bitwise the generic kernel, without
 // its 72 FP64 divisions per dof.  Any other lattice keeps k_assemble.
 __global__ void k_lattice_steps(LevelGeom G, int* flag) {
@@ -376,11 +377,9 @@ __device__ __forceinline__ void st_stencil(Stencil* p, const Stencil& s) {
                : "memory");
 }
 
-template <typename KEY>
-__global__ void __launch_bounds__(kBlock) k_assemble_table(LevelGeom G, Stencil* stA,
-                                                           Stencil* stM, double* dinv) {
-  constexpr KEY kAbsent = ~static_cast<KEY>(0);
-  __shared__ double tabA[kTabEntries], tabM[kTabEntries];
+// The table: entry (upper, rot, kd, kn) of A at [i], of M at [kTabEntries + i],
+// evaluated once per level with local_entry itself.
+__global__ void k_assemble_table_build(LevelGeom G, double* tab) {
   if (threadIdx.x < kTabEntries) {
     const int kn = threadIdx.x % 3, kd = threadIdx.x / 3 % 3, rot = threadIdx.x / 9 % 3,
               upper = threadIdx.x / 27;
@@ -395,8 +394,20 @@ __global__ void __launch_bounds__(kBlock) k_assemble_table(LevelGeom G, Stencil*
     const int ld = (kd - rot + 3) % 3, ln = (kn - rot + 3) % 3;
     double a, m;
     local_entry(vx[0], vy[0], vx[1], vy[1], vx[2], vy[2], min(ld, ln), max(ld, ln), &a, &m);
-    tabA[threadIdx.x] = a;
-    tabM[threadIdx.x] = m;
+    tab[threadIdx.x] = a;
+    tab[kTabEntries + threadIdx.x] = m;
+  }
+}
+
+template <typename KEY>
+__global__ void __launch_bounds__(kBlock) k_assemble_table(LevelGeom G, const double* tab,
+                                                           Stencil* stA, Stencil* stM,
+                                                           double* dinv) {
+  constexpr KEY kAbsent = ~static_cast<KEY>(0);
+  __shared__ double tabA[kTabEntries], tabM[kTabEntries];
+  if (threadIdx.x < kTabEntries) {
+    tabA[threadIdx.x] = __ldg(tab + threadIdx.x);
+    tabM[threadIdx.x] = __ldg(tab + kTabEntries + threadIdx.x);
   }
   __syncthreads();
   const std::int64_t d = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
@@ -641,6 +652,7 @@ void assemble_level(Ctx& c, Level& L) {
   L.stM.alloc(nd);
   L.dinv.alloc(nd);
   LevelGeom G{L.nx, L.ny, c.cfg.x_min, c.cfg.y_min, L.dx, L.dy, L.geo.get()};
+  DevBuf<double> tab;  // element-matrix table of k_assemble_table (outlives the event pair)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (c.profile) {  // roofline evidence: the assembly launch alone
     ev0 = c.event(0);
@@ -684,13 +696,18 @@ void assemble_level(Ctx& c, Level& L) {
       c.sync();
     }
     L.asm_table = uniform_steps;
-    if (c.profile) MLG_CUDA(cudaEventRecord(ev0, c.stream));  // the assembly launch alone
+    if (uniform_steps) tab.alloc(2 * kTabEntries);
+    if (c.profile) MLG_CUDA(cudaEventRecord(ev0, c.stream));  // the assembly launches alone
+    if (uniform_steps) {
+      k_assemble_table_build<<<1, 64, 0, c.stream>>>(G, tab.get());
+      MLG_LAUNCH_CHECK();
+    }
     if (uniform_steps && (static_cast<std::uint64_t>(L.nt) << 6) < 0xFFFFFFFFull)
       k_assemble_table<unsigned><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(
-          G, L.stA.get(), L.stM.get(), L.dinv.get());
+          G, tab.get(), L.stA.get(), L.stM.get(), L.dinv.get());
     else if (uniform_steps)
       k_assemble_table<unsigned long long><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(
-          G, L.stA.get(), L.stM.get(), L.dinv.get());
+          G, tab.get(), L.stA.get(), L.stM.get(), L.dinv.get());
     else
       k_assemble<0><<<grid_for(nd, kBlock), kBlock, 0, c.stream>>>(G, L.stA.get(), L.stM.get(),
                                                                    L.dinv.get());

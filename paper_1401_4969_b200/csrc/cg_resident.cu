@@ -79,6 +79,10 @@ constexpr int kResCap = kResT * kResPT;
 #define MLG_RES_GHOSTR 1
 #endif
 constexpr bool kGhostR = MLG_RES_GHOSTR != 0;
+#ifndef MLG_RES_GHOSTPRE
+#define MLG_RES_GHOSTPRE 3
+#endif
+constexpr int kGhostPre = MLG_RES_GHOSTPRE;  // ghost points per thread requested ahead
 constexpr int kHaloFields = kGhostR ? 1 : 2;
 constexpr unsigned kFullMask = 0xffffffffu;
 __host__ __device__ constexpr int part_cpad(int C) { return (C + 15) & ~15; }  // 128-byte rows
@@ -378,6 +382,21 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         const bool rst = s_ctl.restart != 0;
         const double al = rst ? 0.0 : s_ctl.alpha;
         const double be = rst ? 0.0 : s_ctl.beta;
+        // the neighbours' published rows were written by other SMs: their L2
+        // reads take microseconds, so the first kGhostPre ghost points of the
+        // thread are requested now and consumed after the own points
+        double gpre[kGhostPre > 0 ? kGhostPre : 1];
+        if constexpr (kGhostR) {
+#pragma unroll
+          for (int g = 0; g < kGhostPre; ++g) {
+            const int i = t + g * kResT;
+            const int side = i >= pitch;
+            gpre[g] = 0.0;
+            if (i < 2 * pitch && (side ? has_hi : has_lo))
+              gpre[g] = __ldcg(halo_row(par_prev, side ? ci + 1 : ci - 1, side ? 0 : 1, 0) +
+                               (i - side * pitch));
+          }
+        }
         // phase 1: own points
 #pragma unroll
         for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
@@ -403,14 +422,14 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         // the ghosts are kept here, the neighbour's q row (r row at a
         // (re)start) comes from its published boundary row
         if (has_lo || has_hi) {
-          for (int i = t; i < 2 * pitch; i += kResT) {
+          auto ghost_point = [&](int i, bool pre, double pv) {
             const int side = i >= pitch;  // 0: row -1 (from ci-1's last row), 1: row nr
             const int col = i - side * pitch;
-            if (side ? !has_hi : !has_lo) continue;
+            if (side ? !has_hi : !has_lo) return;
             const int src = side ? ci + 1 : ci - 1;
             double rn;
             if constexpr (kGhostR) {
-              const double hv = __ldcg(halo_row(par_prev, src, side ? 0 : 1, 0) + col);
+              const double hv = pre ? pv : __ldcg(halo_row(par_prev, src, side ? 0 : 1, 0) + col);
               rn = rst ? hv : fma(-al, hv, Rg[i]);
               Rg[i] = rn;
             } else {
@@ -421,6 +440,15 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
             const double tz = __dmul_rn(dv, rn);
             double* pg = P + (side ? off + nr * pitch + col : off - pitch + col);
             *pg = fma(be, *pg, tz);
+          };
+          if constexpr (kGhostR) {
+#pragma unroll
+            for (int g = 0; g < kGhostPre; ++g)
+              if (t + g * kResT < 2 * pitch) ghost_point(t + g * kResT, true, gpre[g]);
+            for (int i = t + kGhostPre * kResT; i < 2 * pitch; i += kResT)
+              ghost_point(i, false, 0.0);
+          } else {
+            for (int i = t; i < 2 * pitch; i += kResT) ghost_point(i, false, 0.0);
           }
         }
         __syncthreads();
