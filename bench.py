@@ -455,6 +455,13 @@ def _roofline(kernel, bound, achieved, role, workload, rows_per_launch, launch_m
     if bound != "hbm":  # the same algorithmic bytes against HBM, for reference
         hp, _ = measured_peak("hbm")
         e["frac_of_hbm_peak"] = achieved / hp
+        if bound == "smem" and bytes_per_row:
+            # the row rate of the resident kernel priced at the 44 B/row the
+            # HBM-streaming formulation (k_cg_iter, deferred x) moves per row:
+            # > 1 means no streaming kernel could keep up under the HBM roof
+            eq = achieved / bytes_per_row * 44.0
+            e["hbm_streaming_equivalent"] = {"bytes_per_row": 44, "GB/s": eq,
+                                             "frac_of_hbm_peak": eq / hp}
     if extra:
         e.update(extra)
     return e

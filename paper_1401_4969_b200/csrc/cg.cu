@@ -1807,10 +1807,22 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     for (CgSys& s : sys_h) s.maxit = maxit_override;
     sys_d.upload(sys_h.data(), sys_h.size(), c.stream);
   }
-  // HBM-streaming batches that fit on chip: one SM-resident launch
-  // (cg_resident.cu; measured at config 5: local 2.39 -> 2.31 s).  Batches that
-  // stay in L2 keep the persistent kernel (config 2: it is faster there).
-  if (!use_persist) {
+  // Batches whose five pooled vectors do not fit L2 and whose systems fit on
+  // chip: one SM-resident launch (cg_resident.cu; config 5 local 2.31 -> 1.69 s,
+  // config 3 local 74 -> 49 ms).  Batches that stay in L2 keep the persistent
+  // kernel (config 2: 18.7 ms against 24.7 ms resident).
+  static const int resident_mode = [] {
+    const char* e = std::getenv("MLG_CG_RESIDENT");  // A/B hook: 0 never, 2 whenever it fits
+    return e ? std::atoi(e) : 1;
+  }();
+  static const long long l2_bytes = [] {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    return static_cast<long long>(l2);
+  }();
+  const bool beyond_l2 = total_rows * 5LL * static_cast<long long>(sizeof(double)) > l2_bytes;
+  if (!use_persist || beyond_l2 || resident_mode >= 2) {
     CgResult rr;
     if (solve_resident(c, tol, rr)) return rr;
   }
