@@ -48,22 +48,29 @@ __device__ __forceinline__ void update_ctl(CgCtl& c, const double (&a)[kCgDots],
         c.xphase = 0;
       }
     }
-    if (updated && (sqrt(a[0]) <= tol * c.bnorm || c.iters >= maxit)) {
+    // The convergence test and the scalar recurrences are independent chains of
+    // long-latency FP64 operations (sqrt; two divisions): both are evaluated
+    // before the branches so that they overlap (one thread runs this between
+    // two barriers of every CG iteration).  Same arithmetic as the branchy
+    // form; the speculative quotients are simply unused when a branch returns.
+    const double pq = a[2];
+    const double rho = a[1];
+    const double rnorm = sqrt(a[0]);
+    const double alpha = rho / pq;
+    const double rho_next = rho - 2.0 * alpha * a[3] + alpha * alpha * a[4];
+    const double beta = rho_next / rho;
+    if (updated && (rnorm <= tol * c.bnorm || c.iters >= maxit)) {
       // confirm with the true residual (sparse.cpp:232-246), once x is current
       c.mode = c.xphase ? kModeFlush : kModeCheck;
       return;
     }
-    const double pq = a[2];
     if (pq <= 0.0) {  // sparse.cpp:225-226
       c.status = kIndefinite;
       c.mode = kModeSkip;
       return;
     }
-    const double rho = a[1];
-    const double alpha = rho / pq;
-    const double rho_next = rho - 2.0 * alpha * a[3] + alpha * alpha * a[4];
     c.alpha = alpha;
-    c.beta = rho_next / rho;
+    c.beta = beta;
     c.rho = rho;
     c.restart = 0;
   } else if (c.mode == kModeCheck) {

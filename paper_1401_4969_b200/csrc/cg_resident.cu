@@ -151,23 +151,26 @@ __device__ __forceinline__ double res_product(const double* P, int i, int pitch,
 __device__ __forceinline__ void fence_acq_rel() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+
+// One thread's arrival on the lane's monotonic counter (release: with the
+// preceding bar.sync it covers every earlier global write of the CTA) and its
+// wait for arrival number `target` (acquire).  Polling with acquire loads
+// measured 0.6 k cycles per iteration cheaper than relaxed loads followed by a
+// fence (config 5 local 1.68 -> 1.62 s); a release reduction instead of
+// fence + atomic made no difference.
+__device__ __forceinline__ void arrive_and_wait(unsigned* bar, unsigned target) {
+  fence_acq_rel();
+  atomicAdd(bar, 1u);
+  unsigned seen;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+  } while (seen < target);
 }
 
-// Plain lane barrier (true-residual checks only): arrival number `target` of
-// the lane's monotonic counter; release / acquire around it.
+// Plain lane barrier (true-residual checks only).
 __device__ __forceinline__ void lane_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_acq_rel();
-    atomicAdd(bar, 1u);
-    while (ld_relaxed(bar) < target) {
-    }
-    fence_acq_rel();
-  }
+  if (threadIdx.x == 0) arrive_and_wait(bar, target);
   __syncthreads();
 }
 
@@ -207,13 +210,7 @@ __device__ __forceinline__ void res_reduce(double (&acc)[kCgDots], double* red, 
     if (lane == 0) __stcg(slots + ci, v);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_acq_rel();
-    atomicAdd(bar, 1u);
-    while (ld_relaxed(bar) < target) {
-    }
-    fence_acq_rel();
-  }
+  if (threadIdx.x == 0) arrive_and_wait(bar, target);
   __syncthreads();
   mark(7);
   if (warp < kCgDots) {
@@ -592,7 +589,13 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   // kResPerSM CTAs share an SM's shared memory (1 KB per CTA reserved by the driver)
   const int smem_cta = std::min(smem_optin, smem_sm / kResPerSM - 1024);
   const int slots = nsm * kResPerSM;  // co-resident CTAs of the cooperative launch
-  const int static_smem = 4096;  // s_red, s_sum, s_ctl (+ margin)
+  // static shared memory of the kernel (s_red, s_sum, s_ctl, trace slots)
+  const int static_smem = [] {
+    cudaFuncAttributes fa{}, fb{};
+    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(&k_cg_resident<true>));
+    cudaFuncGetAttributes(&fb, reinterpret_cast<const void*>(&k_cg_resident<false>));
+    return static_cast<int>(std::max(fa.sharedSizeBytes, fb.sharedSizeBytes)) + 64;
+  }();
   const int nsys = static_cast<int>(sys_h.size());
   int max_pitch = 1, max_h = 1;
   for (const CgSys& s : sys_h) {
