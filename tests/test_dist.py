@@ -58,3 +58,46 @@ def test_cg_bytes_model():
     assert bench.cg_bytes_per_row(True) == (48, 24)
     # non-uniform levels stream the {C,E,N,NE} stencil and D^-1 as well
     assert bench.cg_bytes_per_row(False) == (88, 64)
+
+
+def test_cpu_baseline_reuses_box_measured_reference_arm(tmp_path, monkeypatch):
+    """The reference arm leaves its line for our arm's cpu_baseline; only a
+    fresh line of the same workload made on this host is reused."""
+    import json
+    import socket
+    import time
+
+    import bench
+    cache = tmp_path / "arm.json"
+    monkeypatch.setattr(bench, "REF_ARM_CACHE", cache)
+    assert bench.cached_reference_arm("c5") is None
+    line = {"ms_per_step": 857000.0,
+            "cpu_baseline": {"value": 19560.0, "unit": "DOF/s", "cores": 16, "kind": "reference",
+                             "sample": "2 sampled steps"}}
+    cache.write_text(json.dumps({"host": socket.gethostname(), "when": time.time() - 120,
+                                 "workload": "c5", "line": line}))
+    assert bench.cached_reference_arm("c2") is None
+    cb = bench.cpu_baseline_leg("c5")
+    assert cb["value"] == 19560.0 and cb["cores"] == 16 and cb["kind"] == "reference"
+    assert abs(cb["seconds"] - 857.0) < 1e-9 and "on this host" in cb["sample"]
+    cache.write_text(json.dumps({"host": "another-box", "when": time.time(), "workload": "c5",
+                                 "line": line}))
+    assert bench.cached_reference_arm("c5") is None
+    cache.write_text(json.dumps({"host": socket.gethostname(), "when": time.time() - 8 * 3600,
+                                 "workload": "c5", "line": line}))
+    assert bench.cached_reference_arm("c5") is None
+
+
+def test_roofline_entry_of_the_resident_kernel():
+    """bound = shared memory; the row rate is also priced at the streaming
+    kernel's 44 B/row against the HBM peak."""
+    import bench
+    e = bench._roofline("k_cg_resident", "smem", 12694.0, "local", "c5", 2.86e11, 1623.0, 1, 1,
+                        0.61, 72)
+    assert e["bound"] == "smem" and e["unit"] == "GB/s" and 0 < e["frac"] < 1
+    eq = e["hbm_streaming_equivalent"]
+    assert eq["bytes_per_row"] == 44 and abs(eq["GB/s"] - 12694.0 / 72 * 44) < 1e-6
+    hp, _ = bench.measured_peak("hbm")
+    assert abs(eq["frac_of_hbm_peak"] - eq["GB/s"] / hp) < 1e-12
+    h = bench._roofline("k_cg_iter", "hbm", 4795.0, "strip", "c5", 4.47e7, 0.41, 100, 100, 0.37, 44)
+    assert "hbm_streaming_equivalent" not in h and "frac_of_hbm_peak" not in h
