@@ -706,7 +706,8 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
     A.trace = trace_buf.get();
   }
   const bool lap = L->ust.c == 4.0 && L->ust.e == -1.0 && L->ust.n == -1.0 &&
-                   L->ust.ne == 0.0 && L->udinv == 0.25;
+                   L->ust.ne == 0.0 && L->udinv == 0.25 &&
+                   std::getenv("MLG_CG_NOLAP") == nullptr;  // (test hook: generic stencil)
   const void* fn = lap ? reinterpret_cast<const void*>(&k_cg_resident<true>)
                        : reinterpret_cast<const void*>(&k_cg_resident<false>);
   const int dyn = static_cast<int>(smem_for(C));

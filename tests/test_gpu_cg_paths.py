@@ -1,9 +1,10 @@
 """Every CG code path reproduces the reference's multilevel eigenvalues (golden
 vectors from the compiled reference, tests/golden/golden.json).
 
-The path is chosen per batch at run time (persistent cooperative kernel for
-L2-resident batches, multi-launch register pipeline, cp.async row pipeline for
-HBM-streaming batches, general per-row stencil, generic uniform stencil); the
+The path is chosen per batch at run time (SM-resident kernel for batches
+beyond L2, persistent cooperative kernel for L2-resident batches, multi-launch
+register pipeline, cp.async row pipeline for HBM-streaming batches, general
+per-row stencil, generic uniform stencil); the
 selection hooks are read once per process, so each variant runs in its own
 subprocess.  The L-shaped cases (config 3's domain, golden vectors of the
 restatement) cover the hole exclusion of every path."""
@@ -31,6 +32,10 @@ VARIANTS = {
                                      "MLG_CG_MAXROWS": "8"},
     "generic_uniform_stencil": {"MLG_CG_NOLAP": "1"},
     "short_tasks": {"MLG_CG_MINROWS": "4", "MLG_CG_MAXROWS": "8"},
+    # k_cg_resident for every constant-stencil batch that fits on chip (by
+    # default only batches beyond L2 take it: config 3 and config 5 sizes)
+    "sm_resident": {"MLG_CG_RESIDENT": "2"},
+    "sm_resident_generic_stencil": {"MLG_CG_RESIDENT": "2", "MLG_CG_NOLAP": "1"},
 }
 
 SCRIPT = r"""
@@ -44,7 +49,8 @@ for name, c in json.loads(sys.argv[2]).items():
                         n_levels=c["n_levels"], nev=c["nev"], hole=hole)
     with mlg.Hierarchy(cfg) as hy:
         lam, pairs, matched, times = mlg.multilevel_correction(hy)
-    out[name] = [list(map(float, l)) for l in lam]
+    out[name] = {"lam": [list(map(float, l)) for l in lam],
+                 "kernels": [[int(t.local_kernel), int(t.strip_kernel)] for t in times[1:]]}
 print(json.dumps(out))
 """
 
@@ -77,7 +83,12 @@ def _run(env_extra):
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
 def test_cg_path_matches_golden_eigenvalues(variant):
     got = _run(VARIANTS[variant])
-    for name, lams in got.items():
+    if variant.startswith("sm_resident"):  # the path under test really ran (2 = k_cg_resident)
+        assert all(2 in [k[0] for k in g["kernels"]] for g in got.values()), \
+            {n: g["kernels"] for n, g in got.items()}
+        assert any(2 in [k[1] for k in g["kernels"]] for g in got.values())  # masked strip too
+    for name, g in got.items():
+        lams = g["lam"]
         ref = _golden(name)
         assert len(lams) == len(ref), name
         for k, (a, b) in enumerate(zip(lams, ref)):
