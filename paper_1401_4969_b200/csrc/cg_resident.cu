@@ -2,13 +2,13 @@
 // for every system of a CgBatch, with each system's iterates held ON CHIP for
 // the whole solve instead of being streamed from HBM/L2 every iteration.
 //
-// Layout.  One cooperative launch, one 512-thread CTA per SM.  The CTAs are
+// Layout.  One cooperative launch, one 256-thread CTA per SM.  The CTAs are
 // grouped into `lanes` of C CTAs; a lane solves its list of systems one after
 // another.  A system (lattice window w x h, row pitch w + 1 with a zero pad
 // column) is cut into C horizontal slabs of R = ceil(h / C) rows; CTA i of the
 // lane owns slab rows [iR, min((i+1)R, h)).  Point j of a slab (row-major over
-// the pitched rows) belongs to thread j mod 512, register slot j / 512:
-//   registers   r, q = A p                 (24 points per thread: 96 registers)
+// the pitched rows) belongs to thread j mod 256, register slot j / 256:
+//   registers   r, q = A p                 (48 points per thread: 192 registers)
 //   shared mem  p with one ghost row above and below the slab, and x.
 //
 // One iteration (the one-reduction rearrangement of cg.cu, same scalars via
@@ -43,6 +43,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "cg.cuh"
@@ -51,14 +52,23 @@
 namespace mlg {
 namespace {
 
+// CTA shape: kResT threads x kResPT points.  The SM's register file holds r and
+// q of 12,288 points (3/4 of it) whatever the shape; with 256 threads x 48
+// points a thread keeps 63 registers for everything else (384 x 32: ~40,
+// 512 x 24: 32), which lets the point loops overlap the loads and FP64 chains
+// that register reuse serialised: config 5 local 1.625 s (512 x 24) -> 1.54 s
+// (384 x 32) -> 1.49 s (256 x 48); 448 x 28 is capped at 128 registers: 1.86 s.
 #ifndef MLG_RES_PT
-#define MLG_RES_PT 24
+#define MLG_RES_PT 48
 #endif
 #ifndef MLG_RES_T
-#define MLG_RES_T 512
+#define MLG_RES_T 256
 #endif
 constexpr int kResT = MLG_RES_T;     // threads per CTA
-constexpr int kResPerSM = 512 / kResT;  // co-resident CTAs per SM
+#ifndef MLG_RES_PERSM
+#define MLG_RES_PERSM 1
+#endif
+constexpr int kResPerSM = MLG_RES_PERSM;  // co-resident CTAs per SM (2 x 256 threads measured +80 %)
 constexpr int kResPT = MLG_RES_PT;  // points per thread (registers r, q)
 #ifndef MLG_RES_CHUNK
 #define MLG_RES_CHUNK MLG_RES_PT
@@ -72,6 +82,8 @@ __device__ __forceinline__ void sched_fence() {
   if constexpr (kChunk < kResPT) asm volatile("" ::: "memory");
 }
 constexpr int kResCap = kResT * kResPT;
+using ActMask = std::conditional_t<(MLG_RES_PT > 32), unsigned long long, unsigned>;
+static_assert(MLG_RES_PT <= 64, "one in-system flag per register slot");
 // MLG_RES_GHOSTR = 1: the CTA keeps r of its two ghost rows in shared memory
 // and the neighbours publish one row per side (q); 0: they publish r and q and
 // no ghost r is kept (2 x pitch doubles less shared memory: the 2-CTAs/SM shape)
@@ -80,7 +92,7 @@ constexpr int kResCap = kResT * kResPT;
 #endif
 constexpr bool kGhostR = MLG_RES_GHOSTR != 0;
 #ifndef MLG_RES_GHOSTPRE
-#define MLG_RES_GHOSTPRE 3
+#define MLG_RES_GHOSTPRE 6
 #endif
 constexpr int kGhostPre = MLG_RES_GHOSTPRE;  // ghost points per thread requested ahead
 constexpr int kHaloFields = kGhostR ? 1 : 2;
@@ -206,7 +218,7 @@ __device__ __forceinline__ void res_reduce(double (&acc)[kCgDots], double* red, 
   if (warp < kCgDots) {
     double v = lane < nw ? red[warp * nw + lane] : 0.0;
 #pragma unroll
-    for (int o = nw / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);  // lanes >= nw add 0
     if (lane == 0) __stcg(slots + ci, v);
   }
   __syncthreads();
@@ -294,7 +306,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     // (0 outside the system), gathered once into the CTA's bslab row: the
     // register arrays below are then filled and refilled without divisions
     double* bs = A.bslab + static_cast<long long>(blockIdx.x) * kResCap;
-    unsigned act = 0;
+    ActMask act = 0;  // bit k: slot k is a point of the system
 #pragma unroll 1
     for (int k = 0; k < kResPT; ++k) {
       const int j = t + k * kResT;
@@ -304,7 +316,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         if (col < S.w) {
           const int gx = S.x0 + col, gy = S.y0 + ya + row;
           if (point_in_system(A, S, gx, gy)) {
-            act |= 1u << k;
+            act |= static_cast<ActMask>(1) << k;
             b = A.bsrc[(static_cast<long long>(gy) * A.nxp1 + gx) * A.bstride + S.rhs];
           }
         }
