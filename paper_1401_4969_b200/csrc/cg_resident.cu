@@ -194,12 +194,16 @@ __device__ __forceinline__ void lane_barrier(unsigned* bar, unsigned target) {
 // reduction and acquires; warp k then reads the C partials of quantity k (both
 // loads of a lane in flight together) and sums them in CTA order (fixed xor
 // tree: identical in every CTA, run-to-run deterministic).
+// `after_barrier` runs in every thread as soon as the arrivals are complete:
+// the kernel requests the neighbours' boundary rows there, so that their L2
+// latency overlaps the reading of the partial sums and update_ctl.
 //   part: the lane's partial sums [2 parity][kCgDots][C rounded up to 16] (dense per
 //   quantity; 64-byte slots per CTA measured 2 % slower)
-template <typename MARK>
+template <typename MARK, typename AFTER>
 __device__ __forceinline__ void res_reduce(double (&acc)[kCgDots], double* red, double* ssum,
                                            double* part, unsigned* bar, unsigned target, int par,
-                                           int ci, int C, double (&a)[kCgDots], MARK&& mark) {
+                                           int ci, int C, double (&a)[kCgDots], MARK&& mark,
+                                           AFTER&& after_barrier) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nw = kResT / 32;
   const int cpad = part_cpad(C);
@@ -224,6 +228,7 @@ __device__ __forceinline__ void res_reduce(double (&acc)[kCgDots], double* red, 
   __syncthreads();
   if (threadIdx.x == 0) arrive_and_wait(bar, target);
   __syncthreads();
+  after_barrier();  // (all threads: loads that only need the barrier, not the sums)
   mark(7);
   if (warp < kCgDots) {
     double s0 = 0.0, s1 = 0.0;
@@ -356,6 +361,24 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         }
       }
     };
+    // The neighbours' published rows were written by other SMs: their L2 reads
+    // take microseconds.  The first kGhostPre ghost points of the thread are
+    // requested right after the lane barrier that makes them visible (inside
+    // res_reduce) and consumed in phase 1 of the next iteration.
+    double gpre[kGhostPre > 0 ? kGhostPre : 1];
+    auto prefetch_ghost = [&](int par) {
+      if constexpr (kGhostR) {
+#pragma unroll
+        for (int g = 0; g < kGhostPre; ++g) {
+          const int i = t + g * kResT;
+          const int side = i >= pitch;
+          gpre[g] = 0.0;
+          if (i < 2 * pitch && (side ? has_hi : has_lo))
+            gpre[g] = __ldcg(halo_row(par, side ? ci + 1 : ci - 1, side ? 0 : 1, 0) +
+                             (i - side * pitch));
+        }
+      }
+    };
     double acc[kCgDots];
 #pragma unroll
     for (int k = 0; k < kCgDots; ++k) acc[k] = 0.0;
@@ -367,7 +390,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     {
       double a[kCgDots];
       res_reduce(acc, s_red, s_sum, part_lane, bar, C * (epoch + 1), epoch & 1, ci, C, a,
-                 [](int) {});
+                 [](int) {}, [&] { prefetch_ghost(epoch & 1); });
       if (t == 0) {
         CgCtl c{};
         update_ctl<kPhaseInit>(c, a, A.tol, S.maxit);
@@ -391,21 +414,6 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         const bool rst = s_ctl.restart != 0;
         const double al = rst ? 0.0 : s_ctl.alpha;
         const double be = rst ? 0.0 : s_ctl.beta;
-        // the neighbours' published rows were written by other SMs: their L2
-        // reads take microseconds, so the first kGhostPre ghost points of the
-        // thread are requested now and consumed after the own points
-        double gpre[kGhostPre > 0 ? kGhostPre : 1];
-        if constexpr (kGhostR) {
-#pragma unroll
-          for (int g = 0; g < kGhostPre; ++g) {
-            const int i = t + g * kResT;
-            const int side = i >= pitch;
-            gpre[g] = 0.0;
-            if (i < 2 * pitch && (side ? has_hi : has_lo))
-              gpre[g] = __ldcg(halo_row(par_prev, side ? ci + 1 : ci - 1, side ? 0 : 1, 0) +
-                               (i - side * pitch));
-          }
-        }
         // phase 1: own points
 #pragma unroll
         for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
@@ -552,7 +560,8 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
       stamp(li, it_now, 1);
 #endif
       double a[kCgDots];
-      res_reduce(acc, s_red, s_sum, part_lane, bar, C * (epoch + 1), epoch & 1, ci, C, a, mark);
+      res_reduce(acc, s_red, s_sum, part_lane, bar, C * (epoch + 1), epoch & 1, ci, C, a, mark,
+                 [&] { prefetch_ghost(epoch & 1); });
       mark(4);
 #ifdef MLG_RES_SKEW
       stamp(li, it_now, 2);
