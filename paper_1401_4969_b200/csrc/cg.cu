@@ -1240,6 +1240,9 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
 #define MLG_CG_PERSIST_TILES 8  // A/B: 16 takes config 5's strip batches persistent: strip +15 % time
 #endif
 constexpr int kPersistTiles = MLG_CG_PERSIST_TILES;
+#ifndef MLG_CG_BOUSTRO_DEFAULT
+#define MLG_CG_BOUSTRO_DEFAULT 0
+#endif
 
 struct GridSync {
   unsigned* count;    // arrivals since the launch began (zeroed before each launch)
@@ -1826,6 +1829,14 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     CgResult rr;
     if (solve_resident(c, tol, rr)) return rr;
   }
+  // HBM-streaming batches sweep their tiles in alternating order: the rows the
+  // previous launch wrote last (still dirty in the 126 MB L2) are the first the
+  // next launch reads (MLG_CG_BOUSTRO=0 restores the fixed order).
+  static const bool boustro_env = [] {
+    const char* e = std::getenv("MLG_CG_BOUSTRO");
+    return e ? std::atoi(e) != 0 : MLG_CG_BOUSTRO_DEFAULT != 0;
+  }();
+  const bool boustro = boustro_env && use_async;
   std::vector<CgTile> tiles;
   auto rebuild = [&](const std::vector<char>& active) {
     tiles.clear();
@@ -1833,6 +1844,11 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       if (active[s])
         for (int t = 0; t < sys_h[s].ntiles; ++t) tiles.push_back({s, t});
     tiles_d.upload(tiles.data(), tiles.size(), c.stream);
+    if (boustro && !use_persist) {  // the same tiles in reverse launch order (odd launches)
+      std::vector<CgTile> rev(tiles.rbegin(), tiles.rend());
+      tiles_rev_d.ensure(rev.size());
+      tiles_rev_d.upload(rev.data(), rev.size(), c.stream);
+    }
   };
   std::vector<char> active(nsys, 1);
   rebuild(active);
@@ -2004,6 +2020,7 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       if (ctl[static_cast<std::size_t>(s)].status == kIndefinite)
         throw SolverError("cg_solve: matrix is not positive definite (p'Mp <= 0)");
   }
+  unsigned launch_no = 0;
   while (!use_persist) {
     for (int it = 0; it < chunk && !tiles.empty(); ++it) {
       const unsigned nt = static_cast<unsigned>(tiles.size());
@@ -2020,21 +2037,22 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
         MLG_CUDA(cudaEventRecord(ev0, st));
       }
       const Finish& Fl = prof && profiling ? Fp : F;
+      const CgTile* tls = boustro && (launch_no++ & 1u) ? tiles_rev_d.get() : tiles_d.get();
       if (uni && use_async && lap)
         k_cg_iter<true, true, true><<<nt, kBlock, kRingBytes, st>>>(
-            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else if (uni && use_async)
         k_cg_iter<true, true, false><<<nt, kBlock, kRingBytes, st>>>(
-            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else if (uni && lap)
         k_cg_iter<true, false, true><<<nt, kBlock, 0, st>>>(
-            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else if (uni)
         k_cg_iter<true, false, false><<<nt, kBlock, 0, st>>>(
-            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else
         k_cg_iter<false, false, false><<<nt, kBlock, 0, st>>>(
-            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       MLG_LAUNCH_CHECK();
       if (prof) {
         MLG_CUDA(cudaEventRecord(ev1, st));

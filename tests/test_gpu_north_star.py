@@ -13,8 +13,9 @@ tests/golden/make_golden_l7.py from oracle/_ref: corrector.cpp:414-462).
   the lambda_2 ~ lambda_3 cluster (relative gap 5.6e-7 < 1e-6) is
   compared as a subspace: the 2x2 least-squares fit S U ~ Q S V has relative
   residual <= 1e-8 (and the same on the sampled point values);
-* the reference's local-solve iteration counts at level 7 (8 tasks) are met
-  within +-2 by the device CG started from the reference's level-6 state.
+* the reference's local-solve iteration counts at level 7 (8 tasks) and its
+  strip-solve count for eigenvector 0 (2321) are met within +-2 by the device CG
+  started from the reference's level-6 state.
 
 Config 2 and the config-5 shape at 1024^2 are compared on FULL vectors in the
 mass norm against a live reference run (compare_pairs, tests/_parity.py).
@@ -121,6 +122,39 @@ def test_c5_local_iterations_match_reference(mlg):
             _, rep = mlg.local_bvp_solve(hy, 7, j, g["lambdas"][5][i], u, 1e-10)
             assert rep.converged
             assert abs(rep.iterations - it_ref) <= 2, (key, rep.iterations, it_ref)
+
+
+def test_c5_strip_iterations_match_reference(mlg):
+    """Level-7 strip solve of eigenvector 0 (interface_solve, corrector.cpp:216-254)
+    from the level-6 state: the reference's own cg_solve on the strip system took
+    2321 iterations (make_golden_l7.py strip()); the device CG is within +-2.
+    Needs the 64 full-length corrections on the host (8.6 GB), as the reference's
+    signature does."""
+    g = _golden()
+    ref_its = g.get("reference_strip_iterations_L7") or []
+    if not ref_its:
+        pytest.skip("no reference strip iteration count recorded")
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 0
+    if avail < 40 * 2**30:
+        pytest.skip("needs ~20 GB of free host memory")
+    c = g["config"]
+    cfg = mlg.RunConfig(domain=mlg.DomainRect(*c["domain"]), H=c["H"], delta=c["delta"],
+                        m=c["m"], n_levels=c["n_levels"], nev=c["nev"])
+    with mlg.Hierarchy(cfg) as hy:
+        lam, pairs, _, _ = mlg.multilevel_correction(hy, last_level=6)
+        hy.extend_to(7)
+        lam0 = g["lambdas"][5][0]
+        u = hy.prolong(hy.expand_interior(6, pairs[0].coeffs), 6, 7)
+        corr = np.empty((c["m"], u.size))
+        for j in range(c["m"]):
+            corr[j], rep = mlg.local_bvp_solve(hy, 7, j, lam0, u, 1e-10)
+            assert rep.converged
+        _, rep = mlg.interface_solve(hy, 7, lam0, u, corr, 1e-10)
+        assert rep.converged
+        assert abs(rep.iterations - ref_its[0]) <= 2, (rep.iterations, ref_its)
 
 
 @pytest.mark.parametrize("name,H,m,L,nev", [("c2sub_16_L6_m16_nev1", 1 / 16, 16, 6, 1),
