@@ -1240,9 +1240,6 @@ __global__ void __launch_bounds__(kBlock, (!UNI ? 4 : ASYNC ? MLG_CG_ASYNC_MINBL
 #define MLG_CG_PERSIST_TILES 8  // A/B: 16 takes config 5's strip batches persistent: strip +15 % time
 #endif
 constexpr int kPersistTiles = MLG_CG_PERSIST_TILES;
-#ifndef MLG_CG_BOUSTRO_DEFAULT
-#define MLG_CG_BOUSTRO_DEFAULT 0
-#endif
 
 struct GridSync {
   unsigned* count;    // arrivals since the launch began (zeroed before each launch)
@@ -1810,12 +1807,15 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     for (CgSys& s : sys_h) s.maxit = maxit_override;
     sys_d.upload(sys_h.data(), sys_h.size(), c.stream);
   }
-  // Batches whose five pooled vectors do not fit L2 and whose systems fit on
-  // chip: one SM-resident launch (cg_resident.cu; config 5 local 2.31 -> 1.69 s,
-  // config 3 local 74 -> 49 ms).  Batches that stay in L2 keep the persistent
-  // kernel (config 2: 18.7 ms against 24.7 ms resident).
+  // Constant-stencil batches whose systems fit on chip run SM-resident
+  // (cg_resident.cu): always when the five pooled vectors do not fit L2 (config 5
+  // local 2.31 -> 1.49 s, config 3 local 74 -> 37 ms), and for L2-sized batches
+  // from 256 k pooled rows up, where the resident kernel with a slab-sized
+  // instantiation beats the persistent one (config 2: strip 13.8 -> 11.0 ms at 48
+  // points per thread already).  Smaller batches keep the persistent kernel.
   static const int resident_mode = [] {
-    const char* e = std::getenv("MLG_CG_RESIDENT");  // A/B hook: 0 never, 2 whenever it fits
+    // A/B hook: 0 never, 2 whenever it fits, 3 only beyond L2 (the earlier rule)
+    const char* e = std::getenv("MLG_CG_RESIDENT");
     return e ? std::atoi(e) : 1;
   }();
   static const long long l2_bytes = [] {
@@ -1825,18 +1825,11 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     return static_cast<long long>(l2);
   }();
   const bool beyond_l2 = total_rows * 5LL * static_cast<long long>(sizeof(double)) > l2_bytes;
-  if (!use_persist || beyond_l2 || resident_mode >= 2) {
+  const bool sizeable = resident_mode != 3 && total_rows >= (1LL << 18);
+  if (!use_persist || beyond_l2 || sizeable || resident_mode == 2) {
     CgResult rr;
     if (solve_resident(c, tol, rr)) return rr;
   }
-  // HBM-streaming batches sweep their tiles in alternating order: the rows the
-  // previous launch wrote last (still dirty in the 126 MB L2) are the first the
-  // next launch reads (MLG_CG_BOUSTRO=0 restores the fixed order).
-  static const bool boustro_env = [] {
-    const char* e = std::getenv("MLG_CG_BOUSTRO");
-    return e ? std::atoi(e) != 0 : MLG_CG_BOUSTRO_DEFAULT != 0;
-  }();
-  const bool boustro = boustro_env && use_async;
   std::vector<CgTile> tiles;
   auto rebuild = [&](const std::vector<char>& active) {
     tiles.clear();
@@ -1844,11 +1837,6 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       if (active[s])
         for (int t = 0; t < sys_h[s].ntiles; ++t) tiles.push_back({s, t});
     tiles_d.upload(tiles.data(), tiles.size(), c.stream);
-    if (boustro && !use_persist) {  // the same tiles in reverse launch order (odd launches)
-      std::vector<CgTile> rev(tiles.rbegin(), tiles.rend());
-      tiles_rev_d.ensure(rev.size());
-      tiles_rev_d.upload(rev.data(), rev.size(), c.stream);
-    }
   };
   std::vector<char> active(nsys, 1);
   rebuild(active);
@@ -2020,7 +2008,6 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
       if (ctl[static_cast<std::size_t>(s)].status == kIndefinite)
         throw SolverError("cg_solve: matrix is not positive definite (p'Mp <= 0)");
   }
-  unsigned launch_no = 0;
   while (!use_persist) {
     for (int it = 0; it < chunk && !tiles.empty(); ++it) {
       const unsigned nt = static_cast<unsigned>(tiles.size());
@@ -2037,22 +2024,21 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
         MLG_CUDA(cudaEventRecord(ev0, st));
       }
       const Finish& Fl = prof && profiling ? Fp : F;
-      const CgTile* tls = boustro && (launch_no++ & 1u) ? tiles_rev_d.get() : tiles_d.get();
       if (uni && use_async && lap)
         k_cg_iter<true, true, true><<<nt, kBlock, kRingBytes, st>>>(
-            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else if (uni && use_async)
         k_cg_iter<true, true, false><<<nt, kBlock, kRingBytes, st>>>(
-            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else if (uni && lap)
         k_cg_iter<true, false, true><<<nt, kBlock, 0, st>>>(
-            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else if (uni)
         k_cg_iter<true, false, false><<<nt, kBlock, 0, st>>>(
-            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       else
         k_cg_iter<false, false, false><<<nt, kBlock, 0, st>>>(
-            sys_d.get(), tls, A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
+            sys_d.get(), tiles_d.get(), A, bsrc, bstride, X.get(), rc, rn, pc, pn, Fl);
       MLG_LAUNCH_CHECK();
       if (prof) {
         MLG_CUDA(cudaEventRecord(ev1, st));

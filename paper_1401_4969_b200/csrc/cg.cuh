@@ -109,7 +109,7 @@ class CgBatch {
   long long total_rows = 0;
   int total_tiles = 0;
   DevBuf<CgSys> sys_d;
-  DevBuf<CgTile> tiles_d, tiles_rev_d;
+  DevBuf<CgTile> tiles_d;
   DevBuf<int> task_map;
   DevBuf<CgCtl> ctl_d;
   DevBuf<unsigned> counters;  // per-system tile arrival counters (last-tile reduction)

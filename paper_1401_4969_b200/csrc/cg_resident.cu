@@ -71,19 +71,18 @@ constexpr int kResT = MLG_RES_T;     // threads per CTA
 constexpr int kResPerSM = MLG_RES_PERSM;  // co-resident CTAs per SM (2 x 256 threads measured +80 %)
 constexpr int kResPT = MLG_RES_PT;  // points per thread (registers r, q)
 #ifndef MLG_RES_CHUNK
-#define MLG_RES_CHUNK MLG_RES_PT
+#define MLG_RES_CHUNK 0  // 0: one chunk (A/B hook)
 #endif
-// The pointwise phases run their kResPT points in chunks of kChunk with a
+// The pointwise phases can run their points in chunks of MLG_RES_CHUNK with a
 // scheduling fence between chunks: the loads of one chunk are hoisted and
-// overlapped, but not across chunks (no spills of the r, q register arrays).
-constexpr int kChunk = MLG_RES_CHUNK;
-static_assert(kResPT % kChunk == 0, "chunk must divide the points per thread");
-__device__ __forceinline__ void sched_fence() {
-  if constexpr (kChunk < kResPT) asm volatile("" ::: "memory");
-}
-constexpr int kResCap = kResT * kResPT;
-using ActMask = std::conditional_t<(MLG_RES_PT > 32), unsigned long long, unsigned>;
+// overlapped, but not across chunks (one chunk measured best at 256 x 48).
+constexpr int kResCap = kResT * kResPT;  // points per CTA of the largest instantiation
 static_assert(MLG_RES_PT <= 64, "one in-system flag per register slot");
+// Instantiated slab capacities (points per thread).  A slab of R rows x pitch
+// points runs the smallest variant that holds it: the unrolled point loops
+// cost their full trip count whatever the slab holds (config 2's strip, 7 rows
+// x 1024 = 28 x 256 points, paid for 48 slots before).
+constexpr int kResVariants[] = {MLG_RES_PT, 36, 28, 20, 12};
 // MLG_RES_GHOSTR = 1: the CTA keeps r of its two ghost rows in shared memory
 // and the neighbours publish one row per side (q); 0: they publish r and q and
 // no ghost r is kept (2 x pitch doubles less shared memory: the 2-CTAs/SM shape)
@@ -91,6 +90,15 @@ static_assert(MLG_RES_PT <= 64, "one in-system flag per register slot");
 #define MLG_RES_GHOSTR 1
 #endif
 constexpr bool kGhostR = MLG_RES_GHOSTR != 0;
+// MLG_RES_FUSEPUB = 1: normal iterations store q of the slab's first and last
+// rows from inside phase 2 (two predicated stores per slot) instead of a
+// separate pass of CTA-uniform branches over the slots afterwards
+#ifndef MLG_RES_FUSEPUB
+#define MLG_RES_FUSEPUB 1
+#endif
+constexpr bool kFusePub = MLG_RES_FUSEPUB != 0 && MLG_RES_GHOSTR != 0;
+constexpr int kFirstSlots = 8;  // slots that can hold a point of the slab's first row
+constexpr int kTailSlots = 12;  // ... of its last row, when the slab is (nearly) full
 #ifndef MLG_RES_GHOSTPRE
 #define MLG_RES_GHOSTPRE 6
 #endif
@@ -231,11 +239,16 @@ __device__ __forceinline__ void res_reduce(double (&acc)[kCgDots], double* red, 
   after_barrier();  // (all threads: loads that only need the barrier, not the sums)
   mark(7);
   if (warp < kCgDots) {
-    double s0 = 0.0, s1 = 0.0;
-    if (lane < C) s0 = __ldcg(slots + lane);
-    if (lane + 32 < C) s1 = __ldcg(slots + lane + 32);
-    double s = s0 + s1;
-    for (int c = lane + 64; c < C; c += 32) s += __ldcg(slots + c);
+    // every load of the lane in flight together (C <= 160 CTAs: five per lane);
+    // a serial tail cost one L2 round trip per 32 CTAs beyond 64 (config 2's
+    // strip, 114 CTAs: lane sums 5.1 k cycles against 3.4 k at C <= 64)
+    double sv[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) sv[k] = lane + 32 * k < C ? __ldcg(slots + lane + 32 * k) : 0.0;
+    double s = sv[0] + sv[1];
+#pragma unroll
+    for (int k = 2; k < 5; ++k) s += sv[k];
+    for (int c = lane + 160; c < C; c += 32) s += __ldcg(slots + c);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFullMask, s, o);
     if (lane == 0) ssum[warp] = s;
@@ -246,8 +259,19 @@ __device__ __forceinline__ void res_reduce(double (&acc)[kCgDots], double* red, 
   for (int k = 0; k < kCgDots; ++k) a[k] = ssum[k];
 }
 
-template <bool LAP>
+template <bool LAP, int PT>
 __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
+  // PT points per thread (register slots of r and q); the point loops run PT
+  // slots whatever the slab holds, so small slabs use a smaller instantiation
+  constexpr int kCap = kResT * PT;
+  constexpr int kCh = MLG_RES_CHUNK > 0 && PT % MLG_RES_CHUNK == 0 ? MLG_RES_CHUNK : PT;
+  using Act = std::conditional_t<(PT > 32), unsigned long long, unsigned>;
+  // ghost points per thread requested ahead: the smaller instantiations have the
+  // registers for 8 (two rows of pitch <= 1024: config 2's strip)
+  constexpr int kGP = PT >= MLG_RES_PT ? kGhostPre : (kGhostPre > 8 ? kGhostPre : 8);
+  auto sched_fence = [] {
+    if constexpr (kCh < PT) asm volatile("" ::: "memory");
+  };
   extern __shared__ double smem[];
   __shared__ double s_red[(kResT / 32) * kCgDots];
   __shared__ CgCtl s_ctl;
@@ -297,23 +321,23 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     const bool has_hi = nr > 0 && (ci + 1) * R < S.h;       // neighbour slab above
     double* P = smem;                           // (R + 2) * pitch + 2, point (row, col) at
     const int off = pitch + 1;                  //   off + row * pitch + col
-    // Every slot j < kResCap of the unrolled point loops may READ P[off + j +-
+    // Every slot j < kCap of the unrolled point loops may READ P[off + j +-
     // pitch +- 1] and Xs[j] (slots past the slab are masked, never stored), so
     // the buffers cover the full capacity: straight-line loops, affine addresses.
-    const int plen = kResCap + 2 * pitch + 4;
-    double* Xs = smem + plen;                   // kResCap
-    double* Rg = Xs + kResCap;                  // (kGhostR) r of the ghost rows: [2 sides][pitch]
+    const int plen = kCap + 2 * pitch + 4;
+    double* Xs = smem + plen;                   // kCap
+    double* Rg = Xs + kCap;                  // (kGhostR) r of the ghost rows: [2 sides][pitch]
     for (int i = t; i < plen; i += kResT) P[i] = 0.0;
-    for (int i = t; i < kResCap; i += kResT) Xs[i] = 0.0;
+    for (int i = t; i < kCap; i += kResT) Xs[i] = 0.0;
     if constexpr (kGhostR)
       for (int i = t; i < 2 * pitch; i += kResT) Rg[i] = 0.0;
     // in-system flags of the thread's points and the slab's right-hand side
     // (0 outside the system), gathered once into the CTA's bslab row: the
     // register arrays below are then filled and refilled without divisions
-    double* bs = A.bslab + static_cast<long long>(blockIdx.x) * kResCap;
-    ActMask act = 0;  // bit k: slot k is a point of the system
+    double* bs = A.bslab + static_cast<long long>(blockIdx.x) * kCap;
+    Act act = 0;  // bit k: slot k is a point of the system
 #pragma unroll 1
-    for (int k = 0; k < kResPT; ++k) {
+    for (int k = 0; k < PT; ++k) {
       const int j = t + k * kResT;
       double b = 0.0;
       if (j < npts) {
@@ -321,16 +345,16 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         if (col < S.w) {
           const int gx = S.x0 + col, gy = S.y0 + ya + row;
           if (point_in_system(A, S, gx, gy)) {
-            act |= static_cast<ActMask>(1) << k;
+            act |= static_cast<Act>(1) << k;
             b = A.bsrc[(static_cast<long long>(gy) * A.nxp1 + gx) * A.bstride + S.rhs];
           }
         }
         bs[j] = b;
       }
     }
-    double r[kResPT], q[kResPT];
+    double r[PT], q[PT];
 #pragma unroll
-    for (int k = 0; k < kResPT; ++k) {
+    for (int k = 0; k < PT; ++k) {
       const int j = t + k * kResT;
       r[k] = (act >> k & 1u) ? bs[j] : 0.0;
       q[k] = 0.0;
@@ -347,11 +371,14 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     // The slot tests are CTA-uniform (no divergence); only the slots that can
     // hold a point of those rows reach the per-thread test.
     const int first_end = min(pitch, npts), last_begin = npts - pitch;
-    auto publish = [&](const double (&v)[kResPT], int par, int field) {
+    // (fused publish: nobody reads the last row of the lane's top slab)
+    const int lb_pub = has_hi ? last_begin : 0x3fffffff;
+    const bool last_in_tail = PT > kTailSlots && lb_pub >= (PT - kTailSlots) * kResT;
+    auto publish = [&](const double (&v)[PT], int par, int field) {
       double* row0 = halo_row(par, ci, 0, field);
       double* row1 = halo_row(par, ci, 1, field) - last_begin;
 #pragma unroll
-      for (int k = 0; k < kResPT; ++k) {
+      for (int k = 0; k < PT; ++k) {
         const int j = t + k * kResT;
         if (k * kResT < first_end) {
           if (j < first_end) __stcg(row0 + j, v[k]);
@@ -365,11 +392,11 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
     // take microseconds.  The first kGhostPre ghost points of the thread are
     // requested right after the lane barrier that makes them visible (inside
     // res_reduce) and consumed in phase 1 of the next iteration.
-    double gpre[kGhostPre > 0 ? kGhostPre : 1];
+    double gpre[kGP > 0 ? kGP : 1];
     auto prefetch_ghost = [&](int par) {
       if constexpr (kGhostR) {
 #pragma unroll
-        for (int g = 0; g < kGhostPre; ++g) {
+        for (int g = 0; g < kGP; ++g) {
           const int i = t + g * kResT;
           const int side = i >= pitch;
           gpre[g] = 0.0;
@@ -383,7 +410,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
 #pragma unroll
     for (int k = 0; k < kCgDots; ++k) acc[k] = 0.0;
 #pragma unroll
-    for (int k = 0; k < kResPT; ++k) acc[0] += r[k] * r[k];
+    for (int k = 0; k < PT; ++k) acc[0] += r[k] * r[k];
     __syncthreads();  // P, Xs, Rg zeroed
     publish(r, epoch & 1, 0);  // r rows: the first iteration is a (re)start
     if constexpr (!kGhostR) publish(q, epoch & 1, 1);  // (zeros)
@@ -416,9 +443,9 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         const double be = rst ? 0.0 : s_ctl.beta;
         // phase 1: own points
 #pragma unroll
-        for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
+        for (int k0 = 0; k0 < PT; k0 += kCh) {
 #pragma unroll
-          for (int k = k0; k < k0 + kChunk; ++k) {
+          for (int k = k0; k < k0 + kCh; ++k) {
             // branch-free (loads of consecutive points overlap): points of the
             // slab outside the system hold r = q = p = 0 and stay so; slots past
             // the slab read a valid dummy point and do not store
@@ -460,9 +487,9 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
           };
           if constexpr (kGhostR) {
 #pragma unroll
-            for (int g = 0; g < kGhostPre; ++g)
+            for (int g = 0; g < kGP; ++g)
               if (t + g * kResT < 2 * pitch) ghost_point(t + g * kResT, true, gpre[g]);
-            for (int i = t + kGhostPre * kResT; i < 2 * pitch; i += kResT)
+            for (int i = t + kGP * kResT; i < 2 * pitch; i += kResT)
               ghost_point(i, false, 0.0);
           } else {
             for (int i = t; i < 2 * pitch; i += kResT) ghost_point(i, false, 0.0);
@@ -471,31 +498,55 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         __syncthreads();
         mark(1);
         // phase 2: q = A p, dot products
-#pragma unroll
-        for (int k0 = 0; k0 < kResPT; k0 += kChunk) {
-#pragma unroll
-          for (int k = k0; k < k0 + kChunk; ++k) {
-            // branch-free: q of points outside the system is forced to 0, so
-            // every dot term of such a point is an exact zero (r = p = 0 there)
-            const int j = t + k * kResT;
-            const double qa = res_product<LAP>(P, off + j, pitch, u);
-            const double qq = (act >> k & 1u) ? qa : 0.0;
-            const double pv = P[off + j];  // finite; its term is 0 where qq is masked
-            q[k] = qq;
-            acc[0] += r[k] * r[k];
-            acc[2] += pv * qq;
-            if constexpr (LAP) {  // D^-1 = 1/4: the z terms are exact quarters (below)
-              acc[1] += qq * r[k];
-              acc[4] += qq * qq;
-            } else {
-              const double tz = __dmul_rn(dv, r[k]);
-              acc[1] += r[k] * tz;
-              acc[3] += qq * tz;
-              acc[4] += qq * __dmul_rn(dv, qq);
+        // (per-thread bases: the slot offsets k * kResT are immediates)
+        double* const pub0 = halo_row(epoch & 1, ci, 0, 0) + t;
+        double* const pub1 = halo_row(epoch & 1, ci, 1, 0) - last_begin + t;
+        // Two copies of the loop: when the slab's last row lies in the last
+        // kTailSlots slots (full slabs: every CTA of configs 2 and 5) only those
+        // slots carry the last-row test.
+        auto phase2 = [&](auto tailc) {
+          constexpr bool TAIL = decltype(tailc)::value;
+  #pragma unroll
+          for (int k0 = 0; k0 < PT; k0 += kCh) {
+  #pragma unroll
+            for (int k = k0; k < k0 + kCh; ++k) {
+              // branch-free: q of points outside the system is forced to 0, so
+              // every dot term of such a point is an exact zero (r = p = 0 there)
+              const int j = t + k * kResT;
+              const double qa = res_product<LAP>(P, off + j, pitch, u);
+              const double qq = (act >> k & 1u) ? qa : 0.0;
+              const double pv = P[off + j];  // finite; its term is 0 where qq is masked
+              q[k] = qq;
+              if constexpr (kFusePub) {  // boundary rows for the neighbours' ghosts
+                // first row: slots below kFirstSlots only (pitch <= kFirstSlots * kResT,
+                // host plan).  (A per-thread slot mask for the last row instead of the
+                // two compares spilled the 48-point kernel: local 1.45 -> 1.62 s.)
+                if (k < kFirstSlots) {  // (folded: the loop is fully unrolled)
+                  if (j < first_end) __stcg(pub0 + k * kResT, qq);
+                }
+                if (!TAIL || k >= PT - kTailSlots) {  // (folded)
+                  if (j >= lb_pub && j < npts) __stcg(pub1 + k * kResT, qq);
+                }
+              }
+              acc[0] += r[k] * r[k];
+              acc[2] += pv * qq;
+              if constexpr (LAP) {  // D^-1 = 1/4: the z terms are exact quarters (below)
+                acc[1] += qq * r[k];
+                acc[4] += qq * qq;
+              } else {
+                const double tz = __dmul_rn(dv, r[k]);
+                acc[1] += r[k] * tz;
+                acc[3] += qq * tz;
+                acc[4] += qq * __dmul_rn(dv, qq);
+              }
             }
+            sched_fence();
           }
-          sched_fence();
-        }
+        };
+        if (last_in_tail)
+          phase2(std::true_type{});
+        else
+          phase2(std::false_type{});
         if constexpr (LAP) {
           // z = r / 4 exactly, so r.z = (r.r)/4, q.z = (q.r)/4, q.D^-1q = (q.q)/4
           // term by term (power-of-two scaling commutes with every rounding of
@@ -525,9 +576,9 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
         __syncthreads();
         // (rolled loop through the CTA's scratch row: no register arrays live
         // in this rarely taken branch)
-        double* rt = bs + static_cast<long long>(gridDim.x) * kResCap;  // 2nd half of bslab
+        double* rt = bs + static_cast<long long>(gridDim.x) * kCap;  // 2nd half of bslab
 #pragma unroll 1
-        for (int k = 0; k < kResPT; ++k) {
+        for (int k = 0; k < PT; ++k) {
           const int j = t + k * kResT;
           if (act >> k & 1u) {
             const double ax = res_product<LAP>(P, off + j, pitch, u);
@@ -537,7 +588,7 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
           }
         }
 #pragma unroll
-        for (int k = 0; k < kResPT; ++k) {
+        for (int k = 0; k < PT; ++k) {
           const int j = t + k * kResT;
           r[k] = (act >> k & 1u) ? rt[j] : 0.0;
           q[k] = 0.0;
@@ -547,10 +598,11 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
       // normal iterations publish q; a true-residual check publishes the new
       // r, which re-seeds the neighbours' ghost rows at the restart
       if constexpr (kGhostR) {
-        if (s_ctl.mode == kModeNormal)
-          publish(q, epoch & 1, 0);
-        else
+        if (s_ctl.mode == kModeNormal) {
+          if constexpr (!kFusePub) publish(q, epoch & 1, 0);
+        } else {
           publish(r, epoch & 1, 0);
+        }
       } else {
         publish(r, epoch & 1, 0);
         publish(q, epoch & 1, 1);
@@ -587,20 +639,41 @@ __global__ void __launch_bounds__(kResT, kResPerSM) k_cg_resident(ResArgs A) {
   if (A.trace != nullptr && t < 16) A.trace[blockIdx.x * 16 + t] = s_tr[t];
 }
 
+constexpr int kResNVar = static_cast<int>(sizeof(kResVariants) / sizeof(kResVariants[0]));
+template <int V>
+const void* res_kernel_v(bool lap) {
+  return lap ? reinterpret_cast<const void*>(&k_cg_resident<true, kResVariants[V]>)
+             : reinterpret_cast<const void*>(&k_cg_resident<false, kResVariants[V]>);
+}
+const void* res_kernel(int v, bool lap) {
+  static_assert(kResNVar == 5, "one case per instantiated capacity");
+  switch (v) {
+    case 0: return res_kernel_v<0>(lap);
+    case 1: return res_kernel_v<1>(lap);
+    case 2: return res_kernel_v<2>(lap);
+    case 3: return res_kernel_v<3>(lap);
+    default: return res_kernel_v<4>(lap);
+  }
+}
+
 }  // namespace
 
-// Host plan: CTAs per lane C and the system -> lane assignment.  Every system
-// must fit: ceil(h / C) rows x pitch points per CTA (<= kResCap) plus the
-// shared buffers (p with ghost rows, x).  Among the feasible C the plan with
-// the smallest estimated makespan wins: a lane's time is the sum over its
-// systems of iterations (~ proportional to the window's larger side) x
-// per-iteration cost (a fixed barrier/reduction latency + the slab's points).
+// Host plan: CTAs per lane C, the kernel instantiation (points per thread) and
+// the system -> lane assignment.  Every system must fit: ceil(h / C) rows x
+// pitch points per CTA within the instantiation's capacity, plus the shared
+// buffers (p with ghost rows, x); each C runs the smallest instantiation that
+// fits.  Among the feasible plans the smallest estimated makespan wins: a
+// lane's time is the sum over its systems of iterations (~ proportional to the
+// window's larger side) x per-iteration cost (the lane exchange + the point
+// loops' slots).
 bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   static const int env = [] {
     const char* e = std::getenv("MLG_CG_RESIDENT");  // A/B hook: 0 disables
     return e ? std::atoi(e) : 1;
   }();
   if (!env || L->uniform == 0 || sys_h.empty()) return false;
+  for (const CgSys& s : sys_h)  // (fused publish: the first row lies in the first slots)
+    if (s.pitch > kFirstSlots * kResT) return false;
   int dev = 0, nsm = 0, smem_optin = 0;
   MLG_CUDA(cudaGetDevice(&dev));
   MLG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -612,10 +685,14 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   const int slots = nsm * kResPerSM;  // co-resident CTAs of the cooperative launch
   // static shared memory of the kernel (s_red, s_sum, s_ctl, trace slots)
   const int static_smem = [] {
-    cudaFuncAttributes fa{}, fb{};
-    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(&k_cg_resident<true>));
-    cudaFuncGetAttributes(&fb, reinterpret_cast<const void*>(&k_cg_resident<false>));
-    return static_cast<int>(std::max(fa.sharedSizeBytes, fb.sharedSizeBytes)) + 64;
+    std::size_t m = 0;
+    for (int v = 0; v < kResNVar; ++v)
+      for (int lap = 0; lap < 2; ++lap) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, res_kernel(v, lap != 0));
+        m = std::max(m, fa.sharedSizeBytes);
+      }
+    return static_cast<int>(m) + 64;
   }();
   const int nsys = static_cast<int>(sys_h.size());
   int max_pitch = 1, max_h = 1;
@@ -623,41 +700,41 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
     max_pitch = std::max(max_pitch, s.pitch);
     max_h = std::max(max_h, s.h);
   }
-  auto smem_for = [&](int C) {
-    long long worst = 0;
-    for (const CgSys& s : sys_h) {
-      const long long R = (s.h + C - 1) / C;
-      worst = std::max(worst, (2LL * kResCap + (kGhostR ? 4 : 2) * s.pitch + 4) * 8 + 0 * R);
+  auto smem_for = [&](int cap) {  // p with ghost rows, x, ghost r (kernel layout)
+    return (2LL * cap + (kGhostR ? 4 : 2) * max_pitch + 4) * 8;
+  };
+  // smallest instantiated capacity that holds every system's slab with C CTAs per lane
+  auto variant_for = [&](int C) {
+    long long need = 0;
+    for (const CgSys& s : sys_h) need = std::max(need, static_cast<long long>((s.h + C - 1) / C) * s.pitch);
+    int best_v = -1;
+    for (int v = 0; v < kResNVar; ++v) {
+      const long long cap = static_cast<long long>(kResT) * kResVariants[v];
+      if (cap < need || smem_for(static_cast<int>(cap)) + static_smem > smem_cta) continue;
+      if (best_v < 0 || kResVariants[v] < kResVariants[best_v]) best_v = v;
     }
-    return worst;
+    return best_v;
   };
-  auto fits = [&](int C) {
-    for (const CgSys& s : sys_h) {
-      const long long R = (s.h + C - 1) / C;
-      if (R * s.pitch > kResCap) return false;
-    }
-    return smem_for(C) + static_smem <= smem_cta;
-  };
-  // per-iteration cost model (microseconds): barrier + reduction latency plus
-  // the slab's points at ~0.33 ns each (72 B of shared-memory traffic per point)
-  auto iter_cost = [&](const CgSys& s, int C) {
-    const double R = (s.h + C - 1) / C;
-    return 2.0 + R * s.pitch * 0.33e-3;
-  };
+  // per-iteration cost model (microseconds), from the cycle traces of configs 2
+  // and 5 (profiles/r2D_resident_trace_c2.txt, r2E_resident_trace_c5.txt): the
+  // lane exchange (L2 round trips + the fixed per-iteration work, growing slowly
+  // with the lane width) plus ~200 cycles per register slot of the point loops
+  auto iter_cost = [&](int C, int pt) { return 2.95 + 0.006 * C + 0.100 * pt; };
   double best = 1e300;
-  int bestC = 0;
+  int bestC = 0, bestV = -1;
   std::vector<std::vector<int>> best_lanes;
   std::vector<int> order(static_cast<std::size_t>(nsys));
   std::iota(order.begin(), order.end(), 0);
   for (int C = 1; C <= slots; ++C) {
-    if (!fits(C)) continue;
+    const int var = variant_for(C);
+    if (var < 0) continue;
     const int nl = slots / C;
     if (nl < 1) break;
     // LPT: systems by decreasing cost to the least-loaded lane
     std::vector<double> cost(static_cast<std::size_t>(nsys));
     for (int s = 0; s < nsys; ++s) {
       const CgSys& S = sys_h[static_cast<std::size_t>(s)];
-      cost[static_cast<std::size_t>(s)] = std::max(S.w, S.h) * iter_cost(S, C);
+      cost[static_cast<std::size_t>(s)] = std::max(S.w, S.h) * iter_cost(C, kResVariants[var]);
     }
     std::vector<int> ord = order;
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
@@ -675,6 +752,7 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
     if (span < best * 0.999) {
       best = span;
       bestC = C;
+      bestV = var;
       best_lanes = lanes;
     }
   }
@@ -695,7 +773,8 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   res_bar.zero(st);
   res_part.ensure(static_cast<std::size_t>(nl) * 2 * kCgDots * part_cpad(C));
   res_halo.ensure(static_cast<std::size_t>(nl) * 2 * C * 2 * kHaloFields * max_pitch);
-  res_bslab.ensure(static_cast<std::size_t>(2) * nl * C * kResCap);
+  const int cap = kResT * kResVariants[bestV];
+  res_bslab.ensure(static_cast<std::size_t>(2) * nl * C * cap);
   ctl_d.zero(st);
 
   ResArgs A{};
@@ -729,9 +808,8 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
   const bool lap = L->ust.c == 4.0 && L->ust.e == -1.0 && L->ust.n == -1.0 &&
                    L->ust.ne == 0.0 && L->udinv == 0.25 &&
                    std::getenv("MLG_CG_NOLAP") == nullptr;  // (test hook: generic stencil)
-  const void* fn = lap ? reinterpret_cast<const void*>(&k_cg_resident<true>)
-                       : reinterpret_cast<const void*>(&k_cg_resident<false>);
-  const int dyn = static_cast<int>(smem_for(C));
+  const void* fn = res_kernel(bestV, lap);
+  const int dyn = static_cast<int>(smem_for(cap));
   MLG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
   int per_sm = 0;
   MLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kResT, dyn));
@@ -766,9 +844,9 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
     static const char* names[] = {"phase1", "ghost+sync", "phase2", "publish", "warp trees+sync",
                                   "block sums+arrive+wait", "lane sums+sync", "(-)", "ctl",
                                   "(unused)"};
-    fprintf(stderr, "resident trace: %d lanes x %d CTAs, %d systems, %s, %.0f iterations/CTA; "
+    fprintf(stderr, "resident trace: %d lanes x %d CTAs x %d points/thread, %d systems, %s, %.0f iterations/CTA; "
             "cycles per iteration (thread 0), mean over CTAs (max over CTAs of the per-CTA mean):",
-            nl, C, nsys, mask ? "strip" : "local", it);
+            nl, C, kResVariants[bestV], nsys, mask ? "strip" : "local", it);
     double tot = 0.0;
     for (int k = 0; k < 10; ++k) {
       fprintf(stderr, " %s %.0f (%.0f),", names[k], sum[order[k]] / (nl * C) / it,

@@ -24,8 +24,10 @@ GOLDEN = json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())
 CASES = ["small_L3_nev3", "unit8_L3_m4_nev4", "square_L4_nev5", "unit8_L4_m4_nev1"]
 VARIANTS = {
     "default": {},
-    "multi_launch_registers": {"MLG_CG_PERSIST": "0"},
-    "cp_async_pipeline": {"MLG_CG_ASYNC": "1"},
+    # (MLG_CG_RESIDENT=0: without it the resident kernel takes every constant-stencil
+    # batch the persistent kernel does not)
+    "multi_launch_registers": {"MLG_CG_PERSIST": "0", "MLG_CG_RESIDENT": "0"},
+    "cp_async_pipeline": {"MLG_CG_ASYNC": "1", "MLG_CG_RESIDENT": "0"},
     "general_stencil": {"MLG_GENERAL_STENCIL": "1"},
     "general_stencil_multi_launch": {"MLG_GENERAL_STENCIL": "1", "MLG_CG_PERSIST": "0"},
     "general_stencil_flagged_only": {"MLG_GENERAL_STENCIL": "1", "MLG_CG_MINROWS": "4",
@@ -33,7 +35,7 @@ VARIANTS = {
     "generic_uniform_stencil": {"MLG_CG_NOLAP": "1"},
     "short_tasks": {"MLG_CG_MINROWS": "4", "MLG_CG_MAXROWS": "8"},
     # k_cg_resident for every constant-stencil batch that fits on chip (by
-    # default only batches beyond L2 take it: config 3 and config 5 sizes)
+    # default only batches beyond L2 or of >= 256 k pooled rows take it)
     "sm_resident": {"MLG_CG_RESIDENT": "2"},
     "sm_resident_generic_stencil": {"MLG_CG_RESIDENT": "2", "MLG_CG_NOLAP": "1"},
 }
@@ -87,6 +89,12 @@ def test_cg_path_matches_golden_eigenvalues(variant):
         assert all(2 in [k[0] for k in g["kernels"]] for g in got.values()), \
             {n: g["kernels"] for n, g in got.items()}
         assert any(2 in [k[1] for k in g["kernels"]] for g in got.values())  # masked strip too
+    if variant in ("multi_launch_registers", "cp_async_pipeline"):  # 0 = k_cg_iter
+        assert all(k == [0, 0] for g in got.values() for k in g["kernels"]), \
+            {n: g["kernels"] for n, g in got.items()}
+    if variant == "default":  # small batches stay off the resident kernel (2)
+        assert all(2 not in k for g in got.values() for k in g["kernels"]), \
+            {n: g["kernels"] for n, g in got.items()}
     for name, g in got.items():
         lams = g["lam"]
         ref = _golden(name)
