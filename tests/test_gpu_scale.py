@@ -64,10 +64,15 @@ def test_multilevel_eigenvalues_match_reference_at_scale(mlg, name):
     cfg = mlg.RunConfig(domain=mlg.DomainRect(*c["domain"]), H=c["H"], delta=c["delta"],
                         m=c["m"], n_levels=c["n_levels"], nev=c["nev"])
     with mlg.Hierarchy(cfg) as hy:
-        lam, pairs, matched, _ = mlg.multilevel_correction(hy)
+        lam, pairs, matched, times = mlg.multilevel_correction(hy)
     ref = np.array(g["lambdas"])
     assert np.max(np.abs(lam - ref) / ref) <= 1e-10
     assert list(matched) == g["matched"]
+    # kernel choice at BASELINE sizes (2 = k_cg_resident, cg.cu CgBatch::solve): the
+    # last level's local solves run SM-resident, and so does config 2's strip solve
+    assert int(times[-1].local_kernel) == 2, [int(t.local_kernel) for t in times]
+    if name.startswith("c2sub"):
+        assert int(times[-1].strip_kernel) == 2, [int(t.strip_kernel) for t in times]
     # eigenfunctions of isolated eigenvalues: seeded projections (size-independent pin)
     vecs = np.stack([p.coeffs for p in pairs])
     proj, rn = projections(vecs)
