@@ -1830,12 +1830,31 @@ CgResult CgBatch::solve(Ctx& c, double tol, int maxit_override) {
     CgResult rr;
     if (solve_resident(c, tol, rr)) return rr;
   }
+  static const bool lpt_env = [] {
+    const char* e = std::getenv("MLG_CG_LPT");  // A/B hook: 0 keeps the system-major order
+    return e ? std::atoi(e) != 0 : true;
+  }();
   std::vector<CgTile> tiles;
   auto rebuild = [&](const std::vector<char>& active) {
     tiles.clear();
     for (int s = 0; s < nsys; ++s)
       if (active[s])
         for (int t = 0; t < sys_h[s].ntiles; ++t) tiles.push_back({s, t});
+    if (lpt_env && !use_persist && !use_async) {
+      // per-iteration launches of the register pipeline (general-stencil batches):
+      // the block scheduler hands tiles out in order, so the costly ones (window
+      // edges, G_j borders: flagged sweeps) go first and the short ones last -- a
+      // shorter drain at the end of every launch (config 4 local 346 -> 336 ms).
+      // Stable: full interior tiles keep their order.  The HBM-streaming cp.async
+      // batches keep the system-major order: there the sort separates vertically
+      // adjacent tiles, whose halo rows then miss L2 (config 5 strip 1.00 -> 1.08 s).
+      std::vector<std::pair<double, CgTile>> keyed;
+      keyed.reserve(tiles.size());
+      for (const CgTile& t : tiles) keyed.emplace_back(tile_cost(t, tmap_h), t);
+      std::stable_sort(keyed.begin(), keyed.end(),
+                       [](const auto& a, const auto& b) { return a.first > b.first; });
+      for (std::size_t i = 0; i < tiles.size(); ++i) tiles[i] = keyed[i].second;
+    }
     tiles_d.upload(tiles.data(), tiles.size(), c.stream);
   };
   std::vector<char> active(nsys, 1);
