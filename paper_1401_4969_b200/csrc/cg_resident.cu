@@ -716,7 +716,7 @@ bool CgBatch::solve_resident(Ctx& c, double tol, CgResult& res) {
     return best_v;
   };
   // per-iteration cost model (microseconds), from the cycle traces of configs 2
-  // and 5 (profiles/r2D_resident_trace_c2.txt, r2E_resident_trace_c5.txt): the
+  // and 5 (profiles/r2E_resident_trace_c2.txt, r2E_resident_trace_c5.txt): the
   // lane exchange (L2 round trips + the fixed per-iteration work, growing slowly
   // with the lane width) plus ~200 cycles per register slot of the point loops
   auto iter_cost = [&](int C, int pt) { return 2.95 + 0.006 * C + 0.100 * pt; };

@@ -1,6 +1,6 @@
 # tile height of the config-5 strip solve (MLG_CG_STRIP_ROWS) against the automatic choice
 mkdir -p gpurun_out
-for r in 0 32 48 64 80 96 128; do
+for r in ${ROWS:-0 32 48 64 80 96 128}; do
   MLG_CG_STRIP_ROWS=$r python bench.py --workload c5 --steps 2 --warmup 1 --no-extras --no-cpu-baseline > gpurun_out/abrows_$r.json 2> gpurun_out/abrows_$r.err
   python -c "
 import json; d=json.loads(open('gpurun_out/abrows_$r.json').read().strip().splitlines()[-1])
